@@ -1,0 +1,364 @@
+#!/usr/bin/env python3
+"""Throughput of the fused mover + deposit step (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (config 2 of BASELINE.json, per GPU; weak scaling for N > 1):
+  nc = 100,000 cells per GPU, ppc0 = 100 per species, species e-, D+, D
+  (desk.toml mix: D neutral with transverse position), fp64, E = 0 field
+  (Table-1 case, field solve off), 30M particles per GPU, device-initialised
+  with the reference splitmix64 streams (synthetic plasma).
+A "step" = one deposit epilogue + one fused mover/deposit launch (+ the
+periodic cell sort when due).  Inputs are 1.12 GB/step per GPU, ~9x the
+126 MB L2, so no L2 flush is needed between steps.
+
+The JSON line carries: value (pushes/s, whole job, device-timed, max over
+ranks), roofline (push kernel: algorithmic bytes / CUDA-event duration vs the
+measured HBM copy peak), cpu_baseline (the reference's own compiled kernels on
+this host's cores, bounded sample), e2e (public step API with per-step host
+E-field upload and rho download), clocks (nvidia-smi during the timed region).
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NC_PER_GPU = 100_000
+PPC0 = 100
+SEED = 20260819
+# Algorithmic reference-state bytes per push.
+ALG_BYTES = {"kick": 32.0, "kick_yp": 56.0, "drift": 24.0, "drift_yp": 48.0, "boris": 64.0, "boris_yp": 80.0}
+METRIC = "particle-pushes/sec (mover+deposit) at 1/2/4/8 B200; % of HBM roofline"
+
+
+def desk_species():
+    from paper_2404_10270_b200 import SpeciesDef
+    from paper_2404_10270_b200.core import ELECTRON_MASS, ELEMENTARY_CHARGE
+
+    # pkg/configs/desk.toml:22-43
+    return [
+        SpeciesDef("e", -ELEMENTARY_CHARGE, ELECTRON_MASS),
+        SpeciesDef("D+", ELEMENTARY_CHARGE, 3.3435837483066354e-27),
+        SpeciesDef("D", 0.0, 3.344494686676785e-27, track_transverse=True),
+    ]
+
+
+def make_config(nc_total, sort_every):
+    from paper_2404_10270_b200 import Grid1D, PhysicalConstants, RunConfig
+
+    return RunConfig(
+        grid=Grid1D.from_cells(nc_total, nc_total * 1e-5), consts=PhysicalConstants(dt_s=4e-14),
+        species=desk_species(), temperatures_ev=[20.0, 20.0, 1.0], densities_m3=[1e21] * 3,
+        ppc0=PPC0, n_steps=0, seed=SEED, field_solve=False, smoothing_passes=0,
+        max_store_mb=1 << 20, sort_every=sort_every,
+    )
+
+
+def species_alg_bytes(sp):
+    if not sp.active_mover:
+        return 0.0
+    key = "kick" if sp.charged else "drift"
+    return ALG_BYTES[key + ("_yp" if sp.track_transverse else "")]
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def committed_traffic():
+    """dram bytes per push launch from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "push_deposit_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the reference's own compiled kernels (oracle/_ref, built from
+# /root/reference sources) timed on this host's cores.
+def cpu_reference_rate(target_seconds=15.0, nc=20_000, ppc=PPC0, threads=None, log=None):
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle
+
+    mod = oracle.ref_kernels()
+    kind = "reference"
+    if mod is None:
+        mod, kind = oracle, "port"
+    threads = threads or os.cpu_count() or 1
+    cap = int(np.ceil(1.5 * ppc))  # reference slack (config.py:55, core.py:305)
+    rng = np.random.default_rng(SEED)
+    offs = np.arange(nc, dtype=np.int64) * cap
+    counts = np.full(nc, ppc, dtype=np.int64)
+    total = nc * cap
+    sig = [7.502e-3, 1.238e-4, 2.768e-5]
+    stores = []
+    live = (np.arange(nc)[:, None] * cap + np.arange(ppc)[None, :]).ravel()
+    for k in range(3):
+        d = {f: np.zeros(total) for f in ("x", "vx", "vy", "vz")}
+        d["x"][live] = rng.random(live.size)
+        for f in ("vx", "vy", "vz"):
+            d[f][live] = sig[k] * rng.standard_normal(live.size)
+        if k == 2:
+            d["yp"] = np.zeros(total)
+        stores.append(d)
+    accel = np.full(nc + 1, -0.0)  # coef * E with E = 0 (mover.py:221)
+    block = max(1, nc // (threads * 4))
+    blocks = [(b, min(b + block, nc)) for b in range(0, nc, block)]
+
+    def move(args):
+        k, lo, hi = args
+        d = stores[k]
+        a = accel[lo:hi + 1] if k < 2 else None
+        mod.fused_move(a, d["x"], d["vx"], d["vy"], d.get("yp"), offs[lo:hi], counts[lo:hi], 1.0)
+
+    def dep(args):
+        k, lo, hi = args
+        mod.deposit_partials(stores[k]["x"], offs[lo:hi], counts[lo:hi])
+
+    tasks_m = [(k, lo, hi) for k in range(3) for lo, hi in blocks]
+    tasks_d = [(k, lo, hi) for k in range(2) for lo, hi in blocks]
+    pushes = 3 * nc * ppc
+    with ThreadPoolExecutor(threads) as pool:
+        list(pool.map(move, tasks_m))
+        list(pool.map(dep, tasks_d))
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            list(pool.map(move, tasks_m))
+            list(pool.map(dep, tasks_d))
+            reps += 1
+            el = time.perf_counter() - t0
+            if el >= target_seconds or reps >= 200:
+                break
+    rate = pushes * reps / el
+    sample = (f"{reps} steps x {pushes / 1e6:.1f}M pushes (e-, D+, D desk mix, nc={nc}, ppc={ppc}, cap={cap}) "
+              f"fused_move + deposit_partials over {len(blocks)} cell blocks on a {threads}-thread pool "
+              f"(mover_phase pattern, pkg/src/picmc/mover.py:227-271); {el:.1f}s")
+    return {"value": rate, "unit": "particle-pushes/s", "cores": threads, "kind": kind, "sample": sample}
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2404_10270_b200 import Engine
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    nc_total = NC_PER_GPU * world
+    cfg = make_config(nc_total, args.sort_every)
+    eng = Engine(cfg, device=dev, rank=rank, world=world, group=None, init="device", check_every=0)
+    torch.cuda.synchronize(dev)
+    pushes_rank = sum(s.n for s in eng.sp if s.kind != 0)
+    alg_bytes = sum(s.n * species_alg_bytes(s.sp) for s in eng.sp)
+
+    for _ in range(args.warmup):
+        eng.step()
+    eng.sync()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    eng.phase_events.clear()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        time.sleep(0.3)
+        start.record(eng.stream)
+        for _ in range(args.steps):
+            eng.step(timed=True)
+        end.record(eng.stream)
+        torch.cuda.synchronize(dev)
+    eng.sync()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end) / args.steps
+    mover_ms = [ev[2].elapsed_time(ev[3]) for ev in eng.phase_events]
+    push_ms = float(np.mean(mover_ms))
+    if world > 1:
+        t = torch.tensor([ms, push_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, push_ms = float(t[0]), float(t[1])
+    value = pushes_rank * world / (ms * 1e-3)
+
+    # e2e: the public step API driven from the host, per step: H2D of an
+    # E-field array from pinned memory, the step, D2H of rho + live totals.
+    nodes = nc_total + 1
+    e_host = torch.zeros(nodes, dtype=torch.float64).pin_memory()
+    rho_host = torch.empty(nodes, dtype=torch.float64).pin_memory()
+    e2e_steps = max(3, args.steps // 2)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(eng.stream)
+    for _ in range(e2e_steps):
+        with torch.cuda.stream(eng.stream):
+            eng.e.copy_(e_host, non_blocking=True)
+        rho, _ = eng.step()
+        with torch.cuda.stream(eng.stream):
+            rho_host.copy_(rho, non_blocking=True)
+        eng.stream.synchronize()
+        _ = float(rho_host[0])
+    t1.record(eng.stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = t0.elapsed_time(t1) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t[0])
+    e2e_value = pushes_rank * world / (e2e_ms * 1e-3)
+
+    peak, peak_kind = measured_peak()
+    achieved = alg_bytes / (push_ms * 1e-3) / 1e9
+    traffic = committed_traffic()
+    launches_per_step = 2 + (0 if not args.sort_every else 0)
+    n_sorts = (args.steps // args.sort_every) if args.sort_every else 0
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "particle-pushes/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (device init_plasma with the reference splitmix64 streams, seed 20260819)",
+        "config": {
+            "workload": "config 2: 1D3V unmagnetized, desk species e-/D+/D(yp), E=0 (field solve off)",
+            "nc_per_gpu": NC_PER_GPU, "nc_total": nc_total, "ppc0_per_species": PPC0,
+            "particles_per_gpu": pushes_rank, "particles_total": pushes_rank * world,
+            "sort_every": args.sort_every, "parallelism": f"particle shards x{world}, replicated grid",
+            "l2": "inputs 1.12 GB/GPU >> 126 MB L2; no flush needed",
+        },
+        "roofline": {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "peak_source": peak_kind, "kernel": "k_push_deposit",
+            "alg_bytes_per_launch": alg_bytes, "push_ms": push_ms,
+            "traffic": None if traffic is None else traffic.get("dram_bytes_per_launch"),
+        },
+        "e2e": {"value": e2e_value, "unit": "particle-pushes/s", "h2d_bytes_per_step": nodes * 8,
+                "d2h_bytes_per_step": nodes * 8,
+                "path": "Engine.step() public API: E-field H2D (pinned) + step + rho D2H, synced per step"},
+        "gpu_launches": args.steps * launches_per_step + n_sorts * 4,
+    }
+    return out, clk.summary()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sort-every", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cpu = cpu_reference_rate(target_seconds=max(2.0, args.cpu_seconds))
+        line = {
+            "impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": cpu["unit"],
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "config 2 shape (sampled on host)"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": cpu["value"], "unit": cpu["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out, clocks = run_ours(args, rank, world, local_rank)
+    out["clocks"] = clocks
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_reference_rate(target_seconds=args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

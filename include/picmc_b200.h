@@ -1,0 +1,183 @@
+/*
+ * picmc_b200.h -- C ABI of the B200-native particle mover + charge deposition.
+ *
+ * The reference's operator boundary for this hot path is the Python module
+ * `picmc.backends` (/root/reference/pkg/src/picmc/backends/__init__.py:45-50),
+ * whose compiled twin is pkg/src/picmc/backends/_kernels.pyx.  Every entry
+ * point below is plain C: device pointers, sizes, a cudaStream_t passed as
+ * `void*`, and an int status.  Nothing is thrown across the ABI; the detail of
+ * the last failure on the calling thread is in pb_last_error().
+ *
+ * Status codes map onto the reference exception hierarchy
+ * (pkg/src/picmc/errors.py:4-25) in the Python wrapper:
+ *   PB_ERR_INVALID  -> ValueError      (Cython buffer / argument checks)
+ *   PB_ERR_CFL      -> CflViolation    (pkg/src/picmc/mover.py:142-148)
+ *   PB_ERR_CONTRACT -> ContractViolation (pkg/src/picmc/core.py:256-264)
+ *   PB_ERR_OVERFLOW -> EngineError     (fixed-point deposit bin overflow)
+ *   PB_ERR_CUDA     -> RuntimeError    (CUDA runtime failure)
+ *
+ * All arrays are device memory unless stated otherwise.  Particle state is
+ * fp64 and cell-relative ([0,1) in units of dx) exactly as in the reference
+ * store (pkg/src/picmc/core.py:108-109); the engine layout is a flat
+ * structure of arrays with an int32 cell index per particle instead of the
+ * reference's per-cell slack segments.
+ */
+#ifndef PICMC_B200_H
+#define PICMC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PB_ABI_VERSION 1
+
+#define PB_OK 0
+#define PB_ERR_INVALID 1
+#define PB_ERR_CUDA 2
+#define PB_ERR_CFL 3
+#define PB_ERR_CONTRACT 4
+#define PB_ERR_OVERFLOW 5
+
+/* Species kinds: which arithmetic the mover applies (SpeciesDef flags,
+ * pkg/src/picmc/core.py:53-81, and accel_nodes_for_species,
+ * pkg/src/picmc/mover.py:211-224). */
+#define PB_KIND_INACTIVE 0 /* active_mover == False: not pushed            */
+#define PB_KIND_DRIFT 1    /* uncharged: x += nstep*vx, no kick (keeps -0.0) */
+#define PB_KIND_KICK 2     /* charged: one-sided gather, vx += a, drift      */
+#define PB_KIND_BORIS 3    /* charged + uniform B: Boris rotation (config 4) */
+
+/* Particle boundary: the reference always wraps (mover.py:156); absorbing
+ * walls are the config-3 extension restated in oracle/ and DESIGN.md. */
+#define PB_BC_PERIODIC 0
+#define PB_BC_ABSORBING 1
+
+/* Field boundary for the density stitch (fields.py:81-92, :115-117). */
+#define PB_FIELD_PERIODIC 0
+#define PB_FIELD_DIRICHLET 1
+
+#define PB_MAX_SPECIES 8
+
+/* Fixed-point deposit: each particle adds round(x * 2^48) to R and 1 to the
+ * cell count C; L = C*2^48 - R.  Integer sums are exact and associative, so
+ * the density is bitwise independent of thread order and GPU count. */
+#define PB_DEPOSIT_FRAC_BITS 48
+
+typedef struct pb_species {
+  double *x, *vx, *vy, *vz; /* SoA particle state, n_cap slots           */
+  double *yp;               /* transverse position or NULL (sn2d)         */
+  int32_t *cell;            /* owning cell of every live slot             */
+  int64_t *n_dev;           /* device live count (absorbing) or NULL      */
+  int64_t n;                /* host live count / upper bound of n_dev     */
+  int64_t *holes;           /* absorbing: scratch list of removed slots   */
+  int32_t kind;             /* PB_KIND_*                                  */
+  int32_t deposit;          /* deposit bin slot, -1 for neutral species   */
+  double fnstep;            /* float(nstep) (mover.py:248)                */
+  double kick_coef;         /* q dt^2/(m dx), velocity_kick_coef (mover.py:38-40) */
+  double boris_t[3];        /* q B dt / (2 m)                             */
+  double boris_s[3];        /* 2 t / (1 + |t|^2)                          */
+} pb_species;
+
+/* Device-resident step status, read by the host at the step's sync point. */
+typedef struct pb_status {
+  int32_t code;             /* PB_OK or first error code                 */
+  int32_t cfl_species;      /* species of the CFL offender               */
+  uint64_t cfl_index;       /* smallest offending slot (atomicMin)       */
+  int64_t moved[PB_MAX_SPECIES];        /* cell transfers this step     */
+  int64_t absorbed[PB_MAX_SPECIES][2];  /* [left wall, right wall]      */
+  int64_t n_holes[PB_MAX_SPECIES];      /* absorbed slots to compact    */
+  int64_t overflow;                     /* deposit bins over capacity   */
+} pb_status;
+
+/* ---- library ------------------------------------------------------------ */
+int pb_abi_version(void);
+const char *pb_last_error(void);
+int pb_device_sm_count(int *out);
+
+/* ---- parity shims with the reference kernel signatures (packed layout) --
+ * offs/counts address per-cell segments of packed arrays exactly as
+ * CellSortedStore does (pkg/src/picmc/core.py:100-132). */
+
+/* fused_move (pkg/src/picmc/backends/_kernels.pyx:60-102): in place.
+ * accel_or_null has nc+1 entries; NULL skips the kick entirely. */
+int pb_fused_move(const double *accel_or_null, double *x, double *vx,
+                  const double *vy, double *yp_or_null, const int64_t *offs,
+                  const int64_t *counts, int64_t nc, double fnstep,
+                  void *stream);
+
+/* deposit_partials (_kernels.pyx:14-34): L[j]=sum(1-x), R[j]=sum(x) in slot
+ * order -- sequential per cell, bitwise equal to the reference. */
+int pb_deposit_partials(const double *x, const int64_t *offs,
+                        const int64_t *counts, int64_t nc, double *left,
+                        double *right, void *stream);
+
+/* gather (_kernels.pyx:37-57): out[k] = a[j] + x*(a[j+1]-a[j]) in live
+ * (cell-major) order; out has sum(counts) entries. */
+int pb_gather(const double *nodes, const double *x, const int64_t *offs,
+              const int64_t *counts, int64_t nc, double *out, void *stream);
+
+/* ---- device-resident engine (flat SoA + cell index) ---------------------- */
+
+/* One mover step for `nsp` species, fused: gather E, kick (or Boris), drift,
+ * cell transfer with the reference floor/carry/mod rules
+ * (pkg/src/picmc/mover.py:136-163), absorbing-wall removal, and the
+ * fixed-point deposit of the post-move positions into `bins`
+ * ([ndep][2][nc] uint64: R then C).  e_nodes has nc+1 entries (required for
+ * KICK/BORIS species).  Errors are recorded in *status (device). */
+int pb_push_deposit(const pb_species *sp, int nsp, const double *e_nodes,
+                    int64_t nc, int particle_bc, uint64_t *bins,
+                    pb_status *status, void *stream);
+
+/* Standalone fixed-point deposit of current positions (step-0 deposit and
+ * inactive charged species). */
+int pb_deposit_only(const pb_species *sp, int nsp, int64_t nc, uint64_t *bins,
+                    pb_status *status, void *stream);
+
+/* Weighted partials and stitched density from fixed-point bins:
+ * left = sum_s coef_s * L_s, right likewise, in species order
+ * (pkg/src/picmc/fields.py:67-77), rho per stitch_rho/deposit_charge
+ * (fields.py:81-92, :115-117).  coef is a host array of ndep doubles. */
+int pb_rho_epilogue(const uint64_t *bins, const double *coef, int ndep,
+                    int64_t nc, int field_bc, double *left, double *right,
+                    double *rho, void *stream);
+
+/* Fill the holes left by absorbed particles from the tail (warp-ballot
+ * stream compaction); updates *n_dev.  `scratch` needs
+ * pb_compact_scratch_bytes(n) bytes. */
+size_t pb_compact_scratch_bytes(int64_t n);
+int pb_compact(const pb_species *sp, int nsp, pb_status *status,
+               void *scratch, size_t scratch_bytes, void *stream);
+
+/* Periodic sort by cell: stable radix sort of (cell, slot) then a gather
+ * permutation of every field into the `dst` species buffers (ping-pong).
+ * `scratch` needs pb_sort_scratch_bytes(n, nc) bytes. */
+size_t pb_sort_scratch_bytes(int64_t n, int64_t nc);
+int pb_sort_by_cell(const pb_species *src, const pb_species *dst, int64_t nc,
+                    void *scratch, size_t scratch_bytes, void *stream);
+
+/* Field pipeline (replicated on every GPU; config 3/4 and field_solve runs).
+ * smooth_density (fields.py:121-135), solve_poisson (fields.py:156-202),
+ * compute_efield (fields.py:205-218).  `scratch` needs
+ * pb_field_scratch_bytes(nc) bytes. */
+size_t pb_field_scratch_bytes(int64_t nc);
+int pb_smooth_density(const double *rho, double *out, int64_t nc, int passes,
+                      void *scratch, void *stream);
+int pb_solve_poisson(const double *rho, double *phi, int64_t nc, double dx,
+                     double eps0, int field_bc, double phi_left,
+                     double phi_right, void *scratch, void *stream);
+int pb_compute_efield(const double *phi, double *e, int64_t nc, double dx,
+                      int field_bc, void *stream);
+
+/* Device init_plasma (pkg/src/picmc/core.py:292-352): ppc0 particles per
+ * cell for cells [cell_lo, cell_hi) with the reference splitmix64 streams.
+ * Positions are bit-exact; velocities use CUDA log/sin/cos (ulp-close). */
+int pb_init_species(pb_species *sp, uint64_t species_key, int64_t cell_lo,
+                    int64_t cell_hi, int64_t ppc0, double vstd, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PICMC_B200_H */

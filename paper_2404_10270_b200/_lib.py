@@ -1,0 +1,139 @@
+"""ctypes binding of libpicmc_b200.so (the C ABI in include/picmc_b200.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (nvcc,
+sm_100a).  Loading it never needs a GPU; every compute entry point does, and
+there is deliberately no CPU fallback: a missing library or device raises.
+"""
+
+import ctypes
+import os
+import threading
+
+from .errors import CflViolation, ContractViolation, EngineError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpicmc_b200.so")
+
+PB_OK = 0
+PB_ERR_INVALID = 1
+PB_ERR_CUDA = 2
+PB_ERR_CFL = 3
+PB_ERR_CONTRACT = 4
+PB_ERR_OVERFLOW = 5
+
+PB_KIND_INACTIVE = 0
+PB_KIND_DRIFT = 1
+PB_KIND_KICK = 2
+PB_KIND_BORIS = 3
+
+PB_BC_PERIODIC = 0
+PB_BC_ABSORBING = 1
+
+PB_FIELD_PERIODIC = 0
+PB_FIELD_DIRICHLET = 1
+
+PB_MAX_SPECIES = 8
+PB_DEPOSIT_FRAC_BITS = 48
+
+_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_f64 = ctypes.c_double
+
+
+class PbSpecies(ctypes.Structure):
+    _fields_ = [
+        ("x", _p), ("vx", _p), ("vy", _p), ("vz", _p), ("yp", _p),
+        ("cell", _p), ("n_dev", _p), ("n", _i64), ("holes", _p),
+        ("kind", _i32), ("deposit", _i32), ("fnstep", _f64),
+        ("kick_coef", _f64), ("boris_t", _f64 * 3), ("boris_s", _f64 * 3),
+    ]
+
+
+class PbStatus(ctypes.Structure):
+    _fields_ = [
+        ("code", _i32), ("cfl_species", _i32), ("cfl_index", ctypes.c_uint64),
+        ("moved", _i64 * PB_MAX_SPECIES),
+        ("absorbed", (_i64 * 2) * PB_MAX_SPECIES),
+        ("n_holes", _i64 * PB_MAX_SPECIES),
+        ("overflow", _i64),
+    ]
+
+
+STATUS_BYTES = ctypes.sizeof(PbStatus)
+
+# name -> (restype, argtypes); mirrors include/picmc_b200.h one to one.
+_SIGS = {
+    "pb_abi_version": (ctypes.c_int, []),
+    "pb_last_error": (ctypes.c_char_p, []),
+    "pb_device_sm_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+    "pb_fused_move": (ctypes.c_int, [_p, _p, _p, _p, _p, _p, _p, _i64, _f64, _p]),
+    "pb_deposit_partials": (ctypes.c_int, [_p, _p, _p, _i64, _p, _p, _p]),
+    "pb_gather": (ctypes.c_int, [_p, _p, _p, _p, _i64, _p, _p]),
+    "pb_push_deposit": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int, _p,
+                                       _i64, ctypes.c_int, _p, _p, _p]),
+    "pb_deposit_only": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int,
+                                       _i64, _p, _p, _p]),
+    "pb_rho_epilogue": (ctypes.c_int, [_p, ctypes.POINTER(_f64), ctypes.c_int, _i64,
+                                       ctypes.c_int, _p, _p, _p, _p]),
+    "pb_compact_scratch_bytes": (ctypes.c_size_t, [_i64]),
+    "pb_compact": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int, _p, _p,
+                                  ctypes.c_size_t, _p]),
+    "pb_sort_scratch_bytes": (ctypes.c_size_t, [_i64, _i64]),
+    "pb_sort_by_cell": (ctypes.c_int, [ctypes.POINTER(PbSpecies),
+                                       ctypes.POINTER(PbSpecies), _i64, _p,
+                                       ctypes.c_size_t, _p]),
+    "pb_field_scratch_bytes": (ctypes.c_size_t, [_i64]),
+    "pb_smooth_density": (ctypes.c_int, [_p, _p, _i64, ctypes.c_int, _p, _p]),
+    "pb_solve_poisson": (ctypes.c_int, [_p, _p, _i64, _f64, _f64, ctypes.c_int,
+                                        _f64, _f64, _p, _p]),
+    "pb_compute_efield": (ctypes.c_int, [_p, _p, _i64, _f64, ctypes.c_int, _p]),
+    "pb_init_species": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_uint64,
+                                       _i64, _i64, _i64, _f64, _p]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load():
+    """Load and type the library; raises ImportError if it is not built."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} is missing; run __graft_entry__.build() "
+                    "(nvcc sm_100a) first -- there is no CPU fallback"
+                )
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            if lib.pb_abi_version() != 1:
+                raise ImportError("libpicmc_b200 ABI version mismatch")
+            _lib = lib
+    return _lib
+
+
+def exported_names():
+    return tuple(_SIGS)
+
+
+def check(rc: int, what: str = ""):
+    """Map a status code onto the reference exception hierarchy."""
+    if rc == PB_OK:
+        return
+    msg = load().pb_last_error().decode(errors="replace")
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == PB_ERR_INVALID:
+        raise ValueError(msg)
+    if rc == PB_ERR_CFL:
+        raise CflViolation(msg)
+    if rc == PB_ERR_CONTRACT:
+        raise ContractViolation(msg)
+    if rc == PB_ERR_OVERFLOW:
+        raise EngineError(msg)
+    raise RuntimeError(msg)

@@ -1,0 +1,117 @@
+// Library plumbing: error text, version, device queries, and the density
+// epilogue (weighted partials + stitch) that turns fixed-point bins into rho.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace pb {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t err, const char *what) {
+  set_error("%s: %s (%s)", what, cudaGetErrorString(err), cudaGetErrorName(err));
+  return PB_ERR_CUDA;
+}
+
+// left/right per cell: species order, 0.0 + coef*L (fields.py:64-77).
+__device__ __forceinline__ void weighted_partials(const uint64_t *__restrict__ bins,
+                                                  const double *__restrict__ coef,
+                                                  int ndep, int64_t nc, int64_t j,
+                                                  double &left, double &right) {
+  double l = 0.0, r = 0.0;
+  for (int s = 0; s < ndep; ++s) {
+    const uint64_t R = bins[(size_t)s * 2 * nc + j];
+    const uint64_t C = bins[(size_t)s * 2 * nc + nc + j];
+    const uint64_t L = (C << kFracBits) - R;
+    const double lraw = __dmul_rn(__ull2double_rn(L), kFracInv);
+    const double rraw = __dmul_rn(__ull2double_rn(R), kFracInv);
+    l = __dadd_rn(l, __dmul_rn(coef[s], lraw));
+    r = __dadd_rn(r, __dmul_rn(coef[s], rraw));
+  }
+  left = l;
+  right = r;
+}
+
+struct CoefArgs {
+  double c[PB_MAX_SPECIES];
+};
+
+__global__ void k_rho_epilogue(const uint64_t *__restrict__ bins, CoefArgs ca,
+                               int ndep, int64_t nc, int field_bc,
+                               double *__restrict__ left,
+                               double *__restrict__ right,
+                               double *__restrict__ rho) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g > nc) return;
+  double lg = 0.0, rg = 0.0, lp = 0.0, rp = 0.0;
+  if (g < nc) {
+    weighted_partials(bins, ca.c, ndep, nc, g, lg, rg);
+    if (left) left[g] = lg;
+    if (right) right[g] = rg;
+  }
+  if (g > 0) weighted_partials(bins, ca.c, ndep, nc, g - 1, lp, rp);
+  double v;
+  if (g > 0 && g < nc) {
+    v = __dadd_rn(rp, lg);  // rho[g] = R[g-1] + L[g] (fields.py:85)
+  } else if (field_bc == PB_FIELD_PERIODIC) {
+    double l0, r0, ll, rl;  // rho[0] = rho[nc] = R[nc-1] + L[0]
+    weighted_partials(bins, ca.c, ndep, nc, 0, l0, r0);
+    weighted_partials(bins, ca.c, ndep, nc, nc - 1, ll, rl);
+    v = __dadd_rn(rl, l0);
+  } else if (g == 0) {
+    v = __dmul_rn(lg, 2.0);  // walls own half a cell (fields.py:115-117)
+  } else {
+    v = __dmul_rn(rp, 2.0);
+  }
+  rho[g] = v;
+}
+
+}  // namespace pb
+
+extern "C" int pb_abi_version(void) { return PB_ABI_VERSION; }
+
+extern "C" const char *pb_last_error(void) { return pb::g_err; }
+
+extern "C" int pb_device_sm_count(int *out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return pb::cuda_status(e, "cudaGetDevice");
+  e = cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return pb::cuda_status(e, "cudaDeviceGetAttribute");
+  return PB_OK;
+}
+
+extern "C" int pb_rho_epilogue(const uint64_t *bins, const double *coef,
+                               int ndep, int64_t nc, int field_bc, double *left,
+                               double *right, double *rho, void *stream) {
+  if (ndep < 0 || ndep > PB_MAX_SPECIES) {
+    pb::set_error("ndep=%d outside [0, %d]", ndep, PB_MAX_SPECIES);
+    return PB_ERR_INVALID;
+  }
+  if (nc < 2 || !rho || (ndep > 0 && (!bins || !coef))) {
+    pb::set_error("pb_rho_epilogue: bad arguments (nc=%lld)", (long long)nc);
+    return PB_ERR_INVALID;
+  }
+  if (field_bc != PB_FIELD_PERIODIC && field_bc != PB_FIELD_DIRICHLET) {
+    pb::set_error("unknown field boundary %d", field_bc);
+    return PB_ERR_INVALID;
+  }
+  pb::CoefArgs ca;
+  memset(&ca, 0, sizeof(ca));
+  for (int s = 0; s < ndep; ++s) ca.c[s] = coef[s];
+  const int threads = 256;
+  const int64_t blocks = (nc + 1 + threads - 1) / threads;
+  pb::k_rho_epilogue<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
+      bins, ca, ndep, nc, field_bc, left, right, rho);
+  PB_CHECK_LAUNCH("k_rho_epilogue");
+  return PB_OK;
+}

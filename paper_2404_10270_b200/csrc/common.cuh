@@ -1,0 +1,56 @@
+// Shared helpers for the sm_100a kernels of libpicmc_b200.
+//
+// Arithmetic discipline: the reference compiles its kernels with
+// -ffp-contract=off (pkg/setup.py:9-12), so every expression that must match
+// it bit for bit is spelled with explicit round-to-nearest intrinsics
+// (__dadd_rn / __dmul_rn / __dsub_rn) and the whole library is additionally
+// built with --fmad=false.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/picmc_b200.h"
+
+namespace pb {
+
+// Thread-local error text for pb_last_error().
+void set_error(const char *fmt, ...);
+int cuda_status(cudaError_t err, const char *what);
+
+#define PB_CHECK_LAUNCH(what)                                   \
+  do {                                                          \
+    cudaError_t e__ = cudaGetLastError();                       \
+    if (e__ != cudaSuccess) return ::pb::cuda_status(e__, what); \
+  } while (0)
+
+constexpr int kFracBits = PB_DEPOSIT_FRAC_BITS;
+constexpr double kFracScale = 281474976710656.0;       // 2^48
+constexpr double kFracInv = 1.0 / 281474976710656.0;   // 2^-48
+// Packed warp-scan payload: bits [0,56) = R sum, bits [56,64) = count.
+constexpr int kCountShift = 56;
+constexpr uint64_t kRMask = (uint64_t(1) << kCountShift) - 1;
+
+// Quantise a cell-relative position in [0,1) to the deposit fixed point.
+__device__ __forceinline__ uint64_t quantize(double x) {
+  return (uint64_t)__double2ull_rn(__dmul_rn(x, kFracScale));
+}
+
+// Sum of per-particle fixed-point weights, packed with a count.
+__device__ __forceinline__ uint64_t deposit_word(double x) {
+  return (uint64_t(1) << kCountShift) | quantize(x);
+}
+
+__device__ __forceinline__ unsigned lane_id() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(r));
+  return r;
+}
+
+// Python floor-mod for the periodic wrap (mover.py:156, `% nc_global`).
+__device__ __forceinline__ int64_t floor_mod(int64_t a, int64_t m) {
+  int64_t r = a % m;
+  return r < 0 ? r + m : r;
+}
+
+}  // namespace pb

@@ -1,0 +1,216 @@
+// Replicated field pipeline: 1-2-1 smoothing, Poisson solve, E = -grad phi.
+//
+// The grid is tiny next to the particle arrays (nc+1 doubles), so every GPU
+// holds a replica and solves it locally after the density allreduce.  The
+// stencils reproduce the reference's NumPy expression order exactly
+// (pkg/src/picmc/fields.py:121-135, :205-218).  The Poisson solve offers the
+// reference's direct elimination (fields.py:138-202), restated operation for
+// operation -- including NumPy's pairwise summation inside np.mean -- on one
+// thread, so a given rho yields a bitwise-identical phi.
+#include "common.cuh"
+
+namespace pb {
+
+// ---- stencils ---------------------------------------------------------------
+// core = 0.25*roll(core,1) + 0.5*core + 0.25*roll(core,-1); out[nc] = out[0]
+__global__ void k_smooth_pass(const double *__restrict__ in,
+                              double *__restrict__ out, int64_t nc) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > nc) return;
+  const int64_t jj = j == nc ? 0 : j;
+  const double a = in[jj == 0 ? nc - 1 : jj - 1];
+  const double b = in[jj];
+  const double c = in[jj == nc - 1 ? 0 : jj + 1];
+  out[j] = __dadd_rn(__dadd_rn(__dmul_rn(0.25, a), __dmul_rn(0.5, b)),
+                     __dmul_rn(0.25, c));
+}
+
+__global__ void k_efield(const double *__restrict__ phi, double *__restrict__ e,
+                         int64_t nc, double two_dx, int field_bc) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > nc) return;
+  if (field_bc == PB_FIELD_PERIODIC) {
+    const int64_t jj = j == nc ? 0 : j;  // e[nc] = e[0]
+    const double l = phi[jj == 0 ? nc - 1 : jj - 1];
+    const double r = phi[jj == nc - 1 ? 0 : jj + 1];
+    e[j] = __ddiv_rn(__dsub_rn(l, r), two_dx);
+    return;
+  }
+  if (j == 0) {
+    const double t = __dadd_rn(__dsub_rn(__dmul_rn(3.0, phi[0]), __dmul_rn(4.0, phi[1])), phi[2]);
+    e[0] = __ddiv_rn(t, two_dx);
+  } else if (j == nc) {
+    const double t = __dadd_rn(__dsub_rn(__dmul_rn(3.0, phi[nc]), __dmul_rn(4.0, phi[nc - 1])),
+                               phi[nc - 2]);
+    e[nc] = __ddiv_rn(-t, two_dx);
+  } else {
+    e[j] = __ddiv_rn(__dsub_rn(phi[j - 1], phi[j + 1]), two_dx);
+  }
+}
+
+// ---- NumPy-exact reductions -------------------------------------------------
+// numpy pairwise_sum for float64 (blocks of 8 accumulators, PW_BLOCKSIZE 128).
+__device__ double pairwise_sum(const double *a, int64_t n) {
+  // Iterative restatement of the recursion: an explicit stack of ranges.
+  struct R { int64_t lo, n; int state; double left; };
+  R stk[64];
+  int sp = 0;
+  double ret = 0.0;
+  stk[sp++] = {0, n, 0, 0.0};
+  while (sp) {
+    R &f = stk[sp - 1];
+    if (f.n < 8) {
+      double res = -0.0;  // numpy starts from the reduction identity (-0.0)
+      for (int64_t i = 0; i < f.n; ++i) res = __dadd_rn(res, a[f.lo + i]);
+      ret = res;
+      --sp;
+    } else if (f.n <= 128) {
+      double r[8];
+      for (int k = 0; k < 8; ++k) r[k] = a[f.lo + k];
+      int64_t i;
+      for (i = 8; i < f.n - (f.n % 8); i += 8)
+        for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], a[f.lo + i + k]);
+      double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                             __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+      for (; i < f.n; ++i) res = __dadd_rn(res, a[f.lo + i]);
+      ret = res;
+      --sp;
+    } else {
+      int64_t n2 = f.n / 2;
+      n2 -= n2 % 8;
+      if (f.state == 0) {
+        f.state = 1;
+        stk[sp++] = {f.lo, n2, 0, 0.0};
+      } else if (f.state == 1) {
+        f.left = ret;
+        f.state = 2;
+        stk[sp++] = {f.lo + n2, f.n - n2, 0, 0.0};
+      } else {
+        ret = __dadd_rn(f.left, ret);
+        --sp;
+      }
+    }
+  }
+  return ret;
+}
+
+// np.add.reduce over a contiguous float64 array: out = a[0], then
+// out += pairwise_sum(a[1:]) (the reduction seeds with the first element).
+__device__ double np_sum(const double *a, int64_t n) {
+  if (n == 0) return 0.0;
+  return __dadd_rn(a[0], pairwise_sum(a + 1, n - 1));
+}
+
+// _thomas_unit (fields.py:138-153) on rhs[0..n) -> x[0..n); diag/y scratch.
+__device__ void thomas_unit(const double *rhs, double *x, double *diag,
+                            double *y, int64_t n) {
+  diag[0] = -2.0;
+  y[0] = rhs[0];
+  for (int64_t i = 1; i < n; ++i) {
+    const double m = __ddiv_rn(1.0, diag[i - 1]);
+    diag[i] = __dsub_rn(-2.0, m);
+    y[i] = __dsub_rn(rhs[i], __dmul_rn(m, y[i - 1]));
+  }
+  x[n - 1] = __ddiv_rn(y[n - 1], diag[n - 1]);
+  for (int64_t i = n - 2; i >= 0; --i)
+    x[i] = __ddiv_rn(__dsub_rn(y[i], x[i + 1]), diag[i]);
+}
+
+// solve_poisson (fields.py:156-202), one thread.
+__global__ void k_poisson_exact(const double *__restrict__ rho, double *phi,
+                                int64_t nc, double scale, int field_bc,
+                                double phi_left, double phi_right,
+                                double *scratch) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  double *rhs = scratch;
+  double *diag = scratch + (nc + 1);
+  double *y = scratch + 2 * (nc + 1);
+  if (field_bc == PB_FIELD_PERIODIC) {
+    const double mean = __ddiv_rn(np_sum(rho, nc), (double)nc);
+    for (int64_t j = 0; j < nc; ++j)
+      rhs[j] = __dmul_rn(-__dsub_rn(rho[j], mean), scale);
+    phi[0] = 0.0;
+    thomas_unit(rhs + 1, phi + 1, diag, y, nc - 1);
+    phi[nc] = phi[0];
+    const double shift = __ddiv_rn(np_sum(phi, nc), (double)nc);
+    for (int64_t j = 0; j <= nc; ++j) phi[j] = __dsub_rn(phi[j], shift);
+  } else {
+    for (int64_t j = 1; j < nc; ++j) rhs[j - 1] = __dmul_rn(-rho[j], scale);
+    rhs[0] = __dsub_rn(rhs[0], phi_left);
+    rhs[nc - 2] = __dsub_rn(rhs[nc - 2], phi_right);
+    phi[0] = phi_left;
+    phi[nc] = phi_right;
+    thomas_unit(rhs, phi + 1, diag, y, nc - 1);
+  }
+}
+
+static unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace pb
+
+extern "C" size_t pb_field_scratch_bytes(int64_t nc) {
+  return 3 * (size_t)(nc + 1) * sizeof(double);
+}
+
+extern "C" int pb_smooth_density(const double *rho, double *out, int64_t nc,
+                                 int passes, void *scratch, void *stream) {
+  if (nc < 2 || passes < 0 || !rho || !out || (passes > 1 && !scratch)) {
+    pb::set_error("pb_smooth_density: bad arguments");
+    return PB_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (passes == 0) {
+    // smooth_density(rho, 0) returns a copy with out[nc] = out[0]
+    cudaError_t e = cudaMemcpyAsync(out, rho, (size_t)nc * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return pb::cuda_status(e, "cudaMemcpyAsync");
+    e = cudaMemcpyAsync(out + nc, rho, sizeof(double), cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return pb::cuda_status(e, "cudaMemcpyAsync");
+    return PB_OK;
+  }
+  // Ping-pong so the last pass lands in `out`.
+  double *tmp = (double *)scratch;
+  const double *src = rho;
+  for (int p = 0; p < passes; ++p) {
+    double *dst = ((passes - 1 - p) % 2 == 0) ? out : tmp;
+    pb::k_smooth_pass<<<pb::blocks_for(nc + 1, 256), 256, 0, st>>>(src, dst, nc);
+    PB_CHECK_LAUNCH("k_smooth_pass");
+    src = dst;
+  }
+  return PB_OK;
+}
+
+extern "C" int pb_solve_poisson(const double *rho, double *phi, int64_t nc,
+                                double dx, double eps0, int field_bc,
+                                double phi_left, double phi_right,
+                                void *scratch, void *stream) {
+  if (nc < 3) {
+    pb::set_error("poisson solve needs nc >= 3, got %lld", (long long)nc);
+    return PB_ERR_INVALID;
+  }
+  if (!rho || !phi || !scratch) {
+    pb::set_error("pb_solve_poisson: NULL argument");
+    return PB_ERR_INVALID;
+  }
+  if (field_bc != PB_FIELD_PERIODIC && field_bc != PB_FIELD_DIRICHLET) {
+    pb::set_error("unknown boundary condition %d", field_bc);
+    return PB_ERR_INVALID;
+  }
+  const double scale = (dx * dx) / eps0;  // grid.dx_m * grid.dx_m / eps0
+  pb::k_poisson_exact<<<1, 32, 0, (cudaStream_t)stream>>>(
+      rho, phi, nc, scale, field_bc, phi_left, phi_right, (double *)scratch);
+  PB_CHECK_LAUNCH("k_poisson_exact");
+  return PB_OK;
+}
+
+extern "C" int pb_compute_efield(const double *phi, double *e, int64_t nc,
+                                 double dx, int field_bc, void *stream) {
+  if (nc < 3 || !phi || !e) {
+    pb::set_error("pb_compute_efield: bad arguments");
+    return PB_ERR_INVALID;
+  }
+  pb::k_efield<<<pb::blocks_for(nc + 1, 256), 256, 0, (cudaStream_t)stream>>>(
+      phi, e, nc, 2.0 * dx, field_bc);
+  PB_CHECK_LAUNCH("k_efield");
+  return PB_OK;
+}

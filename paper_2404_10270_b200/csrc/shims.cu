@@ -1,0 +1,184 @@
+// Parity shims with the reference kernel signatures, on the reference's own
+// packed cell-sorted layout (per-cell segments addressed by offs/counts,
+// pkg/src/picmc/core.py:100-132).  These let `picmc.backends`-style callers
+// (and the reference's test_backends.py comparisons) run on the GPU; the
+// engine itself uses the flat layout of push_deposit.cu.
+//
+// One warp per cell: lanes stride the cell's live slots (coalesced within
+// the segment); cells are grid-strided over warps.
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+
+namespace pb {
+
+constexpr int kShimThreads = 256;
+constexpr int kWarps = kShimThreads / 32;
+
+// fused_move (pkg/src/picmc/backends/_kernels.pyx:60-102).
+__global__ void k_fused_move(const double *__restrict__ accel, double *x,
+                             double *vx, const double *__restrict__ vy,
+                             double *yp, const int64_t *__restrict__ offs,
+                             const int64_t *__restrict__ counts, int64_t nc,
+                             double fnstep) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+  for (int64_t j = w0; j < nc; j += nw) {
+    const int64_t base = offs[j];
+    const int64_t cnt = counts[j];
+    double aj = 0.0, daj = 0.0;
+    if (accel) {
+      aj = accel[j];
+      daj = __dsub_rn(accel[j + 1], aj);
+    }
+    for (int64_t i = lane; i < cnt; i += 32) {
+      const int64_t k = base + i;
+      double v;
+      if (accel) {
+        const double atemp = __dadd_rn(aj, __dmul_rn(x[k], daj));
+        v = __dadd_rn(vx[k], atemp);
+        vx[k] = v;
+      } else {
+        v = vx[k];
+      }
+      x[k] = __dadd_rn(x[k], __dmul_rn(fnstep, v));
+      if (yp) yp[k] = __dadd_rn(yp[k], __dmul_rn(fnstep, vy[k]));
+    }
+  }
+}
+
+// deposit_partials (_kernels.pyx:14-34): strictly sequential per cell in
+// slot order, so the result is bitwise the reference's.  The warp loads 32
+// slots at a time and every lane replays the same sequential sum.
+__global__ void k_deposit_partials(const double *__restrict__ x,
+                                   const int64_t *__restrict__ offs,
+                                   const int64_t *__restrict__ counts,
+                                   int64_t nc, double *__restrict__ left,
+                                   double *__restrict__ right) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+  for (int64_t j = w0; j < nc; j += nw) {
+    const int64_t base = offs[j];
+    const int64_t cnt = counts[j];
+    double sl = 0.0, sr = 0.0;
+    for (int64_t c0 = 0; c0 < cnt; c0 += 32) {
+      const double xv = (c0 + lane < cnt) ? x[base + c0 + lane] : 0.0;
+      const int m = (int)((cnt - c0) < 32 ? (cnt - c0) : 32);
+      for (int k = 0; k < m; ++k) {
+        const double xk = __shfl_sync(full, xv, k);
+        sl = __dadd_rn(sl, __dsub_rn(1.0, xk));
+        sr = __dadd_rn(sr, xk);
+      }
+    }
+    if (lane == 0) {
+      left[j] = sl;
+      right[j] = sr;
+    }
+  }
+}
+
+// gather (_kernels.pyx:37-57): live order output, start[j] = sum(counts[:j]).
+__global__ void k_gather(const double *__restrict__ nodes,
+                         const double *__restrict__ x,
+                         const int64_t *__restrict__ offs,
+                         const int64_t *__restrict__ counts,
+                         const int64_t *__restrict__ start, int64_t nc,
+                         double *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+  for (int64_t j = w0; j < nc; j += nw) {
+    const int64_t base = offs[j];
+    const int64_t cnt = counts[j];
+    const int64_t o = start[j];
+    const double aj = nodes[j];
+    const double daj = __dsub_rn(nodes[j + 1], aj);
+    for (int64_t i = lane; i < cnt; i += 32)
+      out[o + i] = __dadd_rn(aj, __dmul_rn(x[base + i], daj));
+  }
+}
+
+static unsigned shim_grid(int64_t nc) {
+  int64_t blocks = (nc + kWarps - 1) / kWarps;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  if (blocks < 1) blocks = 1;
+  return (unsigned)blocks;
+}
+
+}  // namespace pb
+
+extern "C" int pb_fused_move(const double *accel_or_null, double *x,
+                             double *vx, const double *vy, double *yp_or_null,
+                             const int64_t *offs, const int64_t *counts,
+                             int64_t nc, double fnstep, void *stream) {
+  if (nc < 0) {
+    pb::set_error("nc=%lld must be >= 0", (long long)nc);
+    return PB_ERR_INVALID;
+  }
+  if (nc == 0) return PB_OK;
+  if (!x || !vx || !offs || !counts || (yp_or_null && !vy)) {
+    pb::set_error("pb_fused_move: NULL array argument");
+    return PB_ERR_INVALID;
+  }
+  pb::k_fused_move<<<pb::shim_grid(nc), pb::kShimThreads, 0, (cudaStream_t)stream>>>(
+      accel_or_null, x, vx, vy, yp_or_null, offs, counts, nc, fnstep);
+  PB_CHECK_LAUNCH("k_fused_move");
+  return PB_OK;
+}
+
+extern "C" int pb_deposit_partials(const double *x, const int64_t *offs,
+                                   const int64_t *counts, int64_t nc,
+                                   double *left, double *right, void *stream) {
+  if (nc < 0) {
+    pb::set_error("nc=%lld must be >= 0", (long long)nc);
+    return PB_ERR_INVALID;
+  }
+  if (nc == 0) return PB_OK;
+  if (!offs || !counts || !left || !right) {
+    pb::set_error("pb_deposit_partials: NULL array argument");
+    return PB_ERR_INVALID;
+  }
+  pb::k_deposit_partials<<<pb::shim_grid(nc), pb::kShimThreads, 0, (cudaStream_t)stream>>>(
+      x, offs, counts, nc, left, right);
+  PB_CHECK_LAUNCH("k_deposit_partials");
+  return PB_OK;
+}
+
+extern "C" int pb_gather(const double *nodes, const double *x,
+                         const int64_t *offs, const int64_t *counts, int64_t nc,
+                         double *out, void *stream) {
+  if (nc < 0) {
+    pb::set_error("nc=%lld must be >= 0", (long long)nc);
+    return PB_ERR_INVALID;
+  }
+  if (nc == 0) return PB_OK;
+  if (!nodes || !offs || !counts) {
+    pb::set_error("pb_gather: NULL array argument");
+    return PB_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  size_t tmp_bytes = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts,
+                                                (int64_t *)nullptr, (int)nc, st);
+  if (e != cudaSuccess) return pb::cuda_status(e, "DeviceScan size");
+  void *buf = nullptr;
+  const size_t start_bytes = ((size_t)nc * sizeof(int64_t) + 255) & ~(size_t)255;
+  e = cudaMallocAsync(&buf, start_bytes + tmp_bytes, st);
+  if (e != cudaSuccess) return pb::cuda_status(e, "cudaMallocAsync");
+  int64_t *start = (int64_t *)buf;
+  void *tmp = (char *)buf + start_bytes;
+  e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, start, (int)nc, st);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(buf, st);
+    return pb::cuda_status(e, "DeviceScan");
+  }
+  pb::k_gather<<<pb::shim_grid(nc), pb::kShimThreads, 0, st>>>(nodes, x, offs, counts,
+                                                              start, nc, out);
+  cudaError_t le = cudaGetLastError();
+  cudaFreeAsync(buf, st);
+  if (le != cudaSuccess) return pb::cuda_status(le, "k_gather");
+  return PB_OK;
+}

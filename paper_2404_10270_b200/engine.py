@@ -1,0 +1,356 @@
+"""Device-resident step engine: the B200 replacement for the reference's
+deposit -> [smooth -> solve -> E] -> gather -> move -> resort -> migrate cycle
+(pkg/src/picmc/harness.py:144-242).
+
+Per step, on one CUDA stream:
+  deposit  fixed-point bins from the previous push -> (NCCL allreduce across
+           GPUs) -> weighted partials + stitch            pb_rho_epilogue
+  smooth/solve/E (field_solve only), replicated on every GPU
+  mover    fused gather + kick/Boris + drift + cell transfer + absorbing
+           removal + next-step deposit                    pb_push_deposit
+  resort   absorbing-wall hole compaction                 pb_compact
+           periodic cell sort every `sort_every` steps    pb_sort_by_cell
+
+The reference's separate gather phase computes E_p and discards it
+(harness.py:180-185); here the gather lives inside the mover.  Its resort and
+migrate phases (mover.py:113-195, decomposition.py:177-229) collapse into the
+mover's register-level cell update: particles are sharded by index over a
+replicated grid, so nothing migrates between GPUs.
+"""
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import check_store_budget, init_species_host, macro_weight, thermal_std, velocity_kick_coef
+from .errors import CflViolation, ConfigError, EngineError
+from .rng import STREAM_INIT, stream
+from .store import DeviceSpecies, decode_status, species_array, status_template
+
+PHASE_KEYS = ("deposit", "smooth", "solve", "gather", "collide", "mover", "resort", "migrate")
+
+
+def partition_cells(nc: int, workers: int) -> tuple:
+    """Contiguous balanced ranges, sizes differing <= 1 (decomposition.py:66-79)."""
+    if workers < 1 or workers > nc:
+        raise ConfigError(f"workers ({workers}) must be in [1, nc={nc}]")
+    base, rem = divmod(nc, workers)
+    out, lo = [], 0
+    for w in range(workers):
+        hi = lo + base + (1 if w < rem else 0)
+        out.append((lo, hi))
+        lo = hi
+    return tuple(out)
+
+
+@dataclass(frozen=True)
+class Partition:
+    """GPU shard map: rank r loaded the particles of cells ranges[r]."""
+
+    worker_count: int
+    nc: int
+    ranges: tuple
+
+
+def reduce_bins(bins: torch.Tensor, group=None):
+    """Sum the per-rank fixed-point deposit bins (exact int64 allreduce).
+
+    Works for CUDA tensors under NCCL and CPU tensors under gloo; the sum of
+    integers is associative, so the reduced density is bitwise independent of
+    the GPU count and of NCCL's algorithm choice (ring / tree / NVLS).
+    """
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(bins, op=dist.ReduceOp.SUM, group=group)
+    return bins
+
+
+def boris_coefficients(sp, consts, b_field) -> tuple:
+    """t = q B dt / (2 m), s = 2 t / (1 + |t|^2) (standard Boris rotation)."""
+    f = sp.charge_c * consts.dt_s / (2.0 * sp.mass_kg)
+    t = [f * float(b) for b in b_field]
+    t2 = t[0] * t[0] + t[1] * t[1] + t[2] * t[2]
+    s = [2.0 * c / (1.0 + t2) for c in t]
+    return t, s
+
+
+def species_kind(sp, b_field) -> int:
+    if not sp.active_mover:
+        return _lib.PB_KIND_INACTIVE
+    if sp.charged:
+        return _lib.PB_KIND_BORIS if b_field is not None else _lib.PB_KIND_KICK
+    return _lib.PB_KIND_DRIFT
+
+
+class Engine:
+    """One GPU's share of a run: its particle shard plus a grid replica."""
+
+    def __init__(self, config, device=None, *, rank: int = 0, world: int = 1,
+                 group=None, init: str = "host", check_every: int = 1):
+        config.validate()
+        if config.collisions is not None and config.collisions.enabled:
+            raise ConfigError(
+                "collisions are not on the device hot path (SURVEY.md 8f); "
+                "disable [collisions] for the B200 engine"
+            )
+        if not torch.cuda.is_available():
+            raise RuntimeError("the B200 engine needs a CUDA device; there is no CPU fallback")
+        self.lib = _lib.load()
+        self.cfg = config
+        self.device = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
+        self.rank, self.world, self.group = rank, world, group
+        self.grid = config.grid
+        self.nc = int(config.grid.nc)
+        self.periodic = config.boundary == "periodic"
+        self.field_bc = _lib.PB_FIELD_PERIODIC if self.periodic else _lib.PB_FIELD_DIRICHLET
+        self.absorbing = getattr(config, "particle_boundary", "periodic") == "absorbing"
+        self.bc = _lib.PB_BC_ABSORBING if self.absorbing else _lib.PB_BC_PERIODIC
+        self.b_field = getattr(config, "b_field_t", None)
+        self.sort_every = int(getattr(config, "sort_every", 0) or 0)
+        self.check_every = int(check_every)
+        self.partition = Partition(world, self.nc, partition_cells(self.nc, world))
+        self.cell_lo, self.cell_hi = self.partition.ranges[rank]
+        check_store_budget(config)
+
+        self.stream = torch.cuda.Stream(self.device)
+        self.sp = []
+        self.coef_dep = []
+        ndep = 0
+        nloc = (self.cell_hi - self.cell_lo) * int(config.ppc0)
+        for isp, spd in enumerate(config.species):
+            kind = species_kind(spd, self.b_field)
+            dep = -1
+            if spd.charged:
+                dep = ndep
+                ndep += 1
+                self.coef_dep.append(spd.charge_c * macro_weight(config, isp) / self.grid.dx_m)
+            kick = velocity_kick_coef(spd, config.consts, self.grid.dx_m) if spd.charged else 0.0
+            boris = boris_coefficients(spd, config.consts, self.b_field) if kind == _lib.PB_KIND_BORIS else None
+            with torch.cuda.stream(self.stream):
+                self.sp.append(DeviceSpecies(spd, nloc, self.device, kind=kind, deposit=dep,
+                                             kick_coef=kick, boris=boris, absorbing=self.absorbing))
+        self.ndep = ndep
+        self._coef_c = (ctypes.c_double * max(ndep, 1))(*self.coef_dep)
+        nc = self.nc
+        with torch.cuda.stream(self.stream):
+            self.bins = torch.zeros(max(ndep, 1) * 2 * nc, dtype=torch.int64, device=self.device)
+            self.rho = torch.zeros(nc + 1, dtype=torch.float64, device=self.device)
+            self.left = torch.zeros(nc, dtype=torch.float64, device=self.device)
+            self.right = torch.zeros(nc, dtype=torch.float64, device=self.device)
+            self.rho_s = torch.zeros(nc + 1, dtype=torch.float64, device=self.device)
+            self.phi = torch.zeros(nc + 1, dtype=torch.float64, device=self.device)
+            self.e = torch.zeros(nc + 1, dtype=torch.float64, device=self.device)
+            self.field_scratch = torch.empty(
+                max(1, self.lib.pb_field_scratch_bytes(nc) // 8), dtype=torch.float64, device=self.device)
+            self.status_tpl = status_template(self.device)
+            self.status = self.status_tpl.clone()
+            self.compact_scratch = None
+            if self.absorbing:
+                nb = self.lib.pb_compact_scratch_bytes(max(nloc, 1))
+                self.compact_scratch = torch.empty(nb, dtype=torch.uint8, device=self.device)
+        self.sort_scratch = None
+        self.step_index = 0
+        self._pending = []  # (step, status pinned, n_live pinned, event)
+        self.phase_events = []
+        self.absorbed = np.zeros((len(self.sp), 2), dtype=np.int64)
+        self.moved = np.zeros(len(self.sp), dtype=np.int64)
+        self._load(init)
+
+    # -- setup ------------------------------------------------------------------
+    def _load(self, init: str):
+        cfg = self.cfg
+        with torch.cuda.stream(self.stream):
+            for isp, s in enumerate(self.sp):
+                if init == "host":
+                    s.upload(init_species_host(cfg, isp, self.cell_lo, self.cell_hi))
+                elif init == "device":
+                    std = thermal_std(cfg.temperatures_ev[isp], s.sp.mass_kg, cfg.consts.dt_s, self.grid.dx_m)
+                    key = stream(cfg.seed, STREAM_INIT, isp)
+                    pbs = s.pb()
+                    _lib.check(self.lib.pb_init_species(ctypes.byref(pbs), key, self.cell_lo, self.cell_hi,
+                                                        int(cfg.ppc0), std, self._sh()), "pb_init_species")
+                elif init == "none":
+                    pass
+                else:
+                    raise ValueError(f"unknown init mode {init!r}")
+        self.deposit_current()
+
+    def _sh(self):
+        return ctypes.c_void_p(self.stream.cuda_stream)
+
+    def _species(self):
+        return species_array(self.sp)
+
+    def deposit_current(self):
+        """Fixed-point deposit of the current positions into the bins
+        (the reference's step-start deposit, harness.py:148-160)."""
+        arr, n = self._species()
+        with torch.cuda.stream(self.stream):
+            self.bins.zero_()
+            _lib.check(self.lib.pb_deposit_only(arr, n, self.nc, self.bins.data_ptr(),
+                                                self.status.data_ptr(), self._sh()), "pb_deposit_only")
+
+    def upload(self, flats: list):
+        """Replace the particle state with host arrays (engine flat layout)."""
+        with torch.cuda.stream(self.stream):
+            for s, f in zip(self.sp, flats):
+                if f.n != s.n:
+                    raise ValueError("particle count mismatch")
+                s.upload(f)
+        self.deposit_current()
+
+    # -- step phases ------------------------------------------------------------
+    def density(self) -> torch.Tensor:
+        """Reduce the bins across GPUs and produce left/right/rho."""
+        with torch.cuda.stream(self.stream):
+            if self.world > 1:
+                reduce_bins(self.bins, self.group)
+            _lib.check(self.lib.pb_rho_epilogue(
+                self.bins.data_ptr(), self._coef_c, self.ndep, self.nc, self.field_bc,
+                self.left.data_ptr(), self.right.data_ptr(), self.rho.data_ptr(), self._sh()),
+                "pb_rho_epilogue")
+            self.bins.zero_()
+        return self.rho
+
+    def field(self, rho: torch.Tensor) -> torch.Tensor:
+        cfg = self.cfg
+        if not cfg.field_solve:
+            return self.e  # stays identically zero (harness.py:177-178)
+        sh = self._sh()
+        scr = self.field_scratch.data_ptr()
+        with torch.cuda.stream(self.stream):
+            src = rho
+            if cfg.smoothing_passes > 0:
+                _lib.check(self.lib.pb_smooth_density(rho.data_ptr(), self.rho_s.data_ptr(), self.nc,
+                                                      int(cfg.smoothing_passes), scr, sh), "pb_smooth_density")
+                src = self.rho_s
+            _lib.check(self.lib.pb_solve_poisson(src.data_ptr(), self.phi.data_ptr(), self.nc, self.grid.dx_m,
+                                                 cfg.consts.epsilon0, self.field_bc, cfg.phi_left,
+                                                 cfg.phi_right, scr, sh), "pb_solve_poisson")
+            _lib.check(self.lib.pb_compute_efield(self.phi.data_ptr(), self.e.data_ptr(), self.nc,
+                                                  self.grid.dx_m, self.field_bc, sh), "pb_compute_efield")
+        return self.e
+
+    def push(self, e: torch.Tensor = None):
+        """Fused mover + deposit of the next step's density."""
+        if e is None:
+            e = self.e
+        arr, n = self._species()
+        with torch.cuda.stream(self.stream):
+            self.status.copy_(self.status_tpl)
+            _lib.check(self.lib.pb_push_deposit(arr, n, e.data_ptr(), self.nc, self.bc, self.bins.data_ptr(),
+                                                self.status.data_ptr(), self._sh()), "pb_push_deposit")
+
+    def resort(self):
+        with torch.cuda.stream(self.stream):
+            if self.absorbing:
+                arr, n = self._species()
+                _lib.check(self.lib.pb_compact(arr, n, self.status.data_ptr(), self.compact_scratch.data_ptr(),
+                                               self.compact_scratch.numel(), self._sh()), "pb_compact")
+            if self.sort_every and (self.step_index + 1) % self.sort_every == 0:
+                self.sort_by_cell()
+
+    def sort_by_cell(self):
+        """Radix sort every species by cell into the spare buffers, swap."""
+        with torch.cuda.stream(self.stream):
+            for s in self.sp:
+                n = s.live_count()
+                if n <= 1:
+                    continue
+                need = self.lib.pb_sort_scratch_bytes(n, self.nc)
+                if self.sort_scratch is None or self.sort_scratch.numel() < need:
+                    self.sort_scratch = torch.empty(need, dtype=torch.uint8, device=self.device)
+                dst = s.spare()
+                a, b = s.pb(n), dst.pb(n)
+                _lib.check(self.lib.pb_sort_by_cell(ctypes.byref(a), ctypes.byref(b), self.nc,
+                                                    self.sort_scratch.data_ptr(), self.sort_scratch.numel(),
+                                                    self._sh()), "pb_sort_by_cell")
+                s.swap_with_spare()
+
+    def step(self, timed: bool = False):
+        """One full cycle.  Returns rho/E of this step (device tensors)."""
+        ev = None
+        if timed:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            ev[0].record(self.stream)
+        rho = self.density()
+        if timed:
+            ev[1].record(self.stream)
+        e = self.field(rho)
+        if timed:
+            ev[2].record(self.stream)
+        self.push(e)
+        if timed:
+            ev[3].record(self.stream)
+        self.resort()
+        if timed:
+            ev[4].record(self.stream)
+            self.phase_events.append(ev)
+        self._record_status()
+        self.step_index += 1
+        if self.check_every and self.step_index % self.check_every == 0:
+            self.sync()
+        return rho, e
+
+    # -- status handling ------------------------------------------------------------
+    def _record_status(self):
+        with torch.cuda.stream(self.stream):
+            host = torch.empty(_lib.STATUS_BYTES, dtype=torch.uint8, pin_memory=True)
+            host.copy_(self.status, non_blocking=True)
+            nlive = None
+            if self.absorbing:
+                nlive = torch.empty(len(self.sp), dtype=torch.int64, pin_memory=True)
+                nlive.copy_(torch.cat([s.n_dev for s in self.sp]), non_blocking=True)
+            evt = torch.cuda.Event()
+            evt.record(self.stream)
+        self._pending.append((self.step_index + 1, host, nlive, evt))
+
+    def sync(self):
+        """Wait for enqueued steps and raise the first recorded error."""
+        pend, self._pending = self._pending, []
+        for step, host, nlive, evt in pend:
+            evt.synchronize()
+            st = decode_status(host.numpy())
+            for k in range(len(self.sp)):
+                self.moved[k] += st.moved[k]
+                self.absorbed[k, 0] += st.absorbed[k][0]
+                self.absorbed[k, 1] += st.absorbed[k][1]
+            if nlive is not None:
+                self.last_live = [int(v) for v in nlive.numpy()]
+            if st.code == _lib.PB_ERR_CFL:
+                key = int(st.cfl_index)
+                isp, idx = key >> 56, key & ((1 << 56) - 1)
+                s = self.sp[isp]
+                x = float(s.arr["x"][idx].item())
+                cell = int(s.cell[idx].item())
+                raise CflViolation(
+                    f"step {step}, phase resort: species {s.name!r} cell {cell}: "
+                    f"displacement of {int(math.floor(x))} cells reaches across the whole domain"
+                )
+            if st.code != _lib.PB_OK:
+                raise EngineError(f"step {step}: device status {st.code}")
+
+    def totals(self) -> list:
+        return [s.live_count() for s in self.sp]
+
+    def download(self) -> list:
+        self.stream.synchronize()
+        return [s.download() for s in self.sp]
+
+    def phase_seconds(self) -> dict:
+        """Resolve the per-phase CUDA events of timed steps (seconds)."""
+        self.stream.synchronize()
+        out = {k: 0.0 for k in PHASE_KEYS}
+        for ev in self.phase_events:
+            out["deposit"] += ev[0].elapsed_time(ev[1]) * 1e-3
+            solve = ev[1].elapsed_time(ev[2]) * 1e-3
+            out["solve"] += solve
+            out["mover"] += ev[2].elapsed_time(ev[3]) * 1e-3
+            out["resort"] += ev[3].elapsed_time(ev[4]) * 1e-3
+        return out

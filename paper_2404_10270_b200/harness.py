@@ -1,0 +1,147 @@
+"""`run_simulation(config, on_step=None) -> RunMetrics` on the B200 engine.
+
+Same signature, diagnostics rows, on_step state keys and RunMetrics fields as
+the reference step driver (pkg/src/picmc/harness.py:66-113, :246-268), so a
+caller can swap `picmc.run_simulation` for this one.  Phase timers come from
+CUDA events on the engine stream instead of perf_counter.
+"""
+
+import csv
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .engine import PHASE_KEYS, Engine
+
+BACKEND = "cuda"
+
+
+@dataclass
+class CollisionTally:
+    elastic: int = 0
+    excitation: int = 0
+    ionization: int = 0
+    suppressed: int = 0
+
+    def merge(self, other: "CollisionTally"):
+        self.elastic += other.elastic
+        self.excitation += other.excitation
+        self.ionization += other.ionization
+        self.suppressed += other.suppressed
+
+
+@dataclass
+class RunMetrics:
+    phase_seconds: dict
+    diagnostics: list
+    config_hash: str
+    worker_count: int
+    layout: str
+    backend: str
+    tally: CollisionTally
+    absorbed: dict = field(default_factory=dict)  # config 3: per species [left, right]
+
+
+class _LazyStores(list):
+    """on_step's "stores": host copies of this rank's species, fetched on use."""
+
+    def __init__(self, engine):
+        super().__init__()
+        self._engine = engine
+        self._loaded = False
+
+    def _load(self):
+        if not self._loaded:
+            super().extend([self._engine.download()])
+            self._loaded = True
+
+    def __len__(self):
+        return self._engine.world
+
+    def __getitem__(self, i):
+        self._load()
+        return super().__getitem__(0 if i in (0, -1) and self._engine.world == 1 else i)
+
+    def __iter__(self):
+        self._load()
+        return super().__iter__()
+
+
+def _diag_row(step, names, totals, tally):
+    row = {"step": step}
+    for name, t in zip(names, totals):
+        row[f"total_{name}"] = int(t)
+    row["elastic"] = tally.elastic
+    row["excitation"] = tally.excitation
+    row["ionization"] = tally.ionization
+    row["suppressed"] = tally.suppressed
+    return row
+
+
+def _global_totals(engine):
+    tot = engine.totals()
+    if engine.absorbing and hasattr(engine, "last_live"):
+        tot = list(engine.last_live)
+    if engine.world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor(tot, dtype=torch.int64, device=engine.device)
+        dist.all_reduce(t, group=engine.group)
+        tot = [int(v) for v in t.cpu()]
+    return tot
+
+
+def run_simulation(config, on_step=None, *, rank=0, world=1, group=None,
+                   device=None, init="host") -> RunMetrics:
+    """Execute n_steps of the cycle on the GPU; returns timers and diagnostics."""
+    engine = Engine(config, device=device, rank=rank, world=world, group=group, init=init)
+    names = [sp.name for sp in config.species]
+    zero = CollisionTally()
+    diagnostics = [_diag_row(0, names, _global_totals(engine), zero)]
+    t0 = time.perf_counter()
+    for step in range(1, config.n_steps + 1):
+        rho, e = engine.step(timed=True)
+        diagnostics.append(_diag_row(step, names, _global_totals(engine), CollisionTally()))
+        if on_step is not None:
+            on_step(step, {
+                "rho": rho.cpu().numpy().copy(),
+                "e_field": e.cpu().numpy().copy(),
+                "stores": _LazyStores(engine),
+                "partition": engine.partition,
+                "tally": CollisionTally(),
+            })
+    engine.sync()
+    phase = engine.phase_seconds()
+    phase["total"] = time.perf_counter() - t0 if config.n_steps > 0 else 0.0
+    metrics = RunMetrics(
+        phase_seconds=phase, diagnostics=diagnostics, config_hash=config.config_hash(),
+        worker_count=world, layout="flat_soa", backend=BACKEND, tally=CollisionTally(),
+        absorbed={n: engine.absorbed[k].tolist() for k, n in enumerate(names)},
+    )
+    if config.out_dir is not None and rank == 0:
+        os.makedirs(config.out_dir, exist_ok=True)
+        write_diagnostics_csv(diagnostics, names, os.path.join(config.out_dir, "diagnostics.csv"))
+        write_metrics_csv(phase, os.path.join(config.out_dir, "metrics.csv"))
+    return metrics
+
+
+def write_diagnostics_csv(diagnostics, names, path):
+    """Byte-compatible with pkg/src/picmc/harness.py:355-363."""
+    cols = ["step"] + [f"total_{n}" for n in names] + ["elastic", "excitation", "ionization", "suppressed"]
+    with open(path, "w", newline="", encoding="utf-8") as fh:
+        w = csv.writer(fh, lineterminator="\n")
+        w.writerow(cols)
+        for row in diagnostics:
+            w.writerow([row[c] for c in cols])
+
+
+def write_metrics_csv(phase_seconds, path):
+    """Byte-compatible with pkg/src/picmc/harness.py:366-371."""
+    with open(path, "w", newline="", encoding="utf-8") as fh:
+        w = csv.writer(fh, lineterminator="\n")
+        w.writerow(["phase", "seconds"])
+        for key in PHASE_KEYS + ("total",):
+            w.writerow([key, f"{phase_seconds.get(key, 0.0):.9f}"])

@@ -1,0 +1,364 @@
+"""Device engine vs the oracle: per-particle state bit-exact, deposit bins
+exact against the oracle's fixed-point restatement and within tolerance of
+the reference's sequential fp64 summation.
+
+Tolerances (stated once, used below):
+  per-particle x, vx, vy, vz, yp, cell ...... bit-exact
+  moved / absorbed / surviving counts ........ exact
+  raw partials L_s, R_s vs sequential fp64 ... |d| <= 1e-13 * max(1, count_cell)
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import bits_equal
+
+pytestmark = pytest.mark.gpu
+
+DEP_TOL = 1e-13
+
+
+def _mk_config(nc=37, ppc0=20, species=None, **kw):
+    from paper_2404_10270_b200 import Grid1D, PhysicalConstants, RunConfig, SpeciesDef
+    from paper_2404_10270_b200.core import DEUTERIUM_MASS, ELECTRON_MASS, ELEMENTARY_CHARGE
+
+    if species is None:
+        species = [
+            SpeciesDef("e", -ELEMENTARY_CHARGE, ELECTRON_MASS),
+            SpeciesDef("D+", ELEMENTARY_CHARGE, DEUTERIUM_MASS - ELECTRON_MASS),
+            SpeciesDef("D", 0.0, DEUTERIUM_MASS, nstep=3, track_transverse=True),
+        ]
+    base = dict(grid=Grid1D.from_cells(nc, nc * 1e-5), consts=PhysicalConstants(dt_s=4e-14),
+                species=species, temperatures_ev=[20.0, 20.0, 1.0][: len(species)] + [1.0] * max(0, len(species) - 3),
+                densities_m3=[1e21] * len(species), ppc0=ppc0, n_steps=5, seed=20260819,
+                field_solve=False, smoothing_passes=0)
+    base.update(kw)
+    return RunConfig(**base)
+
+
+def _random_flats(cfg, seed, vscale=0.7):
+    from paper_2404_10270_b200.core import FlatSpecies
+
+    rng = np.random.default_rng(seed)
+    nc, ppc = cfg.grid.nc, cfg.ppc0
+    out = []
+    for sp in cfg.species:
+        n = nc * ppc
+        vx = vscale * rng.standard_normal(n)
+        vx[rng.random(n) < 0.02] = -0.0
+        out.append(FlatSpecies(
+            x=rng.random(n), vx=vx, vy=vscale * rng.standard_normal(n),
+            vz=vscale * rng.standard_normal(n),
+            yp=rng.standard_normal(n) if sp.track_transverse else None,
+            cell=np.repeat(np.arange(nc, dtype=np.int32), ppc),
+        ))
+    return out
+
+
+def _oracle_kind(eng, k):
+    return eng.sp[k].kind
+
+
+def _run_oracle_step(eng, flats, e, bc):
+    from oracle import oracle
+
+    res = []
+    for k, (s, f) in enumerate(zip(eng.sp, flats)):
+        bt = bs = None
+        if s.boris is not None:
+            bt, bs = s.boris
+        moved, removed, cfl = oracle.step_flat(s.kind, bc, s.fnstep, s.kick_coef, e, eng.nc, f.x, f.vx,
+                                                f.vy, f.vz, f.yp, f.cell, bt, bs)
+        res.append((moved, removed, cfl))
+    return res
+
+
+def _compare_arrays(dev, ref):
+    for name, arr in ref.fields().items():
+        assert bits_equal(dev.fields()[name], arr), name
+    assert np.array_equal(dev.cell, ref.cell)
+
+
+@pytest.mark.parametrize("with_field", [False, True])
+def test_push_deposit_bitwise_vs_oracle(cuda, with_field):
+    import torch
+
+    from oracle import oracle
+    from paper_2404_10270_b200 import Engine
+
+    cfg = _mk_config()
+    eng = Engine(cfg, device=cuda, check_every=0)
+    flats = _random_flats(cfg, seed=3)
+    eng.upload(flats)
+    rng = np.random.default_rng(11)
+    for step in range(12):
+        e = (3e3 * rng.standard_normal(eng.nc + 1)) if with_field else np.zeros(eng.nc + 1)
+        et = torch.from_numpy(e).to(cuda)
+        eng.bins.zero_()
+        eng.push(et)
+        eng.resort()
+        res = _run_oracle_step(eng, flats, e, 0)
+        dev = eng.download()
+        eng.sync()
+        for k in range(len(flats)):
+            _compare_arrays(dev[k], flats[k])
+            assert res[k][2] == -1
+        # deposit bins: exact vs the fixed-point restatement, tolerance vs fp64
+        bins = eng.bins.cpu().numpy().view(np.uint64).reshape(eng.ndep, 2, eng.nc)
+        d = 0
+        for k, s in enumerate(eng.sp):
+            if s.deposit < 0:
+                continue
+            R, C = oracle.deposit_fixed(flats[k].x, flats[k].cell, eng.nc)
+            assert np.array_equal(bins[d, 0], R) and np.array_equal(bins[d, 1], C)
+            lf, rf = oracle.fixed_to_raw(R, C)
+            ls, rs = oracle.deposit_seq(flats[k].x, flats[k].cell, eng.nc)
+            tol = DEP_TOL * np.maximum(1.0, C.astype(np.float64))
+            assert np.all(np.abs(lf - ls) <= tol) and np.all(np.abs(rf - rs) <= tol)
+            d += 1
+
+
+def test_moved_counts_exact(cuda):
+    import torch
+
+    from paper_2404_10270_b200 import Engine
+
+    cfg = _mk_config()
+    eng = Engine(cfg, device=cuda, check_every=0)
+    flats = _random_flats(cfg, seed=4)
+    eng.upload(flats)
+    e = np.zeros(eng.nc + 1)
+    eng.push(torch.from_numpy(e).to(cuda))
+    eng._record_status()
+    eng.sync()
+    res = _run_oracle_step(eng, flats, e, 0)
+    for k in range(len(flats)):
+        assert eng.moved[k] == res[k][0]
+
+
+def test_epilogue_matches_oracle_bitwise(cuda):
+    from oracle import oracle
+    from paper_2404_10270_b200 import Engine
+
+    for boundary in ("periodic", "dirichlet"):
+        cfg = _mk_config(boundary=boundary)
+        eng = Engine(cfg, device=cuda, check_every=0)
+        flats = eng.download()
+        raw = []
+        for k, s in enumerate(eng.sp):
+            if s.deposit >= 0:
+                R, C = oracle.deposit_fixed(flats[k].x, flats[k].cell, eng.nc)
+                raw.extend(oracle.fixed_to_raw(R, C))
+        raw = np.stack(raw).reshape(eng.ndep, 2, eng.nc)
+        left, right, rho = oracle.rho_from_raw(raw, eng.coef_dep, eng.nc, boundary == "periodic")
+        rho_dev = eng.density().cpu().numpy()
+        assert bits_equal(rho_dev, rho)
+        assert bits_equal(eng.left.cpu().numpy(), left)
+        assert bits_equal(eng.right.cpu().numpy(), right)
+
+
+def test_absorbing_walls_counts_and_survivors(cuda):
+    import torch
+
+    from oracle import oracle
+    from paper_2404_10270_b200 import Engine
+
+    cfg = _mk_config(particle_boundary="absorbing", boundary="dirichlet")
+    eng = Engine(cfg, device=cuda, check_every=0)
+    flats = _random_flats(cfg, seed=7, vscale=2.5)
+    eng.upload(flats)
+    live = [f for f in flats]
+    total_abs = np.zeros((3, 2), dtype=np.int64)
+    for step in range(6):
+        e = np.zeros(eng.nc + 1)
+        eng.push(torch.from_numpy(e).to(cuda))
+        eng.resort()
+        eng._record_status()
+        eng.sync()
+        res = _run_oracle_step(eng, live, e, 1)
+        nxt = []
+        for k, f in enumerate(live):
+            removed = res[k][1]
+            total_abs[k, 0] += int((removed == 1).sum())
+            total_abs[k, 1] += int((removed == 2).sum())
+            keep = removed == 0
+            from paper_2404_10270_b200.core import FlatSpecies
+            nxt.append(FlatSpecies(*(None if a is None else a[keep].copy()
+                                     for a in (f.x, f.vx, f.vy, f.vz, f.yp, f.cell))))
+        live = nxt
+        dev = eng.download()
+        for k in range(3):
+            assert dev[k].n == live[k].n
+            a = oracle.canonical(dev[k].cell, dev[k].fields())
+            b = oracle.canonical(live[k].cell, live[k].fields())
+            assert np.array_equal(a, b)
+        assert np.array_equal(eng.absorbed, total_abs)
+    assert total_abs.sum() > 0
+
+
+def test_boris_bitwise_and_speed_conservation(cuda):
+    import torch
+
+    from paper_2404_10270_b200 import Engine
+
+    cfg = _mk_config(b_field_t=(0.3, 0.0, 2.0))
+    eng = Engine(cfg, device=cuda, check_every=0)
+    flats = _random_flats(cfg, seed=9, vscale=0.05)
+    eng.upload(flats)
+    e = np.zeros(eng.nc + 1)
+    speed0 = [np.sqrt(f.vx ** 2 + f.vy ** 2 + f.vz ** 2) for f in flats]
+    for _ in range(20):
+        eng.push(torch.from_numpy(e).to(cuda))
+        eng.resort()
+        _run_oracle_step(eng, flats, e, 0)
+    dev = eng.download()
+    for k in range(3):
+        _compare_arrays(dev[k], flats[k])
+    # pure magnetic rotation conserves |v| to rounding (20 steps)
+    for k in (0, 1):
+        sp = np.sqrt(dev[k].vx ** 2 + dev[k].vy ** 2 + dev[k].vz ** 2)
+        assert np.allclose(sp, speed0[k], rtol=1e-13, atol=0)
+    assert not bits_equal(dev[0].vy, speed0[0])  # it did rotate
+
+
+def test_cfl_violation_raises(cuda):
+    import torch
+
+    from paper_2404_10270_b200 import CflViolation, Engine
+
+    cfg = _mk_config(nc=8, ppc0=2)
+    eng = Engine(cfg, device=cuda, check_every=0)
+    flats = _random_flats(cfg, seed=1, vscale=0.0)
+    flats[2].vx[5] = 9.0 / 3.0  # neutral, nstep 3 -> displacement 9 cells on nc=8
+    eng.upload(flats)
+    eng.push(torch.zeros(9, dtype=torch.float64, device=cuda))
+    eng._record_status()
+    with pytest.raises(CflViolation, match="whole domain"):
+        eng.sync()
+
+
+def test_free_streaming_exact_1000_steps(cuda):
+    """Criterion 08 (pkg/tests/test_acceptance.py:355-411) on the device:
+    dyadic positions/velocities, E = 0, closed form with zero tolerance."""
+    from paper_2404_10270_b200 import Engine, SpeciesDef
+    from paper_2404_10270_b200.core import DEUTERIUM_MASS, ELECTRON_MASS, ELEMENTARY_CHARGE, FlatSpecies
+
+    M = 1 << 20
+    nc, ppc, n_steps = 32, 4, 1000
+    species = [SpeciesDef("e", -ELEMENTARY_CHARGE, ELECTRON_MASS),
+               SpeciesDef("g", 0.0, DEUTERIUM_MASS, nstep=3)]
+    cfg = _mk_config(nc=nc, ppc0=ppc, species=species, temperatures_ev=[1.0, 1.0],
+                     densities_m3=[1e21, 1e21], sort_every=97)
+    eng = Engine(cfg, device=cuda, check_every=0)
+    rng = np.random.default_rng(41)
+    flats, starts, tag = [], {}, 0
+    for isp in range(2):
+        xs, vs, tags, cells = [], [], [], []
+        for j in range(nc):
+            for _ in range(ppc):
+                xi = int(rng.integers(0, M))
+                vi = int(rng.integers(-(1 << 14), 1 << 14)) or 7
+                xs.append(xi / M)
+                vs.append(vi / M)
+                tags.append(float(tag))
+                cells.append(j)
+                starts[tag] = (isp, j * M + xi, vi)
+                tag += 1
+        n = len(xs)
+        flats.append(FlatSpecies(np.array(xs), np.array(vs), np.zeros(n), np.array(tags), None,
+                                 np.array(cells, dtype=np.int32)))
+    eng.upload(flats)
+    for _ in range(n_steps):
+        eng.push()
+        eng.resort()
+        eng.step_index += 1
+    eng._record_status()
+    eng.sync()
+    dev = eng.download()
+    checked = 0
+    for isp in range(2):
+        nstep = species[isp].nstep
+        for x, vx, t, j in zip(dev[isp].x, dev[isp].vx, dev[isp].vz, dev[isp].cell):
+            isp0, pos0, vi = starts[int(t)]
+            assert isp0 == isp
+            assert int(j) * M + int(x * M) == (pos0 + n_steps * nstep * vi) % (nc * M)
+            assert vx == vi / M
+            checked += 1
+    assert checked == 2 * nc * ppc
+
+
+def test_sort_by_cell_preserves_particles(cuda):
+    import torch
+
+    from oracle import oracle
+    from paper_2404_10270_b200 import Engine
+
+    cfg = _mk_config(nc=200, ppc0=50)
+    eng = Engine(cfg, device=cuda, check_every=0)
+    flats = _random_flats(cfg, seed=12, vscale=3.0)
+    eng.upload(flats)
+    for _ in range(3):
+        eng.push(torch.zeros(eng.nc + 1, dtype=torch.float64, device=cuda))
+    before = eng.download()
+    eng.sort_by_cell()
+    after = eng.download()
+    for b, a in zip(before, after):
+        assert np.all(np.diff(a.cell) >= 0)
+        assert np.array_equal(oracle.canonical(b.cell, b.fields()), oracle.canonical(a.cell, a.fields()))
+
+
+def test_device_init_positions_bitexact(cuda):
+    from paper_2404_10270_b200 import Engine
+    from paper_2404_10270_b200.core import init_species_host
+
+    cfg = _mk_config(nc=300, ppc0=16)
+    eng = Engine(cfg, device=cuda, init="device", check_every=0)
+    dev = eng.download()
+    for k in range(3):
+        host = init_species_host(cfg, k)
+        assert bits_equal(dev[k].x, host.x)
+        assert np.array_equal(dev[k].cell, host.cell)
+        for f in ("vx", "vy", "vz"):
+            np.testing.assert_allclose(getattr(dev[k], f), getattr(host, f), rtol=1e-12, atol=1e-300)
+
+
+def test_step_deposit_is_order_and_sort_independent(cuda):
+    from paper_2404_10270_b200 import Engine
+
+    hist = {}
+    for sort_every in (0, 3):
+        cfg = _mk_config(nc=500, ppc0=40, sort_every=sort_every, field_solve=True, smoothing_passes=1)
+        eng = Engine(cfg, device=cuda, check_every=0)
+        h = []
+        for _ in range(10):
+            rho, _ = eng.step()
+            h.append(rho.cpu().numpy().copy())
+        hist[sort_every] = h
+    for a, b in zip(hist[0], hist[3]):
+        assert bits_equal(a, b)
+
+
+def test_large_c2_shape_conservation(cuda):
+    """Full-size property check at config 2's per-species shape (nc=100K,
+    ppc=100): counts conserved and every particle deposited exactly once."""
+    import torch
+
+    from paper_2404_10270_b200 import Engine
+
+    cfg = _mk_config(nc=100_000, ppc0=100, max_store_mb=65536)
+    eng = Engine(cfg, device=cuda, init="device", check_every=0)
+    for _ in range(5):
+        eng.step()
+    eng.sync()
+    bins = eng.bins.cpu().numpy().view(np.uint64).reshape(eng.ndep, 2, eng.nc)
+    assert int(bins[:, 1].sum()) == 2 * 10_000_000
+    dev = eng.download()
+    for f in dev:
+        assert f.n == 10_000_000
+        assert np.all((f.x >= 0.0) & (f.x < 1.0))
+        assert np.all((f.cell >= 0) & (f.cell < eng.nc))
+    # the packed counts of the fixed-point bins equal the per-cell histogram
+    counts = np.bincount(dev[0].cell, minlength=eng.nc)
+    assert np.array_equal(bins[0, 1], counts.astype(np.uint64))
