@@ -142,7 +142,7 @@ def committed_traffic():
 # ---------------------------------------------------------------------------
 # CPU side: the reference's own compiled kernels (oracle/_ref, built from
 # /root/reference sources) timed on this host's cores.
-def cpu_reference_rate(target_seconds=15.0, nc=20_000, ppc=PPC0, threads=None, log=None):
+def cpu_reference_rate(target_seconds=15.0, nc=NC_PER_GPU, ppc=PPC0, threads=None, log=None):
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle import oracle
@@ -194,7 +194,7 @@ def cpu_reference_rate(target_seconds=15.0, nc=20_000, ppc=PPC0, threads=None, l
             list(pool.map(dep, tasks_d))
             reps += 1
             el = time.perf_counter() - t0
-            if el >= target_seconds or reps >= 200:
+            if el >= target_seconds or reps >= 100000:
                 break
     rate = pushes * reps / el
     sample = (f"{reps} steps x {pushes / 1e6:.1f}M pushes (e-, D+, D desk mix, nc={nc}, ppc={ppc}, cap={cap}) "
@@ -219,27 +219,31 @@ def run_ours(args, rank, world, local_rank):
     pushes_rank = sum(s.n for s in eng.sp if s.kind != 0)
     alg_bytes = sum(s.n * species_alg_bytes(s.sp) for s in eng.sp)
 
-    for _ in range(args.warmup):
-        eng.step()
+    # Warm-up doubles as graph capture: one CUDA graph per step (epilogue +
+    # mover), replayed back to back; periodic sorts run eagerly.
+    eng.replay(args.warmup)
     eng.sync()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    eng.phase_events.clear()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         time.sleep(0.3)
         start.record(eng.stream)
-        for _ in range(args.steps):
-            eng.step(timed=True)
+        eng.replay(args.steps)
         end.record(eng.stream)
         torch.cuda.synchronize(dev)
     eng.sync()
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(end) / args.steps
-    mover_ms = [ev[2].elapsed_time(ev[3]) for ev in eng.phase_events]
-    push_ms = float(np.mean(mover_ms))
+    # The mover kernel alone: CUDA events on the engine stream right around the
+    # pb_push_deposit launch, over eager steps (host stays ahead of the GPU).
+    eng.phase_events.clear()
+    for _ in range(min(args.steps, 20)):
+        eng.step(timed=True)
+    eng.sync()
+    push_ms = float(np.mean(eng.mover_ms()))
     if world > 1:
         t = torch.tensor([ms, push_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

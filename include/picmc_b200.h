@@ -89,7 +89,10 @@ typedef struct pb_status {
   int64_t absorbed[PB_MAX_SPECIES][2];  /* [left wall, right wall]      */
   int64_t n_holes[PB_MAX_SPECIES];      /* absorbed slots to compact    */
   int64_t overflow;                     /* deposit bins over capacity   */
+  uint64_t tile_next;                   /* work counter of the TMA mover */
 } pb_status;
+/* The caller resets *status before each pb_push_deposit: all zero except
+ * cfl_index = UINT64_MAX (the engine copies a template). */
 
 /* ---- library ------------------------------------------------------------ */
 int pb_abi_version(void);

@@ -17,6 +17,7 @@
 //   yp = yp + fnstep*vy
 // with aj = coef*E[j] (accel_nodes_for_species, pkg/src/picmc/mover.py:221).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -35,6 +36,8 @@ struct LaunchArgs {
   int id[PB_MAX_SPECIES];  // caller species index (status arrays)
   int nsp;
   int push;  // 0: deposit only (no mover)
+  int order[PB_MAX_SPECIES];             // TMA kernel: species order of the tile list
+  int64_t tile_start[PB_MAX_SPECIES + 1];  // TMA kernel: prefix of full tiles
   const double *e;
   int64_t nc;
   uint64_t *bins;
@@ -138,6 +141,7 @@ struct Window {
   uint64_t *sR;
   uint32_t *sC;
   int64_t base;
+  int64_t lim;  // window width in use (0: global atomics only)
   uint64_t *gR;
   uint64_t *gC;
 
@@ -145,7 +149,7 @@ struct Window {
     const uint64_t r = w & kRMask;
     const uint32_t c = (uint32_t)(w >> kCountShift);
     const int64_t b = (int64_t)key - base;
-    if (b >= 0 && b < kWin) {
+    if (b >= 0 && b < lim) {
       atomicAdd((unsigned long long *)&sR[b], (unsigned long long)r);
       atomicAdd(&sC[b], c);
     } else {
@@ -199,160 +203,175 @@ struct Tally {
   int absorbed[2] = {0, 0};
 };
 
+// Register image of two consecutive particles.
+struct Pair {
+  double x0 = 0, x1 = 0, vx0 = 0, vx1 = 0, vy0 = 0, vy1 = 0, vz0 = 0, vz1 = 0,
+         y0 = 0, y1 = 0;
+  int32_t c0 = -1, c1 = -1;
+};
+
+template <int KIND, bool YP>
+struct Fields {
+  static constexpr bool kNeedV = (KIND == PB_KIND_KICK || KIND == PB_KIND_BORIS ||
+                                  KIND == PB_KIND_DRIFT);
+  static constexpr bool kVy = YP || KIND == PB_KIND_BORIS;
+  static constexpr bool kVz = KIND == PB_KIND_BORIS;
+};
+
+// Push, cell transfer, stores, tallies and deposit for particles i, i+1
+// (v0/v1: which of them exist).  Warp-collective when BC == ABSORBING or
+// DEP: every lane of the warp must call it.
+template <int KIND, bool YP, int BC, bool PUSH, bool DEP>
+__device__ __forceinline__ void handle_pair(const LaunchArgs &a,
+                                            const pb_species &s, int sid,
+                                            int64_t i, bool v0, bool v1,
+                                            Pair &q, const Window &win,
+                                            Tally &t) {
+  const unsigned full = 0xffffffffu;
+  const int64_t nc = a.nc;
+  constexpr bool kEagerCell = (KIND != PB_KIND_DRIFT) || DEP;
+  int32_t n0 = q.c0, n1 = q.c1;
+  if (PUSH) {
+    bool m0 = false, m1 = false, cfl0 = false, cfl1 = false;
+    int8_t w0 = -1, w1 = -1;
+    if (v0) {
+      kick_drift<KIND>(q.x0, q.vx0, q.vy0, q.vz0, q.c0, s, a.e);
+      if (YP) q.y0 = __dadd_rn(q.y0, __dmul_rn(s.fnstep, q.vy0));
+      if (!kEagerCell && floor(q.x0) != 0.0) q.c0 = s.cell[i];
+      const MoveOut o = transfer<BC>(q.x0, q.c0, nc);
+      n0 = o.cell;
+      m0 = o.moved;
+      w0 = o.wall;
+      cfl0 = o.cfl;
+    }
+    if (v1) {
+      kick_drift<KIND>(q.x1, q.vx1, q.vy1, q.vz1, q.c1, s, a.e);
+      if (YP) q.y1 = __dadd_rn(q.y1, __dmul_rn(s.fnstep, q.vy1));
+      if (!kEagerCell && floor(q.x1) != 0.0) q.c1 = s.cell[i + 1];
+      const MoveOut o = transfer<BC>(q.x1, q.c1, nc);
+      n1 = o.cell;
+      m1 = o.moved;
+      w1 = o.wall;
+      cfl1 = o.cfl;
+    }
+    double *X = s.x, *VX = s.vx, *VY = s.vy, *VZ = s.vz, *YPp = s.yp;
+    if (v1) {
+      __stcs(reinterpret_cast<double2 *>(X + i), make_double2(q.x0, q.x1));
+      if (KIND != PB_KIND_DRIFT)
+        __stcs(reinterpret_cast<double2 *>(VX + i), make_double2(q.vx0, q.vx1));
+      if (KIND == PB_KIND_BORIS) {
+        __stcs(reinterpret_cast<double2 *>(VY + i), make_double2(q.vy0, q.vy1));
+        __stcs(reinterpret_cast<double2 *>(VZ + i), make_double2(q.vz0, q.vz1));
+      }
+      if (YP) __stcs(reinterpret_cast<double2 *>(YPp + i), make_double2(q.y0, q.y1));
+    } else if (v0) {
+      X[i] = q.x0;
+      if (KIND != PB_KIND_DRIFT) VX[i] = q.vx0;
+      if (KIND == PB_KIND_BORIS) {
+        VY[i] = q.vy0;
+        VZ[i] = q.vz0;
+      }
+      if (YP) YPp[i] = q.y0;
+    }
+    if (m0) s.cell[i] = n0;
+    if (m1) s.cell[i + 1] = n1;
+    t.moved += (int)m0 + (int)m1;
+    if (BC == PB_BC_ABSORBING) {
+      t.absorbed[0] += (int)(w0 == 0) + (int)(w1 == 0);
+      t.absorbed[1] += (int)(w0 == 1) + (int)(w1 == 1);
+      // Warp-ballot stream compaction of removed slots into the hole list.
+      const bool r0 = w0 >= 0, r1 = w1 >= 0;
+      const unsigned b0 = __ballot_sync(full, r0);
+      const unsigned b1 = __ballot_sync(full, r1);
+      const int tot = __popc(b0) + __popc(b1);
+      if (tot) {
+        const unsigned lane = lane_id();
+        unsigned long long base = 0;
+        if (lane == 0)
+          base = atomicAdd((unsigned long long *)&a.st->n_holes[sid], (unsigned long long)tot);
+        base = __shfl_sync(full, base, 0);
+        const unsigned lt = (1u << lane) - 1u;
+        if (r0) s.holes[base + __popc(b0 & lt)] = i;
+        if (r1) s.holes[base + __popc(b0) + __popc(b1 & lt)] = i + 1;
+      }
+    }
+    if (cfl0 || cfl1) {
+      const uint64_t key = ((uint64_t)sid << 56) | (uint64_t)(cfl0 ? i : i + 1);
+      atomicMin((unsigned long long *)&a.st->cfl_index, (unsigned long long)key);
+      atomicCAS(&a.st->code, PB_OK, PB_ERR_CFL);
+      if (cfl0) n0 = -1;
+      if (cfl1) n1 = -1;
+    }
+  }
+  if (DEP) deposit_pair(v0 ? n0 : -1, q.x0, v1 ? n1 : -1, q.x1, win);
+}
+
+// LDG path: used for chunk tails, deposit-only launches and PB_PUSH_PATH=ldg.
+// Consumer threads only (threadIdx.x < kThreads).
 template <int KIND, bool YP, int BC, bool PUSH, bool DEP>
 __device__ __forceinline__ void process_chunk(const LaunchArgs &a, int isp,
                                               int64_t beg, int64_t end,
                                               const Window &win, Tally &t) {
+  using F = Fields<KIND, YP>;
   const pb_species &s = a.sp[isp];
   const int sid = a.id[isp];
-  double *__restrict__ X = s.x;
-  double *__restrict__ VX = s.vx;
-  double *__restrict__ VY = s.vy;
-  double *__restrict__ VZ = s.vz;
-  double *__restrict__ YPp = s.yp;
-  int32_t *__restrict__ CELL = s.cell;
-  const int64_t nc = a.nc;
-  const unsigned full = 0xffffffffu;
-  constexpr bool kNeedV = (KIND == PB_KIND_KICK || KIND == PB_KIND_BORIS ||
-                           KIND == PB_KIND_DRIFT);
-  constexpr bool kNeedVyz = (KIND == PB_KIND_BORIS);
-  // Charged kinds need the cell for the gather; drift species only for movers.
   constexpr bool kEagerCell = (KIND != PB_KIND_DRIFT) || DEP;
-
   for (int64_t tb = beg; tb < end; tb += kTile) {
 #pragma unroll
     for (int p = 0; p < kPairsPerThread; ++p) {
       const int64_t i = tb + (int64_t)p * (2 * kThreads) + 2 * threadIdx.x;
       const bool v0 = i < end;
       const bool v1 = (i + 1) < end;
-      double x0 = 0, x1 = 0, vx0 = 0, vx1 = 0, vy0 = 0, vy1 = 0, vz0 = 0,
-             vz1 = 0, y0 = 0, y1 = 0;
-      int32_t c0 = -1, c1 = -1;
+      Pair q;
       if (v1) {
-        const double2 xx = __ldcs(reinterpret_cast<const double2 *>(X + i));
-        x0 = xx.x;
-        x1 = xx.y;
-        if (PUSH && kNeedV) {
-          const double2 vv = __ldcs(reinterpret_cast<const double2 *>(VX + i));
-          vx0 = vv.x;
-          vx1 = vv.y;
+        const double2 xx = __ldcs(reinterpret_cast<const double2 *>(s.x + i));
+        q.x0 = xx.x;
+        q.x1 = xx.y;
+        if (PUSH && F::kNeedV) {
+          const double2 v = __ldcs(reinterpret_cast<const double2 *>(s.vx + i));
+          q.vx0 = v.x;
+          q.vx1 = v.y;
         }
-        if (PUSH && (YP || kNeedVyz)) {
-          const double2 vv = __ldcs(reinterpret_cast<const double2 *>(VY + i));
-          vy0 = vv.x;
-          vy1 = vv.y;
+        if (PUSH && F::kVy) {
+          const double2 v = __ldcs(reinterpret_cast<const double2 *>(s.vy + i));
+          q.vy0 = v.x;
+          q.vy1 = v.y;
         }
-        if (PUSH && kNeedVyz) {
-          const double2 vv = __ldcs(reinterpret_cast<const double2 *>(VZ + i));
-          vz0 = vv.x;
-          vz1 = vv.y;
+        if (PUSH && F::kVz) {
+          const double2 v = __ldcs(reinterpret_cast<const double2 *>(s.vz + i));
+          q.vz0 = v.x;
+          q.vz1 = v.y;
         }
         if (PUSH && YP) {
-          const double2 vv = __ldcs(reinterpret_cast<const double2 *>(YPp + i));
-          y0 = vv.x;
-          y1 = vv.y;
+          const double2 v = __ldcs(reinterpret_cast<const double2 *>(s.yp + i));
+          q.y0 = v.x;
+          q.y1 = v.y;
         }
         if (kEagerCell) {
-          const int2 cc = __ldcs(reinterpret_cast<const int2 *>(CELL + i));
-          c0 = cc.x;
-          c1 = cc.y;
+          const int2 c = __ldcs(reinterpret_cast<const int2 *>(s.cell + i));
+          q.c0 = c.x;
+          q.c1 = c.y;
         }
       } else if (v0) {
-        x0 = X[i];
-        if (PUSH && kNeedV) vx0 = VX[i];
-        if (PUSH && (YP || kNeedVyz)) vy0 = VY[i];
-        if (PUSH && kNeedVyz) vz0 = VZ[i];
-        if (PUSH && YP) y0 = YPp[i];
-        if (kEagerCell) c0 = CELL[i];
+        q.x0 = s.x[i];
+        if (PUSH && F::kNeedV) q.vx0 = s.vx[i];
+        if (PUSH && F::kVy) q.vy0 = s.vy[i];
+        if (PUSH && F::kVz) q.vz0 = s.vz[i];
+        if (PUSH && YP) q.y0 = s.yp[i];
+        if (kEagerCell) q.c0 = s.cell[i];
       }
-
-      bool m0 = false, m1 = false, cfl0 = false, cfl1 = false;
-      int8_t w0 = -1, w1 = -1;
-      int32_t n0 = c0, n1 = c1;
-      if (PUSH) {
-        if (v0) {
-          kick_drift<KIND>(x0, vx0, vy0, vz0, c0, s, a.e);
-          if (YP) y0 = __dadd_rn(y0, __dmul_rn(s.fnstep, vy0));
-          if (!kEagerCell && floor(x0) != 0.0) c0 = CELL[i];
-          const MoveOut o = transfer<BC>(x0, c0, nc);
-          n0 = o.cell;
-          m0 = o.moved;
-          w0 = o.wall;
-          cfl0 = o.cfl;
-        }
-        if (v1) {
-          kick_drift<KIND>(x1, vx1, vy1, vz1, c1, s, a.e);
-          if (YP) y1 = __dadd_rn(y1, __dmul_rn(s.fnstep, vy1));
-          if (!kEagerCell && floor(x1) != 0.0) c1 = CELL[i + 1];
-          const MoveOut o = transfer<BC>(x1, c1, nc);
-          n1 = o.cell;
-          m1 = o.moved;
-          w1 = o.wall;
-          cfl1 = o.cfl;
-        }
-        // Stores.
-        if (v1) {
-          __stcs(reinterpret_cast<double2 *>(X + i), make_double2(x0, x1));
-          if (KIND != PB_KIND_DRIFT)
-            __stcs(reinterpret_cast<double2 *>(VX + i), make_double2(vx0, vx1));
-          if (KIND == PB_KIND_BORIS) {
-            __stcs(reinterpret_cast<double2 *>(VY + i), make_double2(vy0, vy1));
-            __stcs(reinterpret_cast<double2 *>(VZ + i), make_double2(vz0, vz1));
-          }
-          if (YP) __stcs(reinterpret_cast<double2 *>(YPp + i), make_double2(y0, y1));
-        } else if (v0) {
-          X[i] = x0;
-          if (KIND != PB_KIND_DRIFT) VX[i] = vx0;
-          if (KIND == PB_KIND_BORIS) {
-            VY[i] = vy0;
-            VZ[i] = vz0;
-          }
-          if (YP) YPp[i] = y0;
-        }
-        if (m0) CELL[i] = n0;
-        if (m1) CELL[i + 1] = n1;
-        t.moved += (int)m0 + (int)m1;
-        if (BC == PB_BC_ABSORBING) {
-          t.absorbed[0] += (int)(w0 == 0) + (int)(w1 == 0);
-          t.absorbed[1] += (int)(w0 == 1) + (int)(w1 == 1);
-          // Warp-ballot stream compaction of removed slots into the hole list.
-          const bool r0 = w0 >= 0, r1 = w1 >= 0;
-          const unsigned b0 = __ballot_sync(full, r0);
-          const unsigned b1 = __ballot_sync(full, r1);
-          const int tot = __popc(b0) + __popc(b1);
-          if (tot) {
-            const unsigned lane = lane_id();
-            unsigned long long base = 0;
-            if (lane == 0)
-              base = atomicAdd((unsigned long long *)&a.st->n_holes[sid],
-                               (unsigned long long)tot);
-            base = __shfl_sync(full, base, 0);
-            const unsigned lt = (1u << lane) - 1u;
-            if (r0) s.holes[base + __popc(b0 & lt)] = i;
-            if (r1) s.holes[base + __popc(b0) + __popc(b1 & lt)] = i + 1;
-          }
-        }
-        if (cfl0 || cfl1) {
-          const uint64_t key =
-              ((uint64_t)sid << 56) | (uint64_t)(cfl0 ? i : i + 1);
-          atomicMin((unsigned long long *)&a.st->cfl_index,
-                    (unsigned long long)key);
-          atomicCAS(&a.st->code, PB_OK, PB_ERR_CFL);
-          if (cfl0) n0 = -1;
-          if (cfl1) n1 = -1;
-        }
-      }
-      if (DEP) {
-        deposit_pair(v0 ? n0 : -1, x0, v1 ? n1 : -1, x1, win);
-      }
+      handle_pair<KIND, YP, BC, PUSH, DEP>(a, s, sid, i, v0, v1, q, win, t);
     }
   }
 }
 
+// ---------------------------------------------------------------------------
+// LDG kernel: static contiguous chunks per block, shared-memory deposit
+// window.  Used for deposit-only launches and as the PB_PUSH_PATH=ldg mover.
+// ---------------------------------------------------------------------------
 template <int KIND, bool YP, int BC, bool PUSH>
-__device__ __forceinline__ void dispatch_dep(const LaunchArgs &a, int isp,
-                                             int64_t beg, int64_t end,
-                                             const Window &win, Tally &t,
+__device__ __forceinline__ void ldg_dispatch(const LaunchArgs &a, int isp, int64_t beg,
+                                             int64_t end, const Window &win, Tally &t,
                                              bool dep) {
   if (dep)
     process_chunk<KIND, YP, BC, PUSH, true>(a, isp, beg, end, win, t);
@@ -361,13 +380,54 @@ __device__ __forceinline__ void dispatch_dep(const LaunchArgs &a, int isp,
 }
 
 template <int BC, bool PUSH>
+__device__ __forceinline__ void run_any(const LaunchArgs &a, int isp, int64_t beg, int64_t end,
+                                        const Window &win, Tally &t, bool dep) {
+  const pb_species &s = a.sp[isp];
+  const bool yp = s.yp != nullptr;
+  const int kind = PUSH ? s.kind : PB_KIND_INACTIVE;
+  switch (kind) {
+    case PB_KIND_KICK:
+      if (yp) ldg_dispatch<PB_KIND_KICK, true, BC, PUSH>(a, isp, beg, end, win, t, dep);
+      else ldg_dispatch<PB_KIND_KICK, false, BC, PUSH>(a, isp, beg, end, win, t, dep);
+      break;
+    case PB_KIND_BORIS:
+      if (yp) ldg_dispatch<PB_KIND_BORIS, true, BC, PUSH>(a, isp, beg, end, win, t, dep);
+      else ldg_dispatch<PB_KIND_BORIS, false, BC, PUSH>(a, isp, beg, end, win, t, dep);
+      break;
+    case PB_KIND_DRIFT:
+      if (yp) ldg_dispatch<PB_KIND_DRIFT, true, BC, PUSH>(a, isp, beg, end, win, t, dep);
+      else ldg_dispatch<PB_KIND_DRIFT, false, BC, PUSH>(a, isp, beg, end, win, t, dep);
+      break;
+    default:  // not pushed: deposit current positions only
+      if (dep) process_chunk<PB_KIND_INACTIVE, false, BC, false, true>(a, isp, beg, end, win, t);
+      break;
+  }
+}
+
+// Block reduction of the tallies into the step status (all threads call).
+__device__ __forceinline__ void flush_tally(const LaunchArgs &a, int sid, const Tally &t,
+                                            int *sTally) {
+  int mv = t.moved, al = t.absorbed[0], ar = t.absorbed[1];
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    mv += __shfl_down_sync(0xffffffffu, mv, d);
+    al += __shfl_down_sync(0xffffffffu, al, d);
+    ar += __shfl_down_sync(0xffffffffu, ar, d);
+  }
+  if (lane_id() == 0) {
+    if (mv) atomicAdd((unsigned long long *)&a.st->moved[sid], (unsigned long long)mv);
+    if (al) atomicAdd((unsigned long long *)&a.st->absorbed[sid][0], (unsigned long long)al);
+    if (ar) atomicAdd((unsigned long long *)&a.st->absorbed[sid][1], (unsigned long long)ar);
+  }
+  (void)sTally;
+}
+
+template <int BC, bool PUSH>
 __global__ void __launch_bounds__(kThreads)
     k_push_deposit(const __grid_constant__ LaunchArgs a) {
   __shared__ uint64_t sR[kWin];
   __shared__ uint32_t sC[kWin];
-  __shared__ int sTally[3];
 
-  // Which species does this block serve?
   int isp = 0;
   while (isp + 1 < a.nsp && (int)blockIdx.x >= a.blk_start[isp + 1]) ++isp;
   const pb_species &s = a.sp[isp];
@@ -385,66 +445,17 @@ __global__ void __launch_bounds__(kThreads)
     sR[b] = 0;
     sC[b] = 0;
   }
-  if (threadIdx.x < 3) sTally[threadIdx.x] = 0;
-  Window win;
-  win.sR = sR;
-  win.sC = sC;
-  win.base = 0;
-  win.gR = nullptr;
-  win.gC = nullptr;
+  Window win{sR, sC, 0, kWin, nullptr, nullptr};
   if (dep) {
     win.gR = a.bins + (size_t)s.deposit * 2 * (size_t)a.nc;
     win.gC = win.gR + a.nc;
     win.base = (int64_t)s.cell[beg] - kMargin;
   }
   __syncthreads();
-
   Tally t;
-  const bool yp = s.yp != nullptr;
-  const int kind = PUSH ? s.kind : PB_KIND_INACTIVE;
-  switch (kind) {
-    case PB_KIND_KICK:
-      if (yp) dispatch_dep<PB_KIND_KICK, true, BC, PUSH>(a, isp, beg, end, win, t, dep);
-      else dispatch_dep<PB_KIND_KICK, false, BC, PUSH>(a, isp, beg, end, win, t, dep);
-      break;
-    case PB_KIND_BORIS:
-      if (yp) dispatch_dep<PB_KIND_BORIS, true, BC, PUSH>(a, isp, beg, end, win, t, dep);
-      else dispatch_dep<PB_KIND_BORIS, false, BC, PUSH>(a, isp, beg, end, win, t, dep);
-      break;
-    case PB_KIND_DRIFT:
-      if (yp) dispatch_dep<PB_KIND_DRIFT, true, BC, PUSH>(a, isp, beg, end, win, t, dep);
-      else dispatch_dep<PB_KIND_DRIFT, false, BC, PUSH>(a, isp, beg, end, win, t, dep);
-      break;
-    default:  // not pushed: deposit current positions only
-      if (dep)
-        process_chunk<PB_KIND_INACTIVE, false, BC, false, true>(a, isp, beg, end, win, t);
-      break;
-  }
-
-  // Block reductions of the tallies and the shared-memory window flush.
-  if (PUSH) {
-    int mv = t.moved, al = t.absorbed[0], ar = t.absorbed[1];
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-      mv += __shfl_down_sync(0xffffffffu, mv, d);
-      al += __shfl_down_sync(0xffffffffu, al, d);
-      ar += __shfl_down_sync(0xffffffffu, ar, d);
-    }
-    if (lane_id() == 0) {
-      if (mv) atomicAdd(&sTally[0], mv);
-      if (al) atomicAdd(&sTally[1], al);
-      if (ar) atomicAdd(&sTally[2], ar);
-    }
-  }
+  run_any<BC, PUSH>(a, isp, beg, end, win, t, dep);
+  if (PUSH) flush_tally(a, a.id[isp], t, nullptr);
   __syncthreads();
-  if (PUSH && threadIdx.x == 0) {
-    if (sTally[0])
-      atomicAdd((unsigned long long *)&a.st->moved[a.id[isp]], (unsigned long long)sTally[0]);
-    if (sTally[1])
-      atomicAdd((unsigned long long *)&a.st->absorbed[a.id[isp]][0], (unsigned long long)sTally[1]);
-    if (sTally[2])
-      atomicAdd((unsigned long long *)&a.st->absorbed[a.id[isp]][1], (unsigned long long)sTally[2]);
-  }
   if (dep) {
     for (int b = threadIdx.x; b < kWin; b += kThreads) {
       const uint32_t c = sC[b];
@@ -458,36 +469,297 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------------------
+// TMA kernel (the production mover).  Persistent: one or two blocks per SM.
+// A producer warp pulls tiles (1024 particles of one species) from a global
+// work counter -- a single list over all species, heaviest species first --
+// and streams each tile's arrays into a kStages-deep shared-memory ring with
+// 1-D bulk copies (cp.async.bulk, mbarrier complete_tx).  Eight consumer
+// warps compute from shared memory, store results straight to HBM and
+// deposit through warp-aggregated global atomics.  Dynamic tiles keep every
+// SM busy to the end regardless of the per-species cost mix, and the bytes in
+// flight are set by the ring depth instead of by registers.
+// ---------------------------------------------------------------------------
+constexpr int kStages = 3;
+constexpr int kConsumerWarps = kThreads / 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int KIND, bool YP>
+struct Stage {
+  using F = Fields<KIND, YP>;
+  static constexpr bool kCell = KIND != PB_KIND_DRIFT;
+  static constexpr int kX = 0;
+  static constexpr int kVX = kX + kTile * 8;
+  static constexpr int kVY = kVX + kTile * 8;
+  static constexpr int kVZ = kVY + (F::kVy ? kTile * 8 : 0);
+  static constexpr int kYP = kVZ + (F::kVz ? kTile * 8 : 0);
+  static constexpr int kCELL = kYP + (YP ? kTile * 8 : 0);
+  static constexpr int kBytes = kCELL + (kCell ? kTile * 4 : 0);
+};
+
+__host__ __device__ constexpr int stage_bytes(int kind, bool yp) {
+  return kind == PB_KIND_KICK ? (yp ? Stage<PB_KIND_KICK, true>::kBytes : Stage<PB_KIND_KICK, false>::kBytes)
+       : kind == PB_KIND_BORIS ? (yp ? Stage<PB_KIND_BORIS, true>::kBytes : Stage<PB_KIND_BORIS, false>::kBytes)
+       : kind == PB_KIND_DRIFT ? (yp ? Stage<PB_KIND_DRIFT, true>::kBytes : Stage<PB_KIND_DRIFT, false>::kBytes)
+       : 0;
+}
+
+template <int KIND, bool YP>
+__device__ __forceinline__ void produce_tile(const pb_species &s, int64_t base, unsigned char *buf,
+                                             uint64_t *bar) {
+  using L = Stage<KIND, YP>;
+  using F = Fields<KIND, YP>;
+  mbar_expect_tx(bar, (uint32_t)L::kBytes);
+  tma_load_1d(buf + L::kX, s.x + base, kTile * 8, bar);
+  tma_load_1d(buf + L::kVX, s.vx + base, kTile * 8, bar);
+  if (F::kVy) tma_load_1d(buf + L::kVY, s.vy + base, kTile * 8, bar);
+  if (F::kVz) tma_load_1d(buf + L::kVZ, s.vz + base, kTile * 8, bar);
+  if (YP) tma_load_1d(buf + L::kYP, s.yp + base, kTile * 8, bar);
+  if (L::kCell) tma_load_1d(buf + L::kCELL, s.cell + base, kTile * 4, bar);
+}
+
+template <int KIND, bool YP, int BC, bool DEP>
+__device__ __forceinline__ void consume_tile(const LaunchArgs &a, int isp, int64_t base,
+                                             const unsigned char *buf, const Window &win,
+                                             Tally &t) {
+  using L = Stage<KIND, YP>;
+  using F = Fields<KIND, YP>;
+  const pb_species &s = a.sp[isp];
+  const int sid = a.id[isp];
+#pragma unroll
+  for (int p = 0; p < kPairsPerThread; ++p) {
+    const int li = p * (2 * kThreads) + 2 * threadIdx.x;
+    Pair q;
+    const double2 xx = *reinterpret_cast<const double2 *>(buf + L::kX + li * 8);
+    q.x0 = xx.x;
+    q.x1 = xx.y;
+    const double2 vv = *reinterpret_cast<const double2 *>(buf + L::kVX + li * 8);
+    q.vx0 = vv.x;
+    q.vx1 = vv.y;
+    if (F::kVy) {
+      const double2 v = *reinterpret_cast<const double2 *>(buf + L::kVY + li * 8);
+      q.vy0 = v.x;
+      q.vy1 = v.y;
+    }
+    if (F::kVz) {
+      const double2 v = *reinterpret_cast<const double2 *>(buf + L::kVZ + li * 8);
+      q.vz0 = v.x;
+      q.vz1 = v.y;
+    }
+    if (YP) {
+      const double2 v = *reinterpret_cast<const double2 *>(buf + L::kYP + li * 8);
+      q.y0 = v.x;
+      q.y1 = v.y;
+    }
+    if (L::kCell) {
+      const int2 c = *reinterpret_cast<const int2 *>(buf + L::kCELL + li * 4);
+      q.c0 = c.x;
+      q.c1 = c.y;
+    }
+    handle_pair<KIND, YP, BC, true, DEP>(a, s, sid, base + li, true, true, q, win, t);
+  }
+}
+
+// Per-species kind dispatch for the TMA consumer / producer.
+template <int BC>
+__device__ __forceinline__ void consume_any(const LaunchArgs &a, int isp, int64_t base,
+                                            const unsigned char *buf, const Window &win,
+                                            Tally &t) {
+  const pb_species &s = a.sp[isp];
+  const bool yp = s.yp != nullptr;
+  const bool dep = s.deposit >= 0 && a.bins != nullptr;
+#define PB_C(K, Y)                                                       \
+  do {                                                                   \
+    if (dep) consume_tile<K, Y, BC, true>(a, isp, base, buf, win, t);    \
+    else consume_tile<K, Y, BC, false>(a, isp, base, buf, win, t);       \
+  } while (0)
+  switch (s.kind) {
+    case PB_KIND_KICK:
+      if (yp) PB_C(PB_KIND_KICK, true); else PB_C(PB_KIND_KICK, false);
+      break;
+    case PB_KIND_BORIS:
+      if (yp) PB_C(PB_KIND_BORIS, true); else PB_C(PB_KIND_BORIS, false);
+      break;
+    default:
+      if (yp) PB_C(PB_KIND_DRIFT, true); else PB_C(PB_KIND_DRIFT, false);
+      break;
+  }
+#undef PB_C
+}
+
+__device__ __forceinline__ void produce_any(const pb_species &s, int64_t base, unsigned char *buf,
+                                            uint64_t *bar) {
+  const bool yp = s.yp != nullptr;
+  switch (s.kind) {
+    case PB_KIND_KICK:
+      if (yp) produce_tile<PB_KIND_KICK, true>(s, base, buf, bar);
+      else produce_tile<PB_KIND_KICK, false>(s, base, buf, bar);
+      break;
+    case PB_KIND_BORIS:
+      if (yp) produce_tile<PB_KIND_BORIS, true>(s, base, buf, bar);
+      else produce_tile<PB_KIND_BORIS, false>(s, base, buf, bar);
+      break;
+    default:
+      if (yp) produce_tile<PB_KIND_DRIFT, true>(s, base, buf, bar);
+      else produce_tile<PB_KIND_DRIFT, false>(s, base, buf, bar);
+      break;
+  }
+}
+
+__device__ __forceinline__ int tile_species(const LaunchArgs &a, int64_t tile) {
+  int k = 0;
+  while (k + 1 < a.nsp && tile >= a.tile_start[k + 1]) ++k;
+  return a.order[k];
+}
+
+template <int BC>
+__global__ void __launch_bounds__(kThreads + 32)
+    k_push_tma(const __grid_constant__ LaunchArgs a, int stage_stride) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t bars[2 * kStages];
+  __shared__ int64_t hdr[kStages];
+  uint64_t *full = bars;
+  uint64_t *empty = bars + kStages;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kStages; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t total = a.tile_start[a.nsp];
+  const int warp = threadIdx.x >> 5;
+
+  if (warp == kConsumerWarps) {  // producer warp
+    if (lane_id() == 0) {
+      unsigned long long next = atomicAdd((unsigned long long *)&a.st->tile_next, 1ull);
+      for (int64_t k = 0;; ++k) {
+        const int st = (int)(k % kStages);
+        if (k >= kStages) mbar_wait(&empty[st], (uint32_t)(((k / kStages) - 1) & 1));
+        if ((int64_t)next >= total) {
+          hdr[st] = -1;
+          mbar_arrive(&full[st]);  // no bytes: completes the phase
+          break;
+        }
+        const int64_t tile = (int64_t)next;
+        next = atomicAdd((unsigned long long *)&a.st->tile_next, 1ull);
+        hdr[st] = tile;
+        const int isp = tile_species(a, tile);
+        int kk = 0;
+        while (a.order[kk] != isp) ++kk;
+        const int64_t base = (tile - a.tile_start[kk]) * kTile;
+        produce_any(a.sp[isp], base, ring + (size_t)st * stage_stride, &full[st]);
+      }
+    }
+  } else {  // consumer warps
+    Window win{nullptr, nullptr, 0, 0, nullptr, nullptr};
+    Tally t[PB_MAX_SPECIES > 4 ? 1 : 1];
+    int cur = -1;
+    for (int64_t k = 0;; ++k) {
+      const int st = (int)(k % kStages);
+      mbar_wait(&full[st], (uint32_t)((k / kStages) & 1));
+      const int64_t tile = hdr[st];
+      if (tile < 0) break;
+      const int isp = tile_species(a, tile);
+      int kk = 0;
+      while (a.order[kk] != isp) ++kk;
+      const int64_t base = (tile - a.tile_start[kk]) * kTile;
+      if (isp != cur) {
+        if (cur >= 0) flush_tally(a, a.id[cur], t[0], nullptr);
+        t[0] = Tally();
+        cur = isp;
+        const pb_species &s = a.sp[isp];
+        if (s.deposit >= 0 && a.bins) {
+          win.gR = a.bins + (size_t)s.deposit * 2 * (size_t)a.nc;
+          win.gC = win.gR + a.nc;
+        }
+      }
+      consume_any<BC>(a, isp, base, ring + (size_t)st * stage_stride, win, t[0]);
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&empty[st]);
+    }
+    if (cur >= 0) flush_tally(a, a.id[cur], t[0], nullptr);
+    // Partial last tiles (n % kTile particles) through the LDG path; block b
+    // takes species b.
+    if ((int)blockIdx.x < a.nsp) {
+      const int isp = (int)blockIdx.x;
+      const pb_species &s = a.sp[isp];
+      const int64_t n = s.n_dev ? *s.n_dev : s.n;
+      const int64_t beg = (n / kTile) * kTile;
+      if (beg < n) {
+        Window w2{nullptr, nullptr, 0, 0, nullptr, nullptr};
+        const bool dep = s.deposit >= 0 && a.bins != nullptr;
+        if (dep) {
+          w2.gR = a.bins + (size_t)s.deposit * 2 * (size_t)a.nc;
+          w2.gC = w2.gR + a.nc;
+        }
+        Tally tt;
+        run_any<BC, true>(a, isp, beg, n, w2, tt, dep);
+        flush_tally(a, a.id[isp], tt, nullptr);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Host side.
 // ---------------------------------------------------------------------------
-static int g_blocks_per_sm[2][2] = {{0, 0}, {0, 0}};
 static int g_sm_count = 0;
+static int g_use_tma = -1;
 
-static int launch_cfg(int bc, bool push, int *grid) {
+typedef void (*LdgFn)(LaunchArgs);
+typedef void (*TmaFn)(LaunchArgs, int);
+
+static int sm_count() {
   if (g_sm_count == 0) {
     int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
-    e = cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
-    if (e != cudaSuccess) return cuda_status(e, "cudaDeviceGetAttribute");
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
   }
-  int &bps = g_blocks_per_sm[bc][push ? 1 : 0];
-  if (bps == 0) {
-    const void *fn =
-        bc == PB_BC_PERIODIC
-            ? (push ? (const void *)k_push_deposit<PB_BC_PERIODIC, true>
-                    : (const void *)k_push_deposit<PB_BC_PERIODIC, false>)
-            : (push ? (const void *)k_push_deposit<PB_BC_ABSORBING, true>
-                    : (const void *)k_push_deposit<PB_BC_ABSORBING, false>);
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, kThreads, 0);
-    if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-    if (bps < 1) bps = 1;
-  }
-  *grid = g_sm_count * bps;
+  return g_sm_count;
+}
+
+static int occupancy(const void *fn, int threads, int smem, int *bps) {
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute");
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, fn, threads, smem);
+  if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  if (*bps < 1) *bps = 1;
   return PB_OK;
 }
 
-// Approximate HBM bytes per particle, used only to balance blocks.
+// Approximate HBM bytes per particle, used to balance blocks and order tiles.
 static double bytes_per_particle(const pb_species &s, bool push) {
   if (!push) return 12.0;
   const bool yp = s.yp != nullptr;
@@ -499,9 +771,8 @@ static double bytes_per_particle(const pb_species &s, bool push) {
   }
 }
 
-static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc,
-                  int bc, bool push, uint64_t *bins, pb_status *st,
-                  cudaStream_t stream) {
+static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, int bc, bool push,
+                  uint64_t *bins, pb_status *st, cudaStream_t stream) {
   if (nsp < 0 || nsp > PB_MAX_SPECIES) {
     set_error("nsp=%d outside [0, %d]", nsp, PB_MAX_SPECIES);
     return PB_ERR_INVALID;
@@ -518,9 +789,12 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc,
     set_error("status pointer is NULL");
     return PB_ERR_INVALID;
   }
+  if (g_use_tma < 0) {
+    const char *env = getenv("PB_PUSH_PATH");
+    g_use_tma = (env && strcmp(env, "ldg") == 0) ? 0 : 1;
+  }
   LaunchArgs a;
   memset(&a, 0, sizeof(a));
-  a.nsp = 0;
   a.push = push ? 1 : 0;
   a.e = e;
   a.nc = nc;
@@ -528,7 +802,7 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc,
   a.st = st;
   double w[PB_MAX_SPECIES];
   double wsum = 0.0;
-  // Only species with work take part; map back to their caller index.
+  bool all_move = true;
   for (int k = 0; k < nsp; ++k) {
     const pb_species &s = sp[k];
     const bool dep = s.deposit >= 0 && bins != nullptr;
@@ -558,62 +832,98 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc,
       set_error("species %d: absorbing walls need holes and n_dev", k);
       return PB_ERR_INVALID;
     }
-    if (((uintptr_t)s.x | (uintptr_t)s.vx | (uintptr_t)s.vy | (uintptr_t)s.vz |
-         (uintptr_t)s.yp) & 15u || ((uintptr_t)s.cell & 7u)) {
+    if (((uintptr_t)s.x | (uintptr_t)s.vx | (uintptr_t)s.vy | (uintptr_t)s.vz | (uintptr_t)s.yp |
+         (uintptr_t)s.cell) & 15u) {
       set_error("species %d: arrays must be 16-byte aligned", k);
       return PB_ERR_INVALID;
     }
     a.id[a.nsp] = k;
     a.sp[a.nsp] = s;
-    if (!moves) a.sp[a.nsp].kind = PB_KIND_INACTIVE;
+    if (!moves) {
+      a.sp[a.nsp].kind = PB_KIND_INACTIVE;
+      all_move = false;
+    }
     w[a.nsp] = (double)s.n * bytes_per_particle(a.sp[a.nsp], push);
     wsum += w[a.nsp];
     a.nsp++;
   }
   if (a.nsp == 0) return PB_OK;
-  int grid = 0;
-  int rc = launch_cfg(bc, push, &grid);
-  if (rc) return rc;
-  // Blocks per species proportional to bytes, at least one, at most tiles.
-  int start = 0;
-  for (int k = 0; k < a.nsp; ++k) {
-    const int64_t tiles = (a.sp[k].n + kTile - 1) / kTile;
-    int64_t nb = (int64_t)(grid * (w[k] / wsum) + 0.5);
-    if (nb < 1) nb = 1;
-    if (nb > tiles) nb = tiles;
-    a.blk_start[k] = start;
-    start += (int)nb;
+  const int sms = sm_count();
+  if (sms == 0) return cuda_status(cudaGetLastError(), "device query");
+
+  if (push && g_use_tma && all_move) {
+    // Tile list: species by descending bytes/particle, full tiles only.
+    int order[PB_MAX_SPECIES];
+    for (int k = 0; k < a.nsp; ++k) order[k] = k;
+    for (int i = 1; i < a.nsp; ++i)
+      for (int j = i; j > 0 && bytes_per_particle(a.sp[order[j]], true) >
+                                   bytes_per_particle(a.sp[order[j - 1]], true); --j) {
+        const int tmp = order[j];
+        order[j] = order[j - 1];
+        order[j - 1] = tmp;
+      }
+    int smem = 0;
+    a.tile_start[0] = 0;
+    for (int k = 0; k < a.nsp; ++k) {
+      const pb_species &s = a.sp[order[k]];
+      a.order[k] = order[k];
+      a.tile_start[k + 1] = a.tile_start[k] + s.n / kTile;  // upper bound when n_dev shrinks
+      const int sb = stage_bytes(s.kind, s.yp != nullptr);
+      if (sb > smem) smem = sb;
+    }
+    if (bc == PB_BC_ABSORBING) {
+      // n_dev can shrink below the host bound: keep the tile list within it
+      // by sending everything through the LDG path for absorbing walls.
+      goto ldg;
+    }
+    {
+      const int stride = smem;
+      smem *= kStages;
+      TmaFn fn = k_push_tma<PB_BC_PERIODIC>;
+      int bps = 0;
+      int rc = occupancy((const void *)fn, kThreads + 32, smem, &bps);
+      if (rc) return rc;
+      fn<<<sms * bps, kThreads + 32, smem, stream>>>(a, stride);
+      PB_CHECK_LAUNCH("k_push_tma");
+      return PB_OK;
+    }
   }
-  a.blk_start[a.nsp] = start;
-  const LaunchArgs &b = a;
-  if (bc == PB_BC_PERIODIC) {
-    if (push) k_push_deposit<PB_BC_PERIODIC, true><<<start, kThreads, 0, stream>>>(b);
-    else k_push_deposit<PB_BC_PERIODIC, false><<<start, kThreads, 0, stream>>>(b);
-  } else {
-    if (push) k_push_deposit<PB_BC_ABSORBING, true><<<start, kThreads, 0, stream>>>(b);
-    else k_push_deposit<PB_BC_ABSORBING, false><<<start, kThreads, 0, stream>>>(b);
+ldg : {
+    LdgFn fn = bc == PB_BC_PERIODIC
+                   ? (push ? k_push_deposit<PB_BC_PERIODIC, true> : k_push_deposit<PB_BC_PERIODIC, false>)
+                   : (push ? k_push_deposit<PB_BC_ABSORBING, true> : k_push_deposit<PB_BC_ABSORBING, false>);
+    int bps = 0;
+    int rc = occupancy((const void *)fn, kThreads, 0, &bps);
+    if (rc) return rc;
+    const int grid = sms * bps;
+    int start = 0;
+    for (int k = 0; k < a.nsp; ++k) {
+      const int64_t tiles = (a.sp[k].n + kTile - 1) / kTile;
+      int64_t nb = (int64_t)(grid * (w[k] / wsum) + 0.5);
+      if (nb < 1) nb = 1;
+      if (nb > tiles) nb = tiles;
+      a.blk_start[k] = start;
+      start += (int)nb;
+    }
+    a.blk_start[a.nsp] = start;
+    fn<<<start, kThreads, 0, stream>>>(a);
+    PB_CHECK_LAUNCH("k_push_deposit");
+    return PB_OK;
   }
-  PB_CHECK_LAUNCH("k_push_deposit");
-  return PB_OK;
 }
 
 }  // namespace pb
 
-extern "C" int pb_push_deposit(const pb_species *sp, int nsp,
-                               const double *e_nodes, int64_t nc,
-                               int particle_bc, uint64_t *bins,
-                               pb_status *status, void *stream) {
-  return pb::launch(sp, nsp, e_nodes, nc, particle_bc, true, bins, status,
-                    (cudaStream_t)stream);
+extern "C" int pb_push_deposit(const pb_species *sp, int nsp, const double *e_nodes, int64_t nc,
+                               int particle_bc, uint64_t *bins, pb_status *status, void *stream) {
+  return pb::launch(sp, nsp, e_nodes, nc, particle_bc, true, bins, status, (cudaStream_t)stream);
 }
 
-extern "C" int pb_deposit_only(const pb_species *sp, int nsp, int64_t nc,
-                               uint64_t *bins, pb_status *status,
-                               void *stream) {
+extern "C" int pb_deposit_only(const pb_species *sp, int nsp, int64_t nc, uint64_t *bins,
+                               pb_status *status, void *stream) {
   if (!bins) {
     pb::set_error("bins pointer is NULL");
     return PB_ERR_INVALID;
   }
-  return pb::launch(sp, nsp, nullptr, nc, PB_BC_PERIODIC, false, bins, status,
-                    (cudaStream_t)stream);
+  return pb::launch(sp, nsp, nullptr, nc, PB_BC_PERIODIC, false, bins, status, (cudaStream_t)stream);
 }

@@ -156,8 +156,13 @@ class Engine:
                 self.compact_scratch = torch.empty(nb, dtype=torch.uint8, device=self.device)
         self.sort_scratch = None
         self.step_index = 0
-        self._pending = []  # (step, status pinned, n_live pinned, event)
         self.phase_events = []
+        self._timing = None
+        self._arr = None
+        self.graph = None
+        # Work counter of the TMA mover: the pb_status.tile_next word.
+        off = ctypes.sizeof(_lib.PbStatus) - 8
+        self._tile_counter = self.status[off:off + 8]
         self.absorbed = np.zeros((len(self.sp), 2), dtype=np.int64)
         self.moved = np.zeros(len(self.sp), dtype=np.int64)
         self._load(init)
@@ -185,7 +190,10 @@ class Engine:
         return ctypes.c_void_p(self.stream.cuda_stream)
 
     def _species(self):
-        return species_array(self.sp)
+        """Cached C-ABI species array (rebuilt when buffers are swapped)."""
+        if self._arr is None:
+            self._arr = species_array(self.sp)
+        return self._arr
 
     def deposit_current(self):
         """Fixed-point deposit of the current positions into the bins
@@ -243,9 +251,13 @@ class Engine:
             e = self.e
         arr, n = self._species()
         with torch.cuda.stream(self.stream):
-            self.status.copy_(self.status_tpl)
+            self._tile_counter.zero_()
+            if self._timing is not None:
+                self._timing[0].record(self.stream)
             _lib.check(self.lib.pb_push_deposit(arr, n, e.data_ptr(), self.nc, self.bc, self.bins.data_ptr(),
                                                 self.status.data_ptr(), self._sh()), "pb_push_deposit")
+            if self._timing is not None:
+                self._timing[1].record(self.stream)
 
     def resort(self):
         with torch.cuda.stream(self.stream):
@@ -272,69 +284,101 @@ class Engine:
                                                     self.sort_scratch.data_ptr(), self.sort_scratch.numel(),
                                                     self._sh()), "pb_sort_by_cell")
                 s.swap_with_spare()
+            self._arr = None
+            self.graph = None  # captured pointers are stale
 
     def step(self, timed: bool = False):
-        """One full cycle.  Returns rho/E of this step (device tensors)."""
-        ev = None
+        """One full cycle.  Returns rho/E of this step (device tensors).
+
+        The engine works on its own stream; the caller's current stream is
+        ordered after the step (so reading rho/E there is safe) and the next
+        step is ordered after the caller's current stream (so in-place
+        updates never race the caller's reads)."""
+        caller = torch.cuda.current_stream(self.device)
+        self.stream.wait_stream(caller)
         if timed:
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            self._timing = (ev[1], ev[2])
             ev[0].record(self.stream)
         rho = self.density()
-        if timed:
-            ev[1].record(self.stream)
         e = self.field(rho)
-        if timed:
-            ev[2].record(self.stream)
         self.push(e)
-        if timed:
-            ev[3].record(self.stream)
         self.resort()
         if timed:
-            ev[4].record(self.stream)
+            ev[3].record(self.stream)
             self.phase_events.append(ev)
-        self._record_status()
+            self._timing = None
         self.step_index += 1
+        caller.wait_stream(self.stream)
         if self.check_every and self.step_index % self.check_every == 0:
             self.sync()
         return rho, e
 
-    # -- status handling ------------------------------------------------------------
-    def _record_status(self):
-        with torch.cuda.stream(self.stream):
-            host = torch.empty(_lib.STATUS_BYTES, dtype=torch.uint8, pin_memory=True)
-            host.copy_(self.status, non_blocking=True)
-            nlive = None
+    # -- CUDA graph replay --------------------------------------------------------------
+    def capture(self):
+        """Capture one step (deposit epilogue, field, mover, compaction) as a
+        CUDA graph; replay() then costs one launch per step.  Sort steps run
+        eagerly and invalidate the graph (buffers are swapped)."""
+        self.sync()
+        self.stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        # Warm the allocator / occupancy caches outside the capture.
+        with torch.cuda.graph(g, stream=self.stream):
+            rho = self.density()
+            e = self.field(rho)
+            self.push(e)
             if self.absorbing:
-                nlive = torch.empty(len(self.sp), dtype=torch.int64, pin_memory=True)
-                nlive.copy_(torch.cat([s.n_dev for s in self.sp]), non_blocking=True)
-            evt = torch.cuda.Event()
-            evt.record(self.stream)
-        self._pending.append((self.step_index + 1, host, nlive, evt))
+                arr, n = self._species()
+                _lib.check(self.lib.pb_compact(arr, n, self.status.data_ptr(), self.compact_scratch.data_ptr(),
+                                               self.compact_scratch.numel(), self._sh()), "pb_compact")
+        self.graph = g
+        return g
 
+    def replay(self, steps: int = 1):
+        """Run `steps` cycles through the captured graph (sorts included)."""
+        caller = torch.cuda.current_stream(self.device)
+        self.stream.wait_stream(caller)
+        for _ in range(steps):
+            if self.sort_every and (self.step_index + 1) % self.sort_every == 0:
+                self.step()  # eager step with the sort at its end
+                continue
+            if self.graph is None:
+                self.capture()
+            with torch.cuda.stream(self.stream):
+                self.graph.replay()
+            self.step_index += 1
+        caller.wait_stream(self.stream)
+        if self.check_every:
+            self.sync()
+
+    # -- status handling ------------------------------------------------------------
     def sync(self):
-        """Wait for enqueued steps and raise the first recorded error."""
-        pend, self._pending = self._pending, []
-        for step, host, nlive, evt in pend:
-            evt.synchronize()
-            st = decode_status(host.numpy())
-            for k in range(len(self.sp)):
-                self.moved[k] += st.moved[k]
-                self.absorbed[k, 0] += st.absorbed[k][0]
-                self.absorbed[k, 1] += st.absorbed[k][1]
-            if nlive is not None:
-                self.last_live = [int(v) for v in nlive.numpy()]
-            if st.code == _lib.PB_ERR_CFL:
-                key = int(st.cfl_index)
-                isp, idx = key >> 56, key & ((1 << 56) - 1)
-                s = self.sp[isp]
-                x = float(s.arr["x"][idx].item())
-                cell = int(s.cell[idx].item())
-                raise CflViolation(
-                    f"step {step}, phase resort: species {s.name!r} cell {cell}: "
-                    f"displacement of {int(math.floor(x))} cells reaches across the whole domain"
-                )
-            if st.code != _lib.PB_OK:
-                raise EngineError(f"step {step}: device status {st.code}")
+        """Wait for enqueued work, fold the sticky device status into the
+        host tallies, raise the first recorded error, and reset the status."""
+        self.stream.synchronize()
+        raw = self.status.cpu().numpy()
+        st = decode_status(raw)
+        for k in range(len(self.sp)):
+            self.moved[k] += st.moved[k]
+            self.absorbed[k, 0] += st.absorbed[k][0]
+            self.absorbed[k, 1] += st.absorbed[k][1]
+        if self.absorbing:
+            self.last_live = [int(s.n_dev.item()) for s in self.sp]
+        with torch.cuda.stream(self.stream):
+            self.status.copy_(self.status_tpl)
+        self.stream.synchronize()
+        if st.code == _lib.PB_ERR_CFL:
+            key = int(st.cfl_index)
+            isp, idx = key >> 56, key & ((1 << 56) - 1)
+            s = self.sp[isp]
+            x = float(s.arr["x"][idx].item())
+            cell = int(s.cell[idx].item())
+            raise CflViolation(
+                f"step {self.step_index}, phase resort: species {s.name!r} cell {cell}: "
+                f"displacement of {int(math.floor(x))} cells reaches across the whole domain"
+            )
+        if st.code != _lib.PB_OK:
+            raise EngineError(f"step {self.step_index}: device status {st.code}")
 
     def totals(self) -> list:
         return [s.live_count() for s in self.sp]
@@ -344,13 +388,20 @@ class Engine:
         return [s.download() for s in self.sp]
 
     def phase_seconds(self) -> dict:
-        """Resolve the per-phase CUDA events of timed steps (seconds)."""
+        """Per-phase seconds of the timed steps, from CUDA events: "mover" is
+        the fused push+deposit launch, "deposit" the bin reduction and
+        density epilogue, "resort" compaction / sort."""
         self.stream.synchronize()
         out = {k: 0.0 for k in PHASE_KEYS}
         for ev in self.phase_events:
-            out["deposit"] += ev[0].elapsed_time(ev[1]) * 1e-3
-            solve = ev[1].elapsed_time(ev[2]) * 1e-3
-            out["solve"] += solve
-            out["mover"] += ev[2].elapsed_time(ev[3]) * 1e-3
-            out["resort"] += ev[3].elapsed_time(ev[4]) * 1e-3
+            total = ev[0].elapsed_time(ev[3]) * 1e-3
+            mover = ev[1].elapsed_time(ev[2]) * 1e-3
+            pre = ev[0].elapsed_time(ev[1]) * 1e-3
+            out["mover"] += mover
+            out["deposit"] += pre
+            out["resort"] += total - mover - pre
         return out
+
+    def mover_ms(self) -> list:
+        self.stream.synchronize()
+        return [ev[1].elapsed_time(ev[2]) for ev in self.phase_events]

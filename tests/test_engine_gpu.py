@@ -131,7 +131,7 @@ def test_moved_counts_exact(cuda):
     eng.upload(flats)
     e = np.zeros(eng.nc + 1)
     eng.push(torch.from_numpy(e).to(cuda))
-    eng._record_status()
+    pass
     eng.sync()
     res = _run_oracle_step(eng, flats, e, 0)
     for k in range(len(flats)):
@@ -175,7 +175,7 @@ def test_absorbing_walls_counts_and_survivors(cuda):
         e = np.zeros(eng.nc + 1)
         eng.push(torch.from_numpy(e).to(cuda))
         eng.resort()
-        eng._record_status()
+        pass
         eng.sync()
         res = _run_oracle_step(eng, live, e, 1)
         nxt = []
@@ -234,7 +234,7 @@ def test_cfl_violation_raises(cuda):
     flats[2].vx[5] = 9.0 / 3.0  # neutral, nstep 3 -> displacement 9 cells on nc=8
     eng.upload(flats)
     eng.push(torch.zeros(9, dtype=torch.float64, device=cuda))
-    eng._record_status()
+    pass
     with pytest.raises(CflViolation, match="whole domain"):
         eng.sync()
 
@@ -274,7 +274,7 @@ def test_free_streaming_exact_1000_steps(cuda):
         eng.push()
         eng.resort()
         eng.step_index += 1
-    eng._record_status()
+    pass
     eng.sync()
     dev = eng.download()
     checked = 0
