@@ -279,6 +279,24 @@ def run_ours(args, rank, world, local_rank):
         e2e_ms = float(t[0])
     e2e_value = pushes_rank * world / (e2e_ms * 1e-3)
 
+    # Speed-of-light probe (last: it overwrites particle state): the same
+    # read/write byte mix streamed with a trivial update and no physics.
+    import ctypes
+    arr, nsp = eng._species()
+    actual_bytes = 0.0
+    for s in eng.sp:
+        actual_bytes += s.n * (36.0 if s.kind != 1 else (48.0 if s.has_yp else 24.0))
+    torch.cuda.synchronize(dev)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(2):
+        eng.lib.pb_stream_sol(arr, nsp, ctypes.c_void_p(eng.stream.cuda_stream))
+    s0.record(eng.stream)
+    for _ in range(10):
+        eng.lib.pb_stream_sol(arr, nsp, ctypes.c_void_p(eng.stream.cuda_stream))
+    s1.record(eng.stream)
+    torch.cuda.synchronize(dev)
+    sol_ms = s0.elapsed_time(s1) / 10
+
     peak, peak_kind = measured_peak()
     achieved = alg_bytes / (push_ms * 1e-3) / 1e9
     traffic = committed_traffic()
@@ -314,6 +332,9 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": nodes * 8,
                 "path": "Engine.step() public API: E-field H2D (pinned) + step + rho D2H, synced per step"},
         "gpu_launches": args.steps * launches_per_step + n_sorts * 4,
+        "sol_probe": {"ms": sol_ms, "actual_bytes": actual_bytes, "gbs": actual_bytes / (sol_ms * 1e-3) / 1e9,
+                      "mover_actual_gbs": actual_bytes / (push_ms * 1e-3) / 1e9,
+                      "note": "pb_stream_sol: same bytes (incl. cell index), trivial update, no deposit"},
     }
     return out, clk.summary()
 

@@ -173,6 +173,10 @@ int pb_solve_poisson(const double *rho, double *phi, int64_t nc, double dx,
 int pb_compute_efield(const double *phi, double *e, int64_t nc, double dx,
                       int field_bc, void *stream);
 
+/* Roofline probe: streams the mover's exact read/write bytes per species with
+ * a trivial update (no physics, no deposit).  Destroys particle state. */
+int pb_stream_sol(const pb_species *sp, int nsp, void *stream);
+
 /* Device init_plasma (pkg/src/picmc/core.py:292-352): ppc0 particles per
  * cell for cells [cell_lo, cell_hi) with the reference splitmix64 streams.
  * Positions are bit-exact; velocities use CUDA log/sin/cos (ulp-close). */

@@ -12,7 +12,7 @@ import threading
 from .errors import CflViolation, ContractViolation, EngineError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpicmc_b200.so")
+LIB_PATH = os.environ.get("PB_LIB_PATH") or os.path.join(_HERE, "libpicmc_b200.so")
 
 PB_OK = 0
 PB_ERR_INVALID = 1
@@ -89,6 +89,7 @@ _SIGS = {
     "pb_solve_poisson": (ctypes.c_int, [_p, _p, _i64, _f64, _f64, ctypes.c_int,
                                         _f64, _f64, _p, _p]),
     "pb_compute_efield": (ctypes.c_int, [_p, _p, _i64, _f64, ctypes.c_int, _p]),
+    "pb_stream_sol": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int, _p]),
     "pb_init_species": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_uint64,
                                        _i64, _i64, _i64, _f64, _p]),
 }

@@ -115,3 +115,52 @@ extern "C" int pb_rho_epilogue(const uint64_t *bins, const double *coef,
   PB_CHECK_LAUNCH("k_rho_epilogue");
   return PB_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Speed-of-light probe for the roofline: streams exactly the mover's bytes
+// (reads x, vx[, vy, yp], cell; writes x[, vx], yp) with a trivial update and
+// no deposit, 4 particles per thread, 256-bit accesses, full occupancy.  It
+// measures what this read/write mix can reach on the part; the mover's
+// achieved bandwidth is reported against the copy peak, not against this.
+namespace pb {
+__global__ void __launch_bounds__(256) k_stream_sol(double *x, double *vx, const double *vy,
+                                                    double *yp, const int32_t *cell, int64_t n,
+                                                    int write_v) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i + 3 < n; i += stride) {
+    double a0, a1, a2, a3, b0, b1, b2, b3;
+    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a0), "=d"(a1), "=d"(a2), "=d"(a3) : "l"(x + i));
+    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(b0), "=d"(b1), "=d"(b2), "=d"(b3) : "l"(vx + i));
+    int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    if (cell) {
+      const int4 c = __ldcs(reinterpret_cast<const int4 *>(cell + i));
+      c0 = c.x; c1 = c.y; c2 = c.z; c3 = c.w;
+    }
+    a0 += b0 + c0; a1 += b1 + c1; a2 += b2 + c2; a3 += b3 + c3;
+    asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(x + i), "d"(a0), "d"(a1), "d"(a2), "d"(a3) : "memory");
+    if (write_v)
+      asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(vx + i), "d"(b0), "d"(b1), "d"(b2), "d"(b3) : "memory");
+    if (yp) {
+      double y0, y1, y2, y3, w0, w1, w2, w3;
+      asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(y0), "=d"(y1), "=d"(y2), "=d"(y3) : "l"(yp + i));
+      asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(w0), "=d"(w1), "=d"(w2), "=d"(w3) : "l"(vy + i));
+      asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(yp + i), "d"(y0 + w0), "d"(y1 + w1), "d"(y2 + w2), "d"(y3 + w3) : "memory");
+    }
+  }
+}
+}  // namespace pb
+
+extern "C" int pb_stream_sol(const pb_species *sp, int nsp, void *stream) {
+  int sms = 0;
+  int rc = pb_device_sm_count(&sms);
+  if (rc) return rc;
+  for (int k = 0; k < nsp; ++k) {
+    const pb_species &s = sp[k];
+    if (s.kind == PB_KIND_INACTIVE || s.n < 4) continue;
+    const bool charged = s.kind != PB_KIND_DRIFT;
+    pb::k_stream_sol<<<sms * 8, 256, 0, (cudaStream_t)stream>>>(
+        s.x, s.vx, s.vy, s.yp, charged ? s.cell : nullptr, s.n & ~(int64_t)3, charged ? 1 : 0);
+  }
+  PB_CHECK_LAUNCH("k_stream_sol");
+  return PB_OK;
+}

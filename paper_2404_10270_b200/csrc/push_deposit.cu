@@ -479,7 +479,8 @@ __global__ void __launch_bounds__(kThreads)
 // SM busy to the end regardless of the per-species cost mix, and the bytes in
 // flight are set by the ring depth instead of by registers.
 // ---------------------------------------------------------------------------
-constexpr int kStages = 3;
+constexpr int kMaxStages = 8;
+constexpr int kMaxAhead = 8;
 constexpr int kConsumerWarps = kThreads / 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -514,17 +515,27 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
       : "memory");
 }
 
+// Particles per TMA tile, per species kind: sized so every kind fills a
+// ~32 KB ring slot (a multiple of 2*kThreads for the pair loop).
+__host__ __device__ constexpr int tile_of(int kind, bool yp) {
+  return kind == PB_KIND_KICK ? 1024
+       : kind == PB_KIND_BORIS ? 1024
+       : kind == PB_KIND_DRIFT ? (yp ? 1024 : 2048)
+       : 1024;
+}
+
 template <int KIND, bool YP>
 struct Stage {
   using F = Fields<KIND, YP>;
+  static constexpr int T = tile_of(KIND, YP);
   static constexpr bool kCell = KIND != PB_KIND_DRIFT;
   static constexpr int kX = 0;
-  static constexpr int kVX = kX + kTile * 8;
-  static constexpr int kVY = kVX + kTile * 8;
-  static constexpr int kVZ = kVY + (F::kVy ? kTile * 8 : 0);
-  static constexpr int kYP = kVZ + (F::kVz ? kTile * 8 : 0);
-  static constexpr int kCELL = kYP + (YP ? kTile * 8 : 0);
-  static constexpr int kBytes = kCELL + (kCell ? kTile * 4 : 0);
+  static constexpr int kVX = kX + T * 8;
+  static constexpr int kVY = kVX + T * 8;
+  static constexpr int kVZ = kVY + (F::kVy ? T * 8 : 0);
+  static constexpr int kYP = kVZ + (F::kVz ? T * 8 : 0);
+  static constexpr int kCELL = kYP + (YP ? T * 8 : 0);
+  static constexpr int kBytes = kCELL + (kCell ? T * 4 : 0);
 };
 
 __host__ __device__ constexpr int stage_bytes(int kind, bool yp) {
@@ -534,22 +545,168 @@ __host__ __device__ constexpr int stage_bytes(int kind, bool yp) {
        : 0;
 }
 
+__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+template <int KIND, bool YP>
+__device__ __forceinline__ void prefetch_tile(const pb_species &s, int64_t base) {
+  using L = Stage<KIND, YP>;
+  using F = Fields<KIND, YP>;
+  prefetch_l2(s.x + base, L::T * 8);
+  prefetch_l2(s.vx + base, L::T * 8);
+  if (F::kVy) prefetch_l2(s.vy + base, L::T * 8);
+  if (F::kVz) prefetch_l2(s.vz + base, L::T * 8);
+  if (YP) prefetch_l2(s.yp + base, L::T * 8);
+  if (L::kCell) prefetch_l2(s.cell + base, L::T * 4);
+}
+
 template <int KIND, bool YP>
 __device__ __forceinline__ void produce_tile(const pb_species &s, int64_t base, unsigned char *buf,
                                              uint64_t *bar) {
   using L = Stage<KIND, YP>;
   using F = Fields<KIND, YP>;
   mbar_expect_tx(bar, (uint32_t)L::kBytes);
-  tma_load_1d(buf + L::kX, s.x + base, kTile * 8, bar);
-  tma_load_1d(buf + L::kVX, s.vx + base, kTile * 8, bar);
-  if (F::kVy) tma_load_1d(buf + L::kVY, s.vy + base, kTile * 8, bar);
-  if (F::kVz) tma_load_1d(buf + L::kVZ, s.vz + base, kTile * 8, bar);
-  if (YP) tma_load_1d(buf + L::kYP, s.yp + base, kTile * 8, bar);
-  if (L::kCell) tma_load_1d(buf + L::kCELL, s.cell + base, kTile * 4, bar);
+  tma_load_1d(buf + L::kX, s.x + base, L::T * 8, bar);
+  tma_load_1d(buf + L::kVX, s.vx + base, L::T * 8, bar);
+  if (F::kVy) tma_load_1d(buf + L::kVY, s.vy + base, L::T * 8, bar);
+  if (F::kVz) tma_load_1d(buf + L::kVZ, s.vz + base, L::T * 8, bar);
+  if (YP) tma_load_1d(buf + L::kYP, s.yp + base, L::T * 8, bar);
+  if (L::kCell) tma_load_1d(buf + L::kCELL, s.cell + base, L::T * 4, bar);
+}
+
+// Thread-local run of equal cells, flushed to the window when the cell changes.
+struct RunAcc {
+  int32_t key = -1;
+  uint64_t w = 0;
+  __device__ __forceinline__ void add(int32_t k, double x, const Window &win) {
+    if (k < 0) return;
+    const uint64_t d = deposit_word(x);
+    if (k == key) {
+      w += d;
+    } else {
+      if (key >= 0) win.emit(key, w);
+      key = k;
+      w = d;
+    }
+  }
+};
+
+__device__ __forceinline__ void st4(double *p, double a, double b, double c, double d) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
+}
+
+// Consumer side of one TMA tile: every thread owns quads of 4 consecutive
+// particles (256-bit stores, thread-local deposit runs), one warp segmented
+// scan per tile for the runs that continue into the next lane.
+template <int KIND, bool YP, int BC, bool DEP>
+__device__ __forceinline__ void consume_tile_quads(const LaunchArgs &a, int isp, int64_t base,
+                                             const unsigned char *buf, const Window &win,
+                                             Tally &t) {
+  using L = Stage<KIND, YP>;
+  using F = Fields<KIND, YP>;
+  const pb_species &s = a.sp[isp];
+  const int sid = a.id[isp];
+  const unsigned full = 0xffffffffu;
+  const int64_t nc = a.nc;
+  RunAcc run;
+#pragma unroll 1
+  for (int qd = 0; qd < L::T / (4 * kThreads); ++qd) {
+    const int li = qd * (4 * kThreads) + 4 * threadIdx.x;
+    const int64_t i = base + li;
+    double x[4], vx[4], vy[4] = {0, 0, 0, 0}, vz[4] = {0, 0, 0, 0}, y[4] = {0, 0, 0, 0};
+    int32_t c[4] = {-1, -1, -1, -1};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double2 xx = *reinterpret_cast<const double2 *>(buf + L::kX + (li + 2 * h) * 8);
+      x[2 * h] = xx.x;
+      x[2 * h + 1] = xx.y;
+      const double2 vv = *reinterpret_cast<const double2 *>(buf + L::kVX + (li + 2 * h) * 8);
+      vx[2 * h] = vv.x;
+      vx[2 * h + 1] = vv.y;
+      if (F::kVy) {
+        const double2 v = *reinterpret_cast<const double2 *>(buf + L::kVY + (li + 2 * h) * 8);
+        vy[2 * h] = v.x;
+        vy[2 * h + 1] = v.y;
+      }
+      if (F::kVz) {
+        const double2 v = *reinterpret_cast<const double2 *>(buf + L::kVZ + (li + 2 * h) * 8);
+        vz[2 * h] = v.x;
+        vz[2 * h + 1] = v.y;
+      }
+      if (YP) {
+        const double2 v = *reinterpret_cast<const double2 *>(buf + L::kYP + (li + 2 * h) * 8);
+        y[2 * h] = v.x;
+        y[2 * h + 1] = v.y;
+      }
+    }
+    if (L::kCell) {
+      const int4 cc = *reinterpret_cast<const int4 *>(buf + L::kCELL + li * 4);
+      c[0] = cc.x;
+      c[1] = cc.y;
+      c[2] = cc.z;
+      c[3] = cc.w;
+    }
+    int32_t nn[4];
+    int8_t wall[4];
+    bool mv[4], cfl[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      kick_drift<KIND>(x[k], vx[k], vy[k], vz[k], c[k], s, a.e);
+      if (YP) y[k] = __dadd_rn(y[k], __dmul_rn(s.fnstep, vy[k]));
+      if (!L::kCell && floor(x[k]) != 0.0) c[k] = s.cell[i + k];
+      const MoveOut o = transfer<BC>(x[k], c[k], nc);
+      nn[k] = o.cell;
+      mv[k] = o.moved;
+      wall[k] = o.wall;
+      cfl[k] = o.cfl;
+    }
+    st4(s.x + i, x[0], x[1], x[2], x[3]);
+    if (KIND != PB_KIND_DRIFT) st4(s.vx + i, vx[0], vx[1], vx[2], vx[3]);
+    if (KIND == PB_KIND_BORIS) {
+      st4(s.vy + i, vy[0], vy[1], vy[2], vy[3]);
+      st4(s.vz + i, vz[0], vz[1], vz[2], vz[3]);
+    }
+    if (YP) st4(s.yp + i, y[0], y[1], y[2], y[3]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (mv[k]) s.cell[i + k] = nn[k];
+      t.moved += (int)mv[k];
+      if (cfl[k]) {
+        const uint64_t key = ((uint64_t)sid << 56) | (uint64_t)(i + k);
+        atomicMin((unsigned long long *)&a.st->cfl_index, (unsigned long long)key);
+        atomicCAS(&a.st->code, PB_OK, PB_ERR_CFL);
+        nn[k] = -1;
+      }
+    }
+    if (BC == PB_BC_ABSORBING) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        t.absorbed[0] += (int)(wall[k] == 0);
+        t.absorbed[1] += (int)(wall[k] == 1);
+        const bool r = wall[k] >= 0;
+        const unsigned b = __ballot_sync(full, r);
+        if (b) {
+          const unsigned lane = lane_id();
+          unsigned long long hb = 0;
+          if (lane == 0)
+            hb = atomicAdd((unsigned long long *)&a.st->n_holes[sid], (unsigned long long)__popc(b));
+          hb = __shfl_sync(full, hb, 0);
+          if (r) s.holes[hb + __popc(b & ((1u << lane) - 1u))] = i + k;
+        }
+      }
+    }
+    if (DEP) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) run.add(nn[k], x[k], win);
+    }
+  }
+  if (DEP) warp_segmented_emit(run.key, run.w, win);
 }
 
 template <int KIND, bool YP, int BC, bool DEP>
-__device__ __forceinline__ void consume_tile(const LaunchArgs &a, int isp, int64_t base,
+__device__ __forceinline__ void consume_tile_pairs(const LaunchArgs &a, int isp, int64_t base,
                                              const unsigned char *buf, const Window &win,
                                              Tally &t) {
   using L = Stage<KIND, YP>;
@@ -557,7 +714,7 @@ __device__ __forceinline__ void consume_tile(const LaunchArgs &a, int isp, int64
   const pb_species &s = a.sp[isp];
   const int sid = a.id[isp];
 #pragma unroll
-  for (int p = 0; p < kPairsPerThread; ++p) {
+  for (int p = 0; p < L::T / (2 * kThreads); ++p) {
     const int li = p * (2 * kThreads) + 2 * threadIdx.x;
     Pair q;
     const double2 xx = *reinterpret_cast<const double2 *>(buf + L::kX + li * 8);
@@ -588,6 +745,20 @@ __device__ __forceinline__ void consume_tile(const LaunchArgs &a, int isp, int64
     }
     handle_pair<KIND, YP, BC, true, DEP>(a, s, sid, base + li, true, true, q, win, t);
   }
+}
+
+#ifndef PB_QUADS
+#define PB_QUADS 0
+#endif
+
+template <int KIND, bool YP, int BC, bool DEP>
+__device__ __forceinline__ void consume_tile(const LaunchArgs &a, int isp, int64_t base,
+                                             const unsigned char *buf, const Window &win,
+                                             Tally &t) {
+  if (PB_QUADS)
+    consume_tile_quads<KIND, YP, BC, DEP>(a, isp, base, buf, win, t);
+  else
+    consume_tile_pairs<KIND, YP, BC, DEP>(a, isp, base, buf, win, t);
 }
 
 // Per-species kind dispatch for the TMA consumer / producer.
@@ -636,20 +807,49 @@ __device__ __forceinline__ void produce_any(const pb_species &s, int64_t base, u
   }
 }
 
+__device__ __forceinline__ void prefetch_any(const pb_species &s, int64_t base) {
+  const bool yp = s.yp != nullptr;
+  switch (s.kind) {
+    case PB_KIND_KICK:
+      if (yp) prefetch_tile<PB_KIND_KICK, true>(s, base);
+      else prefetch_tile<PB_KIND_KICK, false>(s, base);
+      break;
+    case PB_KIND_BORIS:
+      if (yp) prefetch_tile<PB_KIND_BORIS, true>(s, base);
+      else prefetch_tile<PB_KIND_BORIS, false>(s, base);
+      break;
+    default:
+      if (yp) prefetch_tile<PB_KIND_DRIFT, true>(s, base);
+      else prefetch_tile<PB_KIND_DRIFT, false>(s, base);
+      break;
+  }
+}
+
 __device__ __forceinline__ int tile_species(const LaunchArgs &a, int64_t tile) {
   int k = 0;
   while (k + 1 < a.nsp && tile >= a.tile_start[k + 1]) ++k;
   return a.order[k];
 }
 
+// First particle of a tile of species isp.
+__device__ __forceinline__ int64_t tile_base(const LaunchArgs &a, int isp, int64_t tile) {
+  int kk = 0;
+  while (a.order[kk] != isp) ++kk;
+  return (tile - a.tile_start[kk]) * tile_of(a.sp[isp].kind, a.sp[isp].yp != nullptr);
+}
+
+#ifndef PB_MINBLOCKS
+#define PB_MINBLOCKS 3
+#endif
+
 template <int BC>
-__global__ void __launch_bounds__(kThreads + 32)
-    k_push_tma(const __grid_constant__ LaunchArgs a, int stage_stride) {
+__global__ void __launch_bounds__(kThreads + 32, PB_MINBLOCKS)
+    k_push_tma(const __grid_constant__ LaunchArgs a, int stage_stride, int kStages, int ahead) {
   extern __shared__ __align__(128) unsigned char ring[];
-  __shared__ __align__(8) uint64_t bars[2 * kStages];
-  __shared__ int64_t hdr[kStages];
+  __shared__ __align__(8) uint64_t bars[2 * kMaxStages];
+  __shared__ int64_t hdr[kMaxStages];
   uint64_t *full = bars;
-  uint64_t *empty = bars + kStages;
+  uint64_t *empty = bars + kMaxStages;
   if (threadIdx.x == 0) {
     for (int k = 0; k < kStages; ++k) {
       mbar_init(&full[k], 1);
@@ -663,23 +863,37 @@ __global__ void __launch_bounds__(kThreads + 32)
 
   if (warp == kConsumerWarps) {  // producer warp
     if (lane_id() == 0) {
-      unsigned long long next = atomicAdd((unsigned long long *)&a.st->tile_next, 1ull);
+      // Claimed-tile queue: tiles are claimed `ahead` steps before their
+      // shared-memory load and prefetched into L2 at claim time, so DRAM
+      // requests stay in flight beyond the depth of the smem ring.
+      int64_t q[kMaxAhead + 1];
+      const int depth = ahead + 1;
+      for (int j = 0; j < depth; ++j) {
+        q[j] = (int64_t)atomicAdd((unsigned long long *)&a.st->tile_next, 1ull);
+        if (j > 0 && q[j] < total) {
+          const int isp = tile_species(a, q[j]);
+          prefetch_any(a.sp[isp], tile_base(a, isp, q[j]));
+        }
+      }
       for (int64_t k = 0;; ++k) {
         const int st = (int)(k % kStages);
+        const int qi = (int)(k % depth);
+        const int64_t tile = q[qi];
         if (k >= kStages) mbar_wait(&empty[st], (uint32_t)(((k / kStages) - 1) & 1));
-        if ((int64_t)next >= total) {
+        if (tile >= total) {
           hdr[st] = -1;
           mbar_arrive(&full[st]);  // no bytes: completes the phase
           break;
         }
-        const int64_t tile = (int64_t)next;
-        next = atomicAdd((unsigned long long *)&a.st->tile_next, 1ull);
         hdr[st] = tile;
         const int isp = tile_species(a, tile);
-        int kk = 0;
-        while (a.order[kk] != isp) ++kk;
-        const int64_t base = (tile - a.tile_start[kk]) * kTile;
-        produce_any(a.sp[isp], base, ring + (size_t)st * stage_stride, &full[st]);
+        produce_any(a.sp[isp], tile_base(a, isp, tile), ring + (size_t)st * stage_stride, &full[st]);
+        const int64_t nt = (int64_t)atomicAdd((unsigned long long *)&a.st->tile_next, 1ull);
+        q[qi] = nt;
+        if (depth > 1 && nt < total) {
+          const int jsp = tile_species(a, nt);
+          prefetch_any(a.sp[jsp], tile_base(a, jsp, nt));
+        }
       }
     }
   } else {  // consumer warps
@@ -694,7 +908,7 @@ __global__ void __launch_bounds__(kThreads + 32)
       const int isp = tile_species(a, tile);
       int kk = 0;
       while (a.order[kk] != isp) ++kk;
-      const int64_t base = (tile - a.tile_start[kk]) * kTile;
+      const int64_t base = (tile - a.tile_start[kk]) * tile_of(a.sp[isp].kind, a.sp[isp].yp != nullptr);
       if (isp != cur) {
         if (cur >= 0) flush_tally(a, a.id[cur], t[0], nullptr);
         t[0] = Tally();
@@ -710,13 +924,14 @@ __global__ void __launch_bounds__(kThreads + 32)
       if (lane_id() == 0) mbar_arrive(&empty[st]);
     }
     if (cur >= 0) flush_tally(a, a.id[cur], t[0], nullptr);
-    // Partial last tiles (n % kTile particles) through the LDG path; block b
+    // Partial last tiles (n % T particles) through the LDG path; block b
     // takes species b.
     if ((int)blockIdx.x < a.nsp) {
       const int isp = (int)blockIdx.x;
       const pb_species &s = a.sp[isp];
       const int64_t n = s.n_dev ? *s.n_dev : s.n;
-      const int64_t beg = (n / kTile) * kTile;
+      const int64_t T = tile_of(s.kind, s.yp != nullptr);
+      const int64_t beg = (n / T) * T;
       if (beg < n) {
         Window w2{nullptr, nullptr, 0, 0, nullptr, nullptr};
         const bool dep = s.deposit >= 0 && a.bins != nullptr;
@@ -733,13 +948,214 @@ __global__ void __launch_bounds__(kThreads + 32)
 }
 
 // ---------------------------------------------------------------------------
+// Quad kernel: warp-granular dynamic chunks, 256-bit LDG/STG, 4 consecutive
+// particles per thread.  Each warp pulls 2048-particle chunks (one species)
+// from a global counter -- heaviest species first -- and streams them with
+// 32-byte loads/stores per lane (LDG.E.256 / STG.E.256, 1 KB per warp
+// instruction).  No block-level synchronisation at all: every warp runs
+// independently, so latency hiding comes from occupancy (lean registers).
+// Deposit: thread-local run of the quad, then one warp segmented scan per
+// 128 particles, global u64 atomics from the segment tails.
+// ---------------------------------------------------------------------------
+constexpr int kChunk = 2048;
+
+#ifndef PB_LD4
+#define PB_LD4 "ld.global.cs.v4.f64"
+#endif
+__device__ __forceinline__ void ld4(const double *p, double &a, double &b, double &c, double &d) {
+  asm volatile(PB_LD4 " {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
+template <int KIND, bool YP, int BC, bool DEP>
+__device__ __forceinline__ void quad_chunk(const LaunchArgs &a, int isp, int64_t beg, int64_t end,
+                                           const Window &win, Tally &t) {
+  using F = Fields<KIND, YP>;
+  const pb_species &s = a.sp[isp];
+  const int sid = a.id[isp];
+  const unsigned full = 0xffffffffu;
+  const int64_t nc = a.nc;
+  constexpr bool kCell = KIND != PB_KIND_DRIFT;
+  const int lane = (int)lane_id();
+#pragma unroll 1
+  for (int64_t q0 = beg; q0 < end; q0 += 128) {
+    const int64_t i = q0 + 4 * lane;
+    const int nv = i >= end ? 0 : (end - i >= 4 ? 4 : (int)(end - i));
+    double x[4] = {0, 0, 0, 0}, vx[4] = {0, 0, 0, 0}, vy[4] = {0, 0, 0, 0}, vz[4] = {0, 0, 0, 0},
+           y[4] = {0, 0, 0, 0};
+    int32_t c[4] = {-1, -1, -1, -1};
+    if (nv == 4) {
+      ld4(s.x + i, x[0], x[1], x[2], x[3]);
+      ld4(s.vx + i, vx[0], vx[1], vx[2], vx[3]);
+      if (F::kVy) ld4(s.vy + i, vy[0], vy[1], vy[2], vy[3]);
+      if (F::kVz) ld4(s.vz + i, vz[0], vz[1], vz[2], vz[3]);
+      if (YP) ld4(s.yp + i, y[0], y[1], y[2], y[3]);
+      if (kCell) {
+        const int4 cc = __ldcs(reinterpret_cast<const int4 *>(s.cell + i));
+        c[0] = cc.x;
+        c[1] = cc.y;
+        c[2] = cc.z;
+        c[3] = cc.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (k < nv) {
+          x[k] = s.x[i + k];
+          vx[k] = s.vx[i + k];
+          if (F::kVy) vy[k] = s.vy[i + k];
+          if (F::kVz) vz[k] = s.vz[i + k];
+          if (YP) y[k] = s.yp[i + k];
+          if (kCell) c[k] = s.cell[i + k];
+        }
+      }
+    }
+    int32_t nn[4];
+    int8_t wall[4];
+    bool mv[4], cfl[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      nn[k] = -1;
+      wall[k] = -1;
+      mv[k] = false;
+      cfl[k] = false;
+      if (k < nv) {
+        kick_drift<KIND>(x[k], vx[k], vy[k], vz[k], c[k], s, a.e);
+        if (YP) y[k] = __dadd_rn(y[k], __dmul_rn(s.fnstep, vy[k]));
+        if (!kCell && floor(x[k]) != 0.0) c[k] = s.cell[i + k];
+        const MoveOut o = transfer<BC>(x[k], c[k], nc);
+        nn[k] = o.cell;
+        mv[k] = o.moved;
+        wall[k] = o.wall;
+        cfl[k] = o.cfl;
+      }
+    }
+    if (nv == 4) {
+      st4(s.x + i, x[0], x[1], x[2], x[3]);
+      if (KIND != PB_KIND_DRIFT) st4(s.vx + i, vx[0], vx[1], vx[2], vx[3]);
+      if (KIND == PB_KIND_BORIS) {
+        st4(s.vy + i, vy[0], vy[1], vy[2], vy[3]);
+        st4(s.vz + i, vz[0], vz[1], vz[2], vz[3]);
+      }
+      if (YP) st4(s.yp + i, y[0], y[1], y[2], y[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (k < nv) {
+          s.x[i + k] = x[k];
+          if (KIND != PB_KIND_DRIFT) s.vx[i + k] = vx[k];
+          if (KIND == PB_KIND_BORIS) {
+            s.vy[i + k] = vy[k];
+            s.vz[i + k] = vz[k];
+          }
+          if (YP) s.yp[i + k] = y[k];
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (mv[k]) s.cell[i + k] = nn[k];
+      t.moved += (int)mv[k];
+      if (cfl[k]) {
+        const uint64_t key = ((uint64_t)sid << 56) | (uint64_t)(i + k);
+        atomicMin((unsigned long long *)&a.st->cfl_index, (unsigned long long)key);
+        atomicCAS(&a.st->code, PB_OK, PB_ERR_CFL);
+        nn[k] = -1;
+      }
+    }
+    if (BC == PB_BC_ABSORBING) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        t.absorbed[0] += (int)(wall[k] == 0);
+        t.absorbed[1] += (int)(wall[k] == 1);
+        const bool r = wall[k] >= 0;
+        const unsigned b = __ballot_sync(full, r);
+        if (b) {
+          unsigned long long hb = 0;
+          if (lane == 0)
+            hb = atomicAdd((unsigned long long *)&a.st->n_holes[sid], (unsigned long long)__popc(b));
+          hb = __shfl_sync(full, hb, 0);
+          if (r) s.holes[hb + __popc(b & ((1u << lane) - 1u))] = i + k;
+        }
+      }
+    }
+    if (DEP) {
+      RunAcc run;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) run.add(nn[k], x[k], win);
+      warp_segmented_emit(run.key, run.w, win);
+    }
+  }
+}
+
+template <int BC, bool BORIS>
+__device__ __forceinline__ void quad_dispatch(const LaunchArgs &a, int isp, int64_t beg,
+                                              int64_t end, const Window &win, Tally &t) {
+  const pb_species &s = a.sp[isp];
+  const bool yp = s.yp != nullptr;
+  const bool dep = s.deposit >= 0 && a.bins != nullptr;
+#define PB_Q(K, Y)                                                  \
+  do {                                                              \
+    if (dep) quad_chunk<K, Y, BC, true>(a, isp, beg, end, win, t);  \
+    else quad_chunk<K, Y, BC, false>(a, isp, beg, end, win, t);     \
+  } while (0)
+  if (s.kind == PB_KIND_KICK) {
+    if (yp) PB_Q(PB_KIND_KICK, true); else PB_Q(PB_KIND_KICK, false);
+  } else if (BORIS && s.kind == PB_KIND_BORIS) {
+    if (yp) PB_Q(PB_KIND_BORIS, true); else PB_Q(PB_KIND_BORIS, false);
+  } else {
+    if (yp) PB_Q(PB_KIND_DRIFT, true); else PB_Q(PB_KIND_DRIFT, false);
+  }
+#undef PB_Q
+}
+
+#ifndef PB_QUAD_MINBLOCKS
+#define PB_QUAD_MINBLOCKS 3
+#endif
+
+template <int BC, bool BORIS>
+__global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
+    k_push_quad(const __grid_constant__ LaunchArgs a) {
+  const int64_t total = a.tile_start[a.nsp];
+  const unsigned full = 0xffffffffu;
+  Window win{nullptr, nullptr, 0, 0, nullptr, nullptr};
+  Tally t;
+  int cur = -1;
+  for (;;) {
+    unsigned long long c = 0;
+    if (lane_id() == 0) c = atomicAdd((unsigned long long *)&a.st->tile_next, 1ull);
+    c = __shfl_sync(full, c, 0);
+    if ((int64_t)c >= total) break;
+    int kk = 0;
+    while (kk + 1 < a.nsp && (int64_t)c >= a.tile_start[kk + 1]) ++kk;
+    const int isp = a.order[kk];
+    const pb_species &s = a.sp[isp];
+    const int64_t n = s.n;
+    const int64_t beg = ((int64_t)c - a.tile_start[kk]) * kChunk;
+    const int64_t end = beg + kChunk < n ? beg + kChunk : n;
+    if (isp != cur) {
+      if (cur >= 0) flush_tally(a, a.id[cur], t, nullptr);
+      t = Tally();
+      cur = isp;
+      if (s.deposit >= 0 && a.bins) {
+        win.gR = a.bins + (size_t)s.deposit * 2 * (size_t)a.nc;
+        win.gC = win.gR + a.nc;
+      }
+    }
+    quad_dispatch<BC, BORIS>(a, isp, beg, end, win, t);
+  }
+  if (cur >= 0) flush_tally(a, a.id[cur], t, nullptr);
+}
+
+// ---------------------------------------------------------------------------
 // Host side.
 // ---------------------------------------------------------------------------
 static int g_sm_count = 0;
-static int g_use_tma = -1;
+static int g_use_tma = -1;  // 0 ldg, 1 tma, 2 quad
 
 typedef void (*LdgFn)(LaunchArgs);
-typedef void (*TmaFn)(LaunchArgs, int);
+typedef void (*TmaFn)(LaunchArgs, int, int, int);
+static int g_stages = 0;
+static int g_ahead = -1;
 
 static int sm_count() {
   if (g_sm_count == 0) {
@@ -791,7 +1207,9 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
   }
   if (g_use_tma < 0) {
     const char *env = getenv("PB_PUSH_PATH");
-    g_use_tma = (env && strcmp(env, "ldg") == 0) ? 0 : 1;
+    g_use_tma = 2;
+    if (env && strcmp(env, "ldg") == 0) g_use_tma = 0;
+    if (env && strcmp(env, "tma") == 0) g_use_tma = 1;
   }
   LaunchArgs a;
   memset(&a, 0, sizeof(a));
@@ -851,7 +1269,35 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
   const int sms = sm_count();
   if (sms == 0) return cuda_status(cudaGetLastError(), "device query");
 
-  if (push && g_use_tma && all_move) {
+  if (push && g_use_tma == 2 && all_move && bc == PB_BC_PERIODIC) {
+    // Chunk list: species by descending bytes/particle.
+    int order[PB_MAX_SPECIES];
+    bool boris = false;
+    for (int k = 0; k < a.nsp; ++k) {
+      order[k] = k;
+      boris |= a.sp[k].kind == PB_KIND_BORIS;
+    }
+    for (int i = 1; i < a.nsp; ++i)
+      for (int j = i; j > 0 && bytes_per_particle(a.sp[order[j]], true) >
+                                   bytes_per_particle(a.sp[order[j - 1]], true); --j) {
+        const int tmp = order[j];
+        order[j] = order[j - 1];
+        order[j - 1] = tmp;
+      }
+    a.tile_start[0] = 0;
+    for (int k = 0; k < a.nsp; ++k) {
+      a.order[k] = order[k];
+      a.tile_start[k + 1] = a.tile_start[k] + (a.sp[order[k]].n + kChunk - 1) / kChunk;
+    }
+    LdgFn fn = boris ? k_push_quad<PB_BC_PERIODIC, true> : k_push_quad<PB_BC_PERIODIC, false>;
+    int bps = 0;
+    int rc = occupancy((const void *)fn, kThreads, 0, &bps);
+    if (rc) return rc;
+    fn<<<sms * bps, kThreads, 0, stream>>>(a);
+    PB_CHECK_LAUNCH("k_push_quad");
+    return PB_OK;
+  }
+  if (push && g_use_tma == 1 && all_move) {
     // Tile list: species by descending bytes/particle, full tiles only.
     int order[PB_MAX_SPECIES];
     for (int k = 0; k < a.nsp; ++k) order[k] = k;
@@ -867,7 +1313,7 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
     for (int k = 0; k < a.nsp; ++k) {
       const pb_species &s = a.sp[order[k]];
       a.order[k] = order[k];
-      a.tile_start[k + 1] = a.tile_start[k] + s.n / kTile;  // upper bound when n_dev shrinks
+      a.tile_start[k + 1] = a.tile_start[k] + s.n / tile_of(s.kind, s.yp != nullptr);
       const int sb = stage_bytes(s.kind, s.yp != nullptr);
       if (sb > smem) smem = sb;
     }
@@ -877,13 +1323,25 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
       goto ldg;
     }
     {
+      if (g_stages == 0) {
+        const char *env = getenv("PB_STAGES");
+        g_stages = env ? atoi(env) : 2;
+        if (g_stages < 2) g_stages = 2;
+        if (g_stages > kMaxStages) g_stages = kMaxStages;
+      }
+      if (g_ahead < 0) {
+        const char *env = getenv("PB_AHEAD");
+        g_ahead = env ? atoi(env) : 0;
+        if (g_ahead < 0) g_ahead = 0;
+        if (g_ahead > kMaxAhead) g_ahead = kMaxAhead;
+      }
       const int stride = smem;
-      smem *= kStages;
+      smem *= g_stages;
       TmaFn fn = k_push_tma<PB_BC_PERIODIC>;
       int bps = 0;
       int rc = occupancy((const void *)fn, kThreads + 32, smem, &bps);
       if (rc) return rc;
-      fn<<<sms * bps, kThreads + 32, smem, stream>>>(a, stride);
+      fn<<<sms * bps, kThreads + 32, smem, stream>>>(a, stride, g_stages, g_ahead);
       PB_CHECK_LAUNCH("k_push_tma");
       return PB_OK;
     }
