@@ -302,6 +302,8 @@ class Engine:
             ev[0].record(self.stream)
         rho = self.density()
         e = self.field(rho)
+        if self.cfg.field_solve and self.cfg.smoothing_passes > 0:
+            rho = self.rho_s  # the reference reports the smoothed density (harness.py:165-166)
         self.push(e)
         self.resort()
         if timed:

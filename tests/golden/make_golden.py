@@ -1,0 +1,268 @@
+"""Generate the golden fixtures in this directory by running the REFERENCE.
+
+Run in the build container (where /root/reference exists):
+    python tests/golden/make_golden.py
+It copies /root/reference/pkg to a scratch dir, builds its Cython kernels
+(python setup.py build_ext --inplace, the reference's own recipe), imports
+`picmc` from there with PICMC_BACKEND=compiled, and records inputs/outputs of
+the hot-path functions as small .npz files.  Nothing here is imported by the
+product; tests/ compare the oracle and the CUDA path against these files, so
+the GPU box never needs /root/reference.
+"""
+
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF = "/root/reference/pkg"
+SCRATCH = "/tmp/picmc_ref_golden"
+
+
+def import_reference():
+    if not os.path.exists(os.path.join(SCRATCH, "src", "picmc", "backends")):
+        shutil.rmtree(SCRATCH, ignore_errors=True)
+        shutil.copytree(REF, SCRATCH)
+    built = [f for f in os.listdir(os.path.join(SCRATCH, "src", "picmc", "backends")) if f.endswith(".so")]
+    if not built:
+        subprocess.run([sys.executable, "setup.py", "build_ext", "--inplace"], cwd=SCRATCH, check=True,
+                       stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+    os.environ["PICMC_BACKEND"] = "compiled"
+    sys.path.insert(0, os.path.join(SCRATCH, "src"))
+    sys.path.insert(0, os.path.join(SCRATCH, "tests"))
+    import picmc  # noqa: F401
+
+    return picmc
+
+
+def packed(seed, nc=13, cap=7):
+    # same recipe as pkg/tests/test_backends.py:21-39
+    rng = np.random.default_rng(seed)
+    counts = rng.integers(0, cap + 1, size=nc).astype(np.int64)
+    caps = np.full(nc, cap, dtype=np.int64)
+    offs = np.concatenate(([0], np.cumsum(caps[:-1]))).astype(np.int64)
+    total = int(caps.sum())
+    x, vx, vy, yp = np.zeros(total), np.zeros(total), np.zeros(total), np.zeros(total)
+    for j in range(nc):
+        n = counts[j]
+        sl = slice(offs[j], offs[j] + n)
+        x[sl] = rng.random(n)
+        vx[sl] = rng.standard_normal(n) * 0.3
+        vy[sl] = rng.standard_normal(n) * 0.3
+        yp[sl] = rng.standard_normal(n)
+    return x, vx, vy, yp, offs, counts
+
+
+def gen_backend(picmc):
+    from picmc import backends
+
+    k = backends.load_backend("compiled")
+    out = {}
+    for seed in range(5):
+        x, vx, vy, yp, offs, counts = packed(seed)
+        out[f"s{seed}_x"], out[f"s{seed}_vx"], out[f"s{seed}_vy"], out[f"s{seed}_yp"] = x, vx, vy, yp
+        out[f"s{seed}_offs"], out[f"s{seed}_counts"] = offs, counts
+        left, right = k.deposit_partials(x, offs, counts)
+        out[f"s{seed}_dep_left"], out[f"s{seed}_dep_right"] = left, right
+        nodes = np.random.default_rng(100 + seed).standard_normal(len(counts) + 1)
+        out[f"s{seed}_nodes"] = nodes
+        out[f"s{seed}_gather"] = k.gather(nodes, x, offs, counts)
+        accel = np.random.default_rng(200 + seed).standard_normal(len(counts) + 1) * 0.1
+        out[f"s{seed}_accel"] = accel
+        for wa in (0, 1):
+            for wy in (0, 1):
+                a = [x.copy(), vx.copy(), vy.copy(), yp.copy() if wy else None]
+                k.fused_move(accel if wa else None, *a, offs, counts, 2.0)
+                out[f"s{seed}_move_a{wa}y{wy}_x"] = a[0]
+                out[f"s{seed}_move_a{wa}y{wy}_vx"] = a[1]
+                if wy:
+                    out[f"s{seed}_move_a{wa}y{wy}_yp"] = a[3]
+    np.savez_compressed(os.path.join(HERE, "backend_kernels.npz"), **out)
+
+
+def gen_resort(picmc):
+    """Exact cell-transfer cases of pkg/tests/test_mover.py:106-160, as
+    (src cell, x) -> (dest cell, x) through the reference resort()."""
+    from picmc.core import CellSortedStore, Grid1D, SpeciesDef
+    from picmc.mover import resort
+
+    cases = [(8, 3, -0.25), (8, 0, -0.25), (8, 7, 1.25), (100, 0, -0.3), (8, 1, 2.0), (8, 2, 3.5),
+             (8, 4, -1e-18), (8, 5, 0.999999999), (8, 6, 1.0), (8, 0, -6.5), (8, 7, 7.999), (8, 3, -0.0),
+             (37, 36, 1e-300 + 1.0), (37, 0, -35.5)]
+    rows = []
+    for nc, cell, x in cases:
+        store = CellSortedStore(Grid1D.from_cells(nc, float(nc)), [SpeciesDef("s", 0.0, 1.0)], initial_cap=4)
+        store.append(0, cell, {"x": x, "vx": 0.5})
+        resort(store)
+        j = int(np.nonzero(store.counts(0))[0][0])
+        xo = float(store.data(0)["x"][store.cell_slice(0, j)][0])
+        rows.append((nc, cell, x, j, xo))
+    arr = np.array(rows, dtype=object)
+    np.savez_compressed(os.path.join(HERE, "resort_kats.npz"),
+                        nc=np.array([r[0] for r in rows], dtype=np.int64),
+                        cell=np.array([r[1] for r in rows], dtype=np.int64),
+                        x=np.array([r[2] for r in rows], dtype=np.float64),
+                        dest=np.array([r[3] for r in rows], dtype=np.int64),
+                        xo=np.array([r[4] for r in rows], dtype=np.float64))
+    del arr
+
+
+def gen_rng(picmc):
+    from picmc import rng
+
+    keys = [0, 1, 1234567, 20260819, (1 << 64) - 1]
+    out = {"keys": np.array(keys, dtype=np.uint64)}
+    out["mix64"] = np.array([rng.mix64(k) for k in keys], dtype=np.uint64)
+    out["derive"] = np.array([[rng.derive(k, n) for n in range(6)] for k in keys], dtype=np.uint64)
+    out["stream"] = np.array([rng.stream(20260819, 1, isp) for isp in range(3)], dtype=np.uint64)
+    ctr = np.arange(64, dtype=np.int64)
+    out["uniforms"] = rng.uniforms(np.uint64(out["stream"][0]), ctr)
+    out["uniforms_open"] = rng.uniforms_open(np.uint64(out["stream"][1]), ctr)
+    np.savez_compressed(os.path.join(HERE, "rng.npz"), **out)
+
+
+def small_config(**kw):
+    from conftest import make_config  # the reference's own test builder
+
+    return make_config(**kw)
+
+
+def config_record(cfg):
+    return json.dumps({
+        "nc": cfg.grid.nc, "length_m": cfg.grid.length_m, "dt_s": cfg.consts.dt_s,
+        "species": [[s.name, s.charge_c, s.mass_kg, s.nstep, s.active_mover, s.track_transverse]
+                    for s in cfg.species],
+        "temperatures_ev": cfg.temperatures_ev, "densities_m3": cfg.densities_m3, "ppc0": cfg.ppc0,
+        "n_steps": cfg.n_steps, "seed": cfg.seed, "boundary": cfg.boundary,
+        "field_solve": cfg.field_solve, "smoothing_passes": cfg.smoothing_passes,
+    })
+
+
+def flatten_store(store):
+    """Live particles in cell-major order with their cell index."""
+    out = {}
+    for isp in range(store.nsp):
+        idx = store.live_indices(isp)
+        out[f"sp{isp}_cell"] = store.cell_of_live(isp).astype(np.int32)
+        for name, arr in store.data(isp).items():
+            out[f"sp{isp}_{name}"] = arr[idx].copy()
+    return out
+
+
+def gen_init(picmc):
+    from picmc.core import init_plasma
+
+    cfg = small_config(nc=16, ppc0=8)
+    store = init_plasma(cfg)
+    out = flatten_store(store)
+    out["config"] = np.array(config_record(cfg))
+    out["weights"] = np.array(store.weights)
+    np.savez_compressed(os.path.join(HERE, "init_plasma.npz"), **out)
+
+
+def gen_runs(picmc):
+    from picmc.decomposition import merge_stores
+    from picmc.harness import run_simulation
+
+    runs = {
+        "run_periodic_nofield": dict(nc=64, ppc0=8, n_steps=20),
+        "run_periodic_field": dict(nc=64, ppc0=8, n_steps=20, field_solve=True, smoothing_passes=1),
+        "run_dirichlet_field": dict(nc=48, ppc0=8, n_steps=20, field_solve=True, smoothing_passes=2,
+                                    boundary="dirichlet"),
+    }
+    for name, kw in runs.items():
+        cfg = small_config(**kw)
+        hist = {"rho": [], "e": []}
+        box = {}
+
+        def probe(step, st, hist=hist, box=box):
+            hist["rho"].append(st["rho"].copy())
+            hist["e"].append(st["e_field"].copy())
+            box["stores"], box["partition"] = st["stores"], st["partition"]
+
+        m = run_simulation(cfg, on_step=probe)
+        final = merge_stores(box["stores"], box["partition"], cfg.grid)
+        out = flatten_store(final)
+        out["rho"] = np.array(hist["rho"])
+        out["e_field"] = np.array(hist["e"])
+        out["totals"] = np.array([[r[f"total_{s.name}"] for s in cfg.species] for r in m.diagnostics])
+        out["config"] = np.array(config_record(cfg))
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+
+
+def gen_fields(picmc):
+    from picmc.core import Grid1D, PhysicalConstants
+    from picmc.fields import compute_efield, smooth_density, solve_poisson
+
+    rng = np.random.default_rng(77)
+    out = {}
+    for nc in (8, 100, 1000):
+        grid = Grid1D.from_cells(nc, nc * 1e-5)
+        consts = PhysicalConstants(dt_s=4e-14)
+        rho = 50.0 * rng.standard_normal(nc + 1)
+        rho[nc] = rho[0]
+        out[f"n{nc}_rho"] = rho
+        out[f"n{nc}_smooth1"] = smooth_density(rho, 1)
+        out[f"n{nc}_smooth3"] = smooth_density(rho, 3)
+        for bc in ("periodic", "dirichlet"):
+            phi = solve_poisson(rho, grid, consts, bc, 1.5, -2.0)
+            out[f"n{nc}_{bc}_phi"] = phi
+            out[f"n{nc}_{bc}_e"] = compute_efield(phi, grid, bc)
+    np.savez_compressed(os.path.join(HERE, "fields.npz"), **out)
+
+
+def gen_mover_multistep(picmc):
+    """mover_phase + resort over 30 steps with multi-cell jumps, signed zeros,
+    nstep=3 + transverse, non-zero E (SURVEY Appendix B.10 setup)."""
+    from picmc.core import CellSortedStore, Grid1D, PhysicalConstants, SpeciesDef
+    from picmc.mover import mover_phase, resort
+    from picmc.scheduler import Scheduler
+
+    nc, ppc = 37, 20
+    species = [SpeciesDef("q", -1.602176634e-19, 9.1093837015e-31),
+               SpeciesDef("n", 0.0, 3.3e-27, nstep=3, track_transverse=True)]
+    store = CellSortedStore(Grid1D.from_cells(nc, nc * 1e-5), species, initial_cap=4 * ppc)
+    rng = np.random.default_rng(2026)
+    for isp in range(2):
+        store.counts(isp)[:] = ppc
+        idx = store.live_indices(isp)
+        d = store.data(isp)
+        d["x"][idx] = rng.random(idx.size)
+        for f in ("vx", "vy", "vz"):
+            d[f][idx] = 0.7 * rng.standard_normal(idx.size)
+        d["vx"][idx[::17]] = -0.0
+        if "yp" in d:
+            d["yp"][idx] = rng.standard_normal(idx.size)
+    init = flatten_store(store)
+    consts = PhysicalConstants(dt_s=4e-14)
+    e_hist = []
+    with Scheduler(workers=2, trace=False) as sched:
+        for _ in range(30):
+            e = 2e3 * rng.standard_normal(nc + 1)
+            e_hist.append(e)
+            mover_phase(store, e, consts, sched, grainsize=5)
+            resort(store)
+    out = {f"init_{k}": v for k, v in init.items()}
+    out.update({f"final_{k}": v for k, v in flatten_store(store).items()})
+    out["e_hist"] = np.array(e_hist)
+    out["dt_s"] = np.array(4e-14)
+    out["dx_m"] = np.array(store.grid.dx_m)
+    np.savez_compressed(os.path.join(HERE, "mover_multistep.npz"), **out)
+
+
+if __name__ == "__main__":
+    ref = import_reference()
+    gen_backend(ref)
+    gen_resort(ref)
+    gen_rng(ref)
+    gen_init(ref)
+    gen_runs(ref)
+    gen_fields(ref)
+    gen_mover_multistep(ref)
+    for f in sorted(os.listdir(HERE)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -1,0 +1,220 @@
+"""Pin the oracle (and the product's host-side init/RNG) to the reference.
+
+CPU-only.  Golden vectors come from running the reference itself
+(tests/golden/make_golden.py); when the reference's own compiled kernels are
+built into oracle/_ref (build container only) they are checked too.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import bits_equal, load_golden
+from oracle import oracle
+
+
+@pytest.fixture(scope="module")
+def bk():
+    return load_golden("backend_kernels.npz")
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_c_oracle_packed_kernels_match_reference(bk, seed):
+    g = {k[len(f"s{seed}_"):]: v for k, v in bk.items() if k.startswith(f"s{seed}_")}
+    left, right = oracle.deposit_partials(g["x"], g["offs"], g["counts"])
+    assert bits_equal(left, g["dep_left"]) and bits_equal(right, g["dep_right"])
+    assert bits_equal(oracle.gather(g["nodes"], g["x"], g["offs"], g["counts"]), g["gather"])
+    for wa in (0, 1):
+        for wy in (0, 1):
+            a = [g["x"].copy(), g["vx"].copy(), g["vy"].copy(), g["yp"].copy() if wy else None]
+            oracle.fused_move(g["accel"] if wa else None, *a, g["offs"], g["counts"], 2.0)
+            assert bits_equal(a[0], g[f"move_a{wa}y{wy}_x"])
+            assert bits_equal(a[1], g[f"move_a{wa}y{wy}_vx"])
+            if wy:
+                assert bits_equal(a[3], g[f"move_a{wa}y{wy}_yp"])
+
+
+def test_reference_build_matches_golden(bk):
+    ref = oracle.ref_kernels()
+    if ref is None:
+        pytest.skip("oracle/_ref not built (no /root/reference here)")
+    g = {k[3:]: v for k, v in bk.items() if k.startswith("s0_")}
+    left, right = ref.deposit_partials(g["x"], g["offs"], g["counts"])
+    assert bits_equal(left, g["dep_left"]) and bits_equal(right, g["dep_right"])
+
+
+def test_flat_wrap_matches_reference_resort_kats():
+    """Exact transfers: left neighbour, wrap both ends, non-dyadic offset,
+    multi-cell jumps, integer landing, -1e-18 carry, -0.0 (test_mover.py:106-160)."""
+    g = load_golden("resort_kats.npz")
+    for nc, cell, x, dest, xo in zip(g["nc"], g["cell"], g["x"], g["dest"], g["xo"]):
+        xs = np.array([x])
+        c = np.array([cell], dtype=np.int32)
+        z = np.zeros(1)
+        _, removed, cfl = oracle.step_flat(0, 0, 1.0, 0.0, np.zeros(nc + 1), int(nc), xs, z.copy(), z.copy(),
+                                           z.copy(), None, c)
+        assert cfl == -1 and removed[0] == 0
+        assert c[0] == dest and bits_equal(xs, [xo])
+
+
+def test_flat_cfl_detection():
+    xs = np.array([0.5, 8.5])
+    c = np.array([0, 1], dtype=np.int32)
+    z = np.zeros(2)
+    _, _, cfl = oracle.step_flat(0, 0, 1.0, 0.0, np.zeros(9), 8, xs, z.copy(), z.copy(), z.copy(), None, c)
+    assert cfl == 1
+
+
+def test_flat_absorbing_counts():
+    xs = np.array([-0.25, 0.5, 1.5, 0.75, 2.0])
+    c = np.array([0, 0, 3, 3, 1], dtype=np.int32)
+    z = np.zeros(5)
+    moved, removed, cfl = oracle.step_flat(0, 1, 1.0, 0.0, np.zeros(5), 4, xs, z.copy(), z.copy(), z.copy(),
+                                           None, c)
+    assert cfl == -1 and moved == 3
+    assert removed.tolist() == [1, 0, 2, 0, 0]
+    assert c[4] == 3 and xs[4] == 0.0
+
+
+def _flat_from(g, prefix, isp):
+    keys = [k for k in g if k.startswith(f"{prefix}sp{isp}_")]
+    return {k[len(f"{prefix}sp{isp}_"):]: g[k].copy() for k in keys}
+
+
+def test_flat_restatement_matches_reference_mover_and_resort():
+    """30 steps of mover_phase + resort on the reference (2 workers, block
+    tasks) equal the flat per-particle restatement bit for bit as multisets."""
+    g = load_golden("mover_multistep.npz")
+    dt, dx = float(g["dt_s"]), float(g["dx_m"])
+    nc = g["e_hist"].shape[1] - 1
+    q, m = -1.602176634e-19, 9.1093837015e-31
+    coef = q * dt * dt / (m * dx)
+    sps = [(_flat_from(g, "init_", 0), 2, 1.0, coef), (_flat_from(g, "init_", 1), 1, 3.0, 0.0)]
+    for e in g["e_hist"]:
+        for f, kind, fnstep, kc in sps:
+            _, _, cfl = oracle.step_flat(kind, 0, fnstep, kc, e, nc, f["x"], f["vx"], f["vy"], f["vz"],
+                                         f.get("yp"), f["cell"])
+            assert cfl == -1
+    for isp, (f, *_rest) in enumerate(sps):
+        ref = _flat_from(g, "final_", isp)
+        fields = {k: v for k, v in f.items() if k != "cell"}
+        rfields = {k: v for k, v in ref.items() if k != "cell"}
+        assert np.array_equal(oracle.canonical(f["cell"], fields), oracle.canonical(ref["cell"], rfields))
+
+
+def test_numpy_field_oracles_match_reference():
+    g = load_golden("fields.npz")
+    for nc in (8, 100, 1000):
+        rho = g[f"n{nc}_rho"]
+        assert bits_equal(oracle.smooth_density(rho, 1), g[f"n{nc}_smooth1"])
+        assert bits_equal(oracle.smooth_density(rho, 3), g[f"n{nc}_smooth3"])
+        for bc in ("periodic", "dirichlet"):
+            phi = oracle.solve_poisson(rho, nc, nc * 1e-5 / nc, 8.8541878128e-12, bc, 1.5, -2.0)
+            assert bits_equal(phi, g[f"n{nc}_{bc}_phi"])
+            assert bits_equal(oracle.compute_efield(phi, nc, nc * 1e-5 / nc, bc), g[f"n{nc}_{bc}_e"])
+
+
+def test_fixed_point_deposit_tolerance_vs_sequential():
+    """The device's fixed-point deposit restated: per cell within
+    1e-13 * max(1, count) of the reference's sequential fp64 sums, counts exact."""
+    rng = np.random.default_rng(3)
+    nc, n = 500, 60_000
+    cell = np.sort(rng.integers(0, nc, n)).astype(np.int32)
+    x = rng.random(n)
+    x[::97] = 0.0
+    x[::89] = np.nextafter(1.0, 0.0)
+    R, C = oracle.deposit_fixed(x, cell, nc)
+    lf, rf = oracle.fixed_to_raw(R, C)
+    ls, rs = oracle.deposit_seq(x, cell, nc)
+    tol = 1e-13 * np.maximum(1.0, C.astype(float))
+    assert np.all(np.abs(lf - ls) <= tol) and np.all(np.abs(rf - rs) <= tol)
+    assert np.array_equal(C, np.bincount(cell, minlength=nc).astype(np.uint64))
+
+
+def test_host_init_matches_reference_init_plasma():
+    from paper_2404_10270_b200 import Grid1D, PhysicalConstants, RunConfig, SpeciesDef
+    from paper_2404_10270_b200.core import init_species_host, macro_weight
+
+    g = load_golden("init_plasma.npz")
+    c = json.loads(str(g["config"]))
+    species = [SpeciesDef(n, q, m, nstep=ns, active_mover=am, track_transverse=tt)
+               for n, q, m, ns, am, tt in c["species"]]
+    cfg = RunConfig(grid=Grid1D.from_cells(c["nc"], c["length_m"]), consts=PhysicalConstants(dt_s=c["dt_s"]),
+                    species=species, temperatures_ev=c["temperatures_ev"], densities_m3=c["densities_m3"],
+                    ppc0=c["ppc0"], n_steps=c["n_steps"], seed=c["seed"])
+    for isp in range(len(species)):
+        f = init_species_host(cfg, isp)
+        assert np.array_equal(f.cell, g[f"sp{isp}_cell"])
+        for name, arr in f.fields().items():
+            assert bits_equal(arr, g[f"sp{isp}_{name}"]), name
+        assert macro_weight(cfg, isp) == g["weights"][isp]
+    # sharded init (cells [lo, hi)) is a bitwise slice of the full load
+    part = init_species_host(cfg, 0, 5, 11)
+    full = init_species_host(cfg, 0)
+    sl = slice(5 * cfg.ppc0, 11 * cfg.ppc0)
+    assert bits_equal(part.vx, full.vx[sl]) and np.array_equal(part.cell, full.cell[sl])
+
+
+def test_rng_matches_reference():
+    from paper_2404_10270_b200 import rng
+
+    g = load_golden("rng.npz")
+    keys = [int(k) for k in g["keys"]]
+    assert [rng.mix64(k) for k in keys] == [int(v) for v in g["mix64"]]
+    assert [[rng.derive(k, n) for n in range(6)] for k in keys] == g["derive"].astype(object).tolist()
+    streams = [rng.stream(20260819, 1, isp) for isp in range(3)]
+    assert streams == [int(v) for v in g["stream"]]
+    ctr = np.arange(64, dtype=np.int64)
+    assert bits_equal(rng.uniforms(np.uint64(streams[0]), ctr), g["uniforms"])
+    assert bits_equal(rng.uniforms_open(np.uint64(streams[1]), ctr), g["uniforms_open"])
+
+
+def test_splitmix64_published_vector():
+    """Vigna's splitmix64 with seed 1234567 (pkg/tests/test_rng.py:14-24):
+    the generator state advances by GOLDEN and is finalised by mix64."""
+    from paper_2404_10270_b200.rng import GOLDEN, M64, mix64
+
+    state, out = 1234567, []
+    for _ in range(5):
+        state = (state + GOLDEN) & M64
+        out.append(mix64(state))
+    assert out == [6457827717110365317, 3203168211198807973, 9817491932198370423,
+                   4593380528125082431, 16408922859458223821]
+
+
+def test_periodic_run_restatement_matches_reference_run():
+    """Reference run_simulation (E = 0, 20 steps, 3 species): the flat oracle
+    reproduces every final particle bit for bit and every per-step density
+    within the stated deposit tolerance."""
+    from paper_2404_10270_b200 import Grid1D, PhysicalConstants, RunConfig, SpeciesDef
+    from paper_2404_10270_b200.core import init_species_host, macro_weight
+
+    g = load_golden("run_periodic_nofield.npz")
+    c = json.loads(str(g["config"]))
+    species = [SpeciesDef(n, q, m, nstep=ns, active_mover=am, track_transverse=tt)
+               for n, q, m, ns, am, tt in c["species"]]
+    cfg = RunConfig(grid=Grid1D.from_cells(c["nc"], c["length_m"]), consts=PhysicalConstants(dt_s=c["dt_s"]),
+                    species=species, temperatures_ev=c["temperatures_ev"], densities_m3=c["densities_m3"],
+                    ppc0=c["ppc0"], n_steps=c["n_steps"], seed=c["seed"], field_solve=False)
+    nc = cfg.grid.nc
+    flats = [init_species_host(cfg, k) for k in range(len(species))]
+    coef_dep = [sp.charge_c * macro_weight(cfg, k) / cfg.grid.dx_m for k, sp in enumerate(species) if sp.charged]
+    kick = [sp.charge_c * cfg.consts.dt_s * cfg.consts.dt_s / (sp.mass_kg * cfg.grid.dx_m) for sp in species]
+    e = np.zeros(nc + 1)
+    for step in range(cfg.n_steps):
+        raw = []
+        for k, sp in enumerate(species):
+            if sp.charged:
+                raw.extend(oracle.deposit_seq(flats[k].x, flats[k].cell, nc))
+        _, _, rho = oracle.rho_from_raw(np.stack(raw).reshape(-1, 2, nc), coef_dep, nc, True)
+        scale = max(abs(cd) for cd in coef_dep) * 2 * cfg.ppc0
+        assert np.max(np.abs(rho - g["rho"][step])) <= 1e-12 * scale
+        for k, sp in enumerate(species):
+            kind = 2 if sp.charged else 1
+            f = flats[k]
+            oracle.step_flat(kind, 0, float(sp.nstep), kick[k], e, nc, f.x, f.vx, f.vy, f.vz, f.yp, f.cell)
+    for k in range(len(species)):
+        ref = {n: g[f"sp{k}_{n}"] for n in flats[k].fields()}
+        assert np.array_equal(oracle.canonical(flats[k].cell, flats[k].fields()),
+                              oracle.canonical(g[f"sp{k}_cell"], ref))
