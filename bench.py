@@ -87,7 +87,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except OSError:
@@ -240,7 +240,7 @@ def run_ours(args, rank, world, local_rank):
     # The mover kernel alone: CUDA events on the engine stream right around the
     # pb_push_deposit launch, over eager steps (host stays ahead of the GPU).
     eng.phase_events.clear()
-    for _ in range(min(args.steps, 20)):
+    for _ in range(min(args.steps, 50)):
         eng.step(timed=True)
     eng.sync()
     push_ms = float(np.mean(eng.mover_ms()))
@@ -255,7 +255,7 @@ def run_ours(args, rank, world, local_rank):
     nodes = nc_total + 1
     e_host = torch.zeros(nodes, dtype=torch.float64).pin_memory()
     rho_host = torch.empty(nodes, dtype=torch.float64).pin_memory()
-    e2e_steps = max(3, args.steps // 2)
+    e2e_steps = max(3, min(args.steps, 200))
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -324,7 +324,7 @@ def run_ours(args, rank, world, local_rank):
         },
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "peak_source": peak_kind, "kernel": "k_push_deposit",
+            "peak_source": peak_kind, "kernel": "k_push_quad",
             "alg_bytes_per_launch": alg_bytes, "push_ms": push_ms,
             "traffic": None if traffic is None else traffic.get("dram_bytes_per_launch"),
         },
@@ -342,8 +342,8 @@ def run_ours(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--sort-every", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

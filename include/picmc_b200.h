@@ -146,6 +146,15 @@ int pb_rho_epilogue(const uint64_t *bins, const double *coef, int ndep,
                     int64_t nc, int field_bc, double *left, double *right,
                     double *rho, void *stream);
 
+/* The engine's per-step form of pb_rho_epilogue: additionally zeroes the
+ * other ping-pong bin set `bins_next` (same shape, written by the coming
+ * pb_push_deposit) and the mover work counter (&status->tile_next), so a
+ * step is exactly two kernels.  Either pointer may be NULL. */
+int pb_density_step(const uint64_t *bins, uint64_t *bins_next,
+                    uint64_t *counter, const double *coef, int ndep,
+                    int64_t nc, int field_bc, double *left, double *right,
+                    double *rho, void *stream);
+
 /* Fill the holes left by absorbed particles from the tail (warp-ballot
  * stream compaction); updates *n_dev.  `scratch` needs
  * pb_compact_scratch_bytes(n) bytes. */

@@ -77,6 +77,8 @@ _SIGS = {
                                        _i64, _p, _p, _p]),
     "pb_rho_epilogue": (ctypes.c_int, [_p, ctypes.POINTER(_f64), ctypes.c_int, _i64,
                                        ctypes.c_int, _p, _p, _p, _p]),
+    "pb_density_step": (ctypes.c_int, [_p, _p, _p, ctypes.POINTER(_f64), ctypes.c_int, _i64,
+                                       ctypes.c_int, _p, _p, _p, _p]),
     "pb_compact_scratch_bytes": (ctypes.c_size_t, [_i64]),
     "pb_compact": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int, _p, _p,
                                   ctypes.c_size_t, _p]),

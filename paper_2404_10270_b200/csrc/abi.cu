@@ -49,9 +49,19 @@ __global__ void k_rho_epilogue(const uint64_t *__restrict__ bins, CoefArgs ca,
                                int ndep, int64_t nc, int field_bc,
                                double *__restrict__ left,
                                double *__restrict__ right,
-                               double *__restrict__ rho) {
+                               double *__restrict__ rho,
+                               uint64_t *__restrict__ clear,
+                               uint64_t *__restrict__ counter) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g > nc) return;
+  // Step fusion: zero the other (ping-pong) bin set for the coming mover
+  // launch and reset the mover's work counter.
+  if (clear && g < nc)
+    for (int s = 0; s < ndep; ++s) {
+      clear[(size_t)s * 2 * nc + g] = 0;
+      clear[(size_t)s * 2 * nc + nc + g] = 0;
+    }
+  if (counter && g == 0) *counter = 0;
   double lg = 0.0, rg = 0.0, lp = 0.0, rp = 0.0;
   if (g < nc) {
     weighted_partials(bins, ca.c, ndep, nc, g, lg, rg);
@@ -90,9 +100,9 @@ extern "C" int pb_device_sm_count(int *out) {
   return PB_OK;
 }
 
-extern "C" int pb_rho_epilogue(const uint64_t *bins, const double *coef,
-                               int ndep, int64_t nc, int field_bc, double *left,
-                               double *right, double *rho, void *stream) {
+static int rho_epilogue(const uint64_t *bins, const double *coef, int ndep, int64_t nc,
+                        int field_bc, double *left, double *right, double *rho,
+                        uint64_t *clear, uint64_t *counter, void *stream) {
   if (ndep < 0 || ndep > PB_MAX_SPECIES) {
     pb::set_error("ndep=%d outside [0, %d]", ndep, PB_MAX_SPECIES);
     return PB_ERR_INVALID;
@@ -105,15 +115,31 @@ extern "C" int pb_rho_epilogue(const uint64_t *bins, const double *coef,
     pb::set_error("unknown field boundary %d", field_bc);
     return PB_ERR_INVALID;
   }
-  pb::CoefArgs ca;
+  pb::CoefArgs ca;  // passed by value: no host pointer reaches the device
   memset(&ca, 0, sizeof(ca));
   for (int s = 0; s < ndep; ++s) ca.c[s] = coef[s];
   const int threads = 256;
   const int64_t blocks = (nc + 1 + threads - 1) / threads;
   pb::k_rho_epilogue<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
-      bins, ca, ndep, nc, field_bc, left, right, rho);
+      bins, ca, ndep, nc, field_bc, left, right, rho, clear, counter);
   PB_CHECK_LAUNCH("k_rho_epilogue");
   return PB_OK;
+}
+
+extern "C" int pb_rho_epilogue(const uint64_t *bins, const double *coef, int ndep, int64_t nc,
+                               int field_bc, double *left, double *right, double *rho,
+                               void *stream) {
+  return rho_epilogue(bins, coef, ndep, nc, field_bc, left, right, rho, nullptr, nullptr, stream);
+}
+
+extern "C" int pb_density_step(const uint64_t *bins, uint64_t *bins_next, uint64_t *counter,
+                               const double *coef, int ndep, int64_t nc, int field_bc,
+                               double *left, double *right, double *rho, void *stream) {
+  if (bins_next == bins && bins != nullptr) {
+    pb::set_error("pb_density_step: bins_next must not alias bins");
+    return PB_ERR_INVALID;
+  }
+  return rho_epilogue(bins, coef, ndep, nc, field_bc, left, right, rho, bins_next, counter, stream);
 }
 
 // ---------------------------------------------------------------------------

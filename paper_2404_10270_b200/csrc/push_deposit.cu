@@ -1129,7 +1129,9 @@ __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
     while (kk + 1 < a.nsp && (int64_t)c >= a.tile_start[kk + 1]) ++kk;
     const int isp = a.order[kk];
     const pb_species &s = a.sp[isp];
-    const int64_t n = s.n;
+    // Absorbing walls shrink the live count on the device: chunks past it
+    // are empty (the chunk list is built from the host's upper bound).
+    const int64_t n = s.n_dev ? *s.n_dev : s.n;
     const int64_t beg = ((int64_t)c - a.tile_start[kk]) * kChunk;
     const int64_t end = beg + kChunk < n ? beg + kChunk : n;
     if (isp != cur) {
@@ -1269,7 +1271,7 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
   const int sms = sm_count();
   if (sms == 0) return cuda_status(cudaGetLastError(), "device query");
 
-  if (push && g_use_tma == 2 && all_move && bc == PB_BC_PERIODIC) {
+  if (push && g_use_tma == 2 && all_move) {
     // Chunk list: species by descending bytes/particle.
     int order[PB_MAX_SPECIES];
     bool boris = false;
@@ -1289,7 +1291,9 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
       a.order[k] = order[k];
       a.tile_start[k + 1] = a.tile_start[k] + (a.sp[order[k]].n + kChunk - 1) / kChunk;
     }
-    LdgFn fn = boris ? k_push_quad<PB_BC_PERIODIC, true> : k_push_quad<PB_BC_PERIODIC, false>;
+    LdgFn fn = bc == PB_BC_PERIODIC
+                   ? (boris ? k_push_quad<PB_BC_PERIODIC, true> : k_push_quad<PB_BC_PERIODIC, false>)
+                   : (boris ? k_push_quad<PB_BC_ABSORBING, true> : k_push_quad<PB_BC_ABSORBING, false>);
     int bps = 0;
     int rc = occupancy((const void *)fn, kThreads, 0, &bps);
     if (rc) return rc;

@@ -139,7 +139,11 @@ class Engine:
         self._coef_c = (ctypes.c_double * max(ndep, 1))(*self.coef_dep)
         nc = self.nc
         with torch.cuda.stream(self.stream):
-            self.bins = torch.zeros(max(ndep, 1) * 2 * nc, dtype=torch.int64, device=self.device)
+            # Ping-pong fixed-point bins: the mover deposits into one set while
+            # the other holds the density being reduced / stitched.
+            self.bins_pp = [torch.zeros(max(ndep, 1) * 2 * nc, dtype=torch.int64, device=self.device)
+                            for _ in range(2)]
+            self.cur = 0
             self.rho = torch.zeros(nc + 1, dtype=torch.float64, device=self.device)
             self.left = torch.zeros(nc, dtype=torch.float64, device=self.device)
             self.right = torch.zeros(nc, dtype=torch.float64, device=self.device)
@@ -159,7 +163,8 @@ class Engine:
         self.phase_events = []
         self._timing = None
         self._arr = None
-        self.graph = None
+        self.graphs = {}
+        self._next_clear = False
         # Work counter of the TMA mover: the pb_status.tile_next word.
         off = ctypes.sizeof(_lib.PbStatus) - 8
         self._tile_counter = self.status[off:off + 8]
@@ -195,6 +200,11 @@ class Engine:
             self._arr = species_array(self.sp)
         return self._arr
 
+    @property
+    def bins(self) -> torch.Tensor:
+        """The bin set holding the latest deposit (read by the next density())."""
+        return self.bins_pp[self.cur]
+
     def deposit_current(self):
         """Fixed-point deposit of the current positions into the bins
         (the reference's step-start deposit, harness.py:148-160)."""
@@ -215,15 +225,17 @@ class Engine:
 
     # -- step phases ------------------------------------------------------------
     def density(self) -> torch.Tensor:
-        """Reduce the bins across GPUs and produce left/right/rho."""
+        """Reduce the bins across GPUs and produce left/right/rho; also clears
+        the other bin set and the mover work counter (one kernel)."""
         with torch.cuda.stream(self.stream):
             if self.world > 1:
                 reduce_bins(self.bins, self.group)
-            _lib.check(self.lib.pb_rho_epilogue(
-                self.bins.data_ptr(), self._coef_c, self.ndep, self.nc, self.field_bc,
+            _lib.check(self.lib.pb_density_step(
+                self.bins.data_ptr(), self.bins_pp[1 - self.cur].data_ptr(), self._tile_counter.data_ptr(),
+                self._coef_c, self.ndep, self.nc, self.field_bc,
                 self.left.data_ptr(), self.right.data_ptr(), self.rho.data_ptr(), self._sh()),
-                "pb_rho_epilogue")
-            self.bins.zero_()
+                "pb_density_step")
+        self._next_clear = True
         return self.rho
 
     def field(self, rho: torch.Tensor) -> torch.Tensor:
@@ -250,14 +262,19 @@ class Engine:
         if e is None:
             e = self.e
         arr, n = self._species()
+        target = self.bins_pp[1 - self.cur]
         with torch.cuda.stream(self.stream):
-            self._tile_counter.zero_()
+            if not self._next_clear:  # push() without a density() in between
+                target.zero_()
+                self._tile_counter.zero_()
             if self._timing is not None:
                 self._timing[0].record(self.stream)
-            _lib.check(self.lib.pb_push_deposit(arr, n, e.data_ptr(), self.nc, self.bc, self.bins.data_ptr(),
+            _lib.check(self.lib.pb_push_deposit(arr, n, e.data_ptr(), self.nc, self.bc, target.data_ptr(),
                                                 self.status.data_ptr(), self._sh()), "pb_push_deposit")
             if self._timing is not None:
                 self._timing[1].record(self.stream)
+        self.cur = 1 - self.cur
+        self._next_clear = False
 
     def resort(self):
         with torch.cuda.stream(self.stream):
@@ -285,7 +302,7 @@ class Engine:
                                                     self._sh()), "pb_sort_by_cell")
                 s.swap_with_spare()
             self._arr = None
-            self.graph = None  # captured pointers are stale
+            self.graphs = {}  # captured pointers are stale
 
     def step(self, timed: bool = False):
         """One full cycle.  Returns rho/E of this step (device tensors).
@@ -318,37 +335,52 @@ class Engine:
 
     # -- CUDA graph replay --------------------------------------------------------------
     def capture(self):
-        """Capture one step (deposit epilogue, field, mover, compaction) as a
-        CUDA graph; replay() then costs one launch per step.  Sort steps run
-        eagerly and invalidate the graph (buffers are swapped)."""
+        """Capture two steps (even + odd bin set) as one CUDA graph, starting
+        from the current ping-pong parity; replay() then costs one launch per
+        two steps.  Sort steps run eagerly and invalidate the graphs."""
         self.sync()
         self.stream.synchronize()
         g = torch.cuda.CUDAGraph()
-        # Warm the allocator / occupancy caches outside the capture.
+        start = self.cur
         with torch.cuda.graph(g, stream=self.stream):
-            rho = self.density()
-            e = self.field(rho)
-            self.push(e)
-            if self.absorbing:
-                arr, n = self._species()
-                _lib.check(self.lib.pb_compact(arr, n, self.status.data_ptr(), self.compact_scratch.data_ptr(),
-                                               self.compact_scratch.numel(), self._sh()), "pb_compact")
-        self.graph = g
+            for _ in range(2):
+                rho = self.density()
+                e = self.field(rho)
+                self.push(e)
+                if self.absorbing:
+                    arr, n = self._species()
+                    _lib.check(self.lib.pb_compact(arr, n, self.status.data_ptr(),
+                                                   self.compact_scratch.data_ptr(),
+                                                   self.compact_scratch.numel(), self._sh()), "pb_compact")
+        assert self.cur == start
+        self.graphs[start] = g
         return g
 
+    def _sort_due(self, k: int) -> bool:
+        return bool(self.sort_every) and (self.step_index + k) % self.sort_every == 0
+
     def replay(self, steps: int = 1):
-        """Run `steps` cycles through the captured graph (sorts included)."""
+        """Run `steps` cycles, two at a time through the captured graph; odd
+        remainders and sort steps run eagerly."""
         caller = torch.cuda.current_stream(self.device)
         self.stream.wait_stream(caller)
-        for _ in range(steps):
-            if self.sort_every and (self.step_index + 1) % self.sort_every == 0:
-                self.step()  # eager step with the sort at its end
-                continue
-            if self.graph is None:
-                self.capture()
-            with torch.cuda.stream(self.stream):
-                self.graph.replay()
-            self.step_index += 1
+        check, self.check_every = self.check_every, 0
+        try:
+            left = steps
+            while left > 0:
+                if left >= 2 and not self._sort_due(1) and not self._sort_due(2):
+                    g = self.graphs.get(self.cur)
+                    if g is None:
+                        g = self.capture()
+                    with torch.cuda.stream(self.stream):
+                        g.replay()
+                    self.step_index += 2
+                    left -= 2
+                else:
+                    self.step()
+                    left -= 1
+        finally:
+            self.check_every = check
         caller.wait_stream(self.stream)
         if self.check_every:
             self.sync()
