@@ -179,6 +179,13 @@ int pb_smooth_density(const double *rho, double *out, int64_t nc, int passes,
 int pb_solve_poisson(const double *rho, double *phi, int64_t nc, double dx,
                      double eps0, int field_bc, double phi_left,
                      double phi_right, void *scratch, void *stream);
+/* Same solve in parallel: the closed-form pivots turn both Thomas sweeps
+ * into prefix sums (double-double accumulation); ~1e-15 relative to the
+ * serial elimination, O(nc/1024) depth.  Used for large field grids. */
+int pb_solve_poisson_scan(const double *rho, double *phi, int64_t nc,
+                          double dx, double eps0, int field_bc,
+                          double phi_left, double phi_right, void *scratch,
+                          void *stream);
 int pb_compute_efield(const double *phi, double *e, int64_t nc, double dx,
                       int field_bc, void *stream);
 

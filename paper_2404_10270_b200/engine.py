@@ -113,6 +113,9 @@ class Engine:
         self.bc = _lib.PB_BC_ABSORBING if self.absorbing else _lib.PB_BC_PERIODIC
         self.b_field = getattr(config, "b_field_t", None)
         self.sort_every = int(getattr(config, "sort_every", 0) or 0)
+        method = getattr(config, "poisson", "auto")
+        # exact: the reference's serial elimination, bitwise; scan: parallel.
+        self.poisson = method if method != "auto" else ("exact" if self.nc <= 8192 else "scan")
         self.check_every = int(check_every)
         self.partition = Partition(world, self.nc, partition_cells(self.nc, world))
         self.cell_lo, self.cell_hi = self.partition.ranges[rank]
@@ -250,9 +253,10 @@ class Engine:
                 _lib.check(self.lib.pb_smooth_density(rho.data_ptr(), self.rho_s.data_ptr(), self.nc,
                                                       int(cfg.smoothing_passes), scr, sh), "pb_smooth_density")
                 src = self.rho_s
-            _lib.check(self.lib.pb_solve_poisson(src.data_ptr(), self.phi.data_ptr(), self.nc, self.grid.dx_m,
-                                                 cfg.consts.epsilon0, self.field_bc, cfg.phi_left,
-                                                 cfg.phi_right, scr, sh), "pb_solve_poisson")
+            solve = self.lib.pb_solve_poisson_scan if self.poisson == "scan" else self.lib.pb_solve_poisson
+            _lib.check(solve(src.data_ptr(), self.phi.data_ptr(), self.nc, self.grid.dx_m,
+                             cfg.consts.epsilon0, self.field_bc, cfg.phi_left,
+                             cfg.phi_right, scr, sh), "poisson")
             _lib.check(self.lib.pb_compute_efield(self.phi.data_ptr(), self.e.data_ptr(), self.nc,
                                                   self.grid.dx_m, self.field_bc, sh), "pb_compute_efield")
         return self.e
