@@ -199,6 +199,75 @@ int pb_stream_sol(const pb_species *sp, int nsp, void *stream);
 int pb_init_species(pb_species *sp, uint64_t species_key, int64_t cell_lo,
                     int64_t cell_hi, int64_t ppc0, double vstd, void *stream);
 
+/* ---- canonical slot order + collisions -------------
+ * In canonical mode every species is a flat SoA in the reference's exact
+ * cell-major slot order (the live slots of CellSortedStore concatenated over
+ * cells, pkg/src/picmc/core.py:100-181) with per-cell offs[nc+1] and
+ * counts[nc] (int64).  The slot order is what the reference's collision
+ * streams are indexed by (pkg/src/picmc/collisions.py:195-219). */
+
+/* Build offs/counts of a cell-sorted species (load time).  Returns
+ * PB_ERR_CONTRACT if `cell` is not in cell-major order.  Synchronises the
+ * stream.  `scratch` needs pb_layout_scratch_bytes(nc) bytes. */
+size_t pb_layout_scratch_bytes(int64_t nc);
+int pb_cell_layout(const int32_t *cell, int64_t n, int64_t nc, int64_t *offs,
+                   int64_t *counts, void *scratch, size_t scratch_bytes,
+                   void *stream);
+
+typedef struct pb_collide_params {
+  uint64_t step_key;      /* stream(seed, STREAM_COLLIDE, step), collisions.py:92-93 */
+  int64_t global_offset;  /* global index of local cell 0 (collide_block)   */
+  double w_over_dx;       /* neutral macro weight / dx (collisions.py:239)  */
+  double dt;              /* consts.dt_s                                    */
+  double rate_elastic, rate_excitation, rate_ionization; /* m^3/s          */
+  double threshold_j;     /* excitation_threshold_ev * ELEMENTARY_CHARGE    */
+  double mass_e;          /* electron mass_kg                               */
+  double dx_over_dt;      /* grid.dx_m / consts.dt_s                        */
+} pb_collide_params;
+
+/* collision_phase (pkg/src/picmc/collisions.py:310-351) over all cells:
+ * elastic / excitation / ionization with the reference splitmix64 streams,
+ * the dt-halving guard, and swap_remove of the ionized neutral
+ * (core.py:205-218): n_counts is updated to the live neutral count, the
+ * vacated neutral slots get cell = -1.  Newborn pairs (ion, electron) are
+ * appended at e->n + t and ion->n + t with cell set, newborn_k[t] = event
+ * index within the cell, newborn_per_cell[j] = pairs born in cell j.
+ * counters (device u64[6]): elastic, excitation, ionization, suppressed,
+ * newborns, overflow (must be zeroed by the caller). */
+int pb_collide(const pb_species *e, const pb_species *neutral,
+               const pb_species *ion, const int64_t *e_offs,
+               const int64_t *e_counts, const int64_t *n_offs,
+               int64_t *n_counts, int64_t nc, const pb_collide_params *params,
+               int64_t *newborn_per_cell, int32_t *newborn_k,
+               int64_t newborn_cap, uint64_t *counters, void *stream);
+
+typedef struct pb_canon {
+  int64_t n_old;      /* slots [0, n_old): pre-step store (cell -1 = vacated) */
+  int64_t n_tail;     /* slots [n_old, n_old+n_tail): newborns               */
+  int64_t *offs;      /* in: slot offsets of the pre-step store; out: new   */
+  int64_t *counts;    /* in: live counts after removals; out: new counts    */
+  const int64_t *newborn_per_cell; /* nc, or NULL when n_tail == 0          */
+  const int32_t *newborn_k;        /* n_tail, or NULL                        */
+} pb_canon;
+
+/* One mover step of one species in canonical order: reference push
+ * (kick/drift, Boris, yp) + resort_collect transfer + commit order
+ * (survivors in slot order, then newborns, then incomers by (src_cell,
+ * src_slot); pkg/src/picmc/mover.py:113-195, collisions.py:286-289), written
+ * into `dst` (ping-pong buffers).  New live count = offs[nc]. */
+size_t pb_canonical_scratch_bytes(int64_t n_cap, int64_t nc);
+int pb_canonical_resort(const pb_species *src, const pb_species *dst,
+                        const pb_canon *cv, const double *e_nodes, int64_t nc,
+                        int particle_bc, int species_id, pb_status *status,
+                        void *scratch, size_t scratch_bytes, void *stream);
+
+/* Weighted partials + stitched rho from fp64 per-species partials
+ * raw[ndep][2][nc] (L then R, as pb_deposit_partials produces them):
+ * bitwise deposit_partials_range + stitch_rho (fields.py:55-92). */
+int pb_rho_from_partials(const double *raw, const double *coef, int ndep,
+                         int64_t nc, int field_bc, double *left,
+                         double *right, double *rho, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

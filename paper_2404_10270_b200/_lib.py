@@ -61,6 +61,22 @@ class PbStatus(ctypes.Structure):
     ]
 
 
+class PbCollideParams(ctypes.Structure):
+    _fields_ = [
+        ("step_key", ctypes.c_uint64), ("global_offset", _i64), ("w_over_dx", _f64),
+        ("dt", _f64), ("rate_elastic", _f64), ("rate_excitation", _f64),
+        ("rate_ionization", _f64), ("threshold_j", _f64), ("mass_e", _f64),
+        ("dx_over_dt", _f64),
+    ]
+
+
+class PbCanon(ctypes.Structure):
+    _fields_ = [
+        ("n_old", _i64), ("n_tail", _i64), ("offs", _p), ("counts", _p),
+        ("newborn_per_cell", _p), ("newborn_k", _p),
+    ]
+
+
 STATUS_BYTES = ctypes.sizeof(PbStatus)
 
 # name -> (restype, argtypes); mirrors include/picmc_b200.h one to one.
@@ -96,6 +112,17 @@ _SIGS = {
     "pb_stream_sol": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int, _p]),
     "pb_init_species": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_uint64,
                                        _i64, _i64, _i64, _f64, _p]),
+    "pb_layout_scratch_bytes": (ctypes.c_size_t, [_i64]),
+    "pb_cell_layout": (ctypes.c_int, [_p, _i64, _i64, _p, _p, _p, ctypes.c_size_t, _p]),
+    "pb_collide": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.POINTER(PbSpecies),
+                                  ctypes.POINTER(PbSpecies), _p, _p, _p, _p, _i64,
+                                  ctypes.POINTER(PbCollideParams), _p, _p, _i64, _p, _p]),
+    "pb_canonical_scratch_bytes": (ctypes.c_size_t, [_i64, _i64]),
+    "pb_canonical_resort": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.POINTER(PbSpecies),
+                                           ctypes.POINTER(PbCanon), _p, _i64, ctypes.c_int,
+                                           ctypes.c_int, _p, _p, ctypes.c_size_t, _p]),
+    "pb_rho_from_partials": (ctypes.c_int, [_p, ctypes.POINTER(_f64), ctypes.c_int, _i64,
+                                            ctypes.c_int, _p, _p, _p, _p]),
 }
 
 _lock = threading.Lock()

@@ -1,0 +1,242 @@
+"""Canonical-order engine: the reference's exact slot order on the GPU, with
+Monte Carlo collisions.
+
+The production `Engine` lets particles sit in any order and deposits with
+order-independent fixed-point sums; that is the fast path and the bench.
+`CanonicalEngine` instead keeps every species in the reference
+CellSortedStore's live slot order (pkg/src/picmc/core.py:100-181) after every
+step.  That order is what the reference's collision streams are indexed by
+(pkg/src/picmc/collisions.py:195-219) and what its sequential per-cell
+deposit sums over (pkg/src/picmc/backends/_kernels.pyx:14-34), so a run here
+reproduces `picmc.run_simulation` bit for bit -- particle stores in slot
+order, rho, E, diagnostics and collision tallies -- with collisions on.
+
+Per step, on the engine stream (harness.py:144-242 order):
+  deposit   pb_deposit_partials per charged species (sequential, bitwise)
+            + pb_rho_from_partials (weights in species order + stitch)
+  field     smooth / Poisson / E as in Engine
+  collide   pb_collide: one warp per cell, splitmix64 streams, dt guard,
+            swap_remove of ionized neutrals, newborns appended to the tails
+  move      pb_canonical_resort per species: push + transfer, radix sort on
+            (dest cell, moved, canonical rank), gather into ping-pong buffers
+One host sync per step reads the newborn count and the new live counts.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import ELEMENTARY_CHARGE, macro_weight
+from .engine import Engine
+from .errors import ConfigError, EngineError
+from .rng import STREAM_COLLIDE, stream
+
+_CTR_ELASTIC, _CTR_EXCITATION, _CTR_IONIZATION, _CTR_SUPPRESSED, _CTR_NEWBORN, _CTR_OVERFLOW = range(6)
+
+
+def collide_step_key(seed: int, step: int) -> int:
+    """step_stream_key (pkg/src/picmc/collisions.py:92-93)."""
+    return stream(seed, STREAM_COLLIDE, step)
+
+
+class CanonicalEngine(Engine):
+    """Single-GPU engine in the reference's canonical slot order."""
+
+    supports_collisions = True
+
+    def __init__(self, config, device=None, *, rank: int = 0, world: int = 1, group=None,
+                 init: str = "host", check_every: int = 1):
+        if world != 1:
+            raise ConfigError("the canonical-order engine runs on one GPU "
+                              "(collisions need every particle of a cell on one rank)")
+        self.roles = None
+        c = config.collisions
+        if c is not None and c.enabled:
+            self.roles = (config.species_index(c.electron), config.species_index(c.neutral),
+                          config.species_index(c.ion))
+        self._nloc = config.grid.nc * int(config.ppc0)
+        super().__init__(config, device, rank=0, world=1, group=group, init=init,
+                         check_every=check_every)
+        nc = self.nc
+        dev = self.device
+        with torch.cuda.stream(self.stream):
+            self.raw = torch.zeros(max(self.ndep, 1) * 2 * nc, dtype=torch.float64, device=dev)
+            self.counters = torch.zeros(6, dtype=torch.int64, device=dev)
+            self.nb_per_cell = torch.zeros(nc, dtype=torch.int64, device=dev)
+            ncap = self.sp[self.roles[1]].cap if self.roles else 1
+            self.nb_k = torch.zeros(max(ncap, 1), dtype=torch.int32, device=dev)
+            cap = max(s.cap for s in self.sp)
+            self.canon_scratch = torch.empty(self.lib.pb_canonical_scratch_bytes(cap, nc),
+                                             dtype=torch.uint8, device=dev)
+        self.tally_last = (0, 0, 0, 0)
+        self.tally_total = np.zeros(4, dtype=np.int64)
+        if self.roles:
+            e, n, _ = self.roles
+            rates = c.rates
+            p = _lib.PbCollideParams()
+            p.global_offset = 0
+            p.w_over_dx = macro_weight(config, n) / self.grid.dx_m
+            p.dt = config.consts.dt_s
+            p.rate_elastic = rates.rate_elastic_m3s
+            p.rate_excitation = rates.rate_excitation_m3s
+            p.rate_ionization = rates.rate_ionization_m3s
+            p.threshold_j = rates.excitation_threshold_ev * ELEMENTARY_CHARGE
+            p.mass_e = config.species[e].mass_kg
+            p.dx_over_dt = self.grid.dx_m / config.consts.dt_s
+            self.cparams = p
+
+    # -- layout ---------------------------------------------------------------
+    def _species_cap(self, isp: int, nloc: int) -> int:
+        # Every ionization consumes a neutral, so the electron and ion stores
+        # never outgrow n + (initial neutrals): no reallocation mid-run.
+        if self.roles and isp in (self.roles[0], self.roles[2]):
+            return nloc + self._nloc
+        return nloc
+
+    def deposit_current(self):
+        """(Re)build per-cell offs/counts of the loaded, cell-sorted store."""
+        nc = self.nc
+        if not hasattr(self, "layout_scratch"):
+            self.layout_scratch = torch.empty(self.lib.pb_layout_scratch_bytes(nc), dtype=torch.uint8,
+                                              device=self.device)
+            self.offs = [torch.zeros(nc + 1, dtype=torch.int64, device=self.device) for _ in self.sp]
+            self.counts = [torch.zeros(nc, dtype=torch.int64, device=self.device) for _ in self.sp]
+        for k, s in enumerate(self.sp):
+            _lib.check(self.lib.pb_cell_layout(s.cell.data_ptr(), s.n, nc, self.offs[k].data_ptr(),
+                                               self.counts[k].data_ptr(), self.layout_scratch.data_ptr(),
+                                               self.layout_scratch.numel(), self._sh()), "pb_cell_layout")
+
+    # -- step phases ----------------------------------------------------------
+    def density(self) -> torch.Tensor:
+        """deposit_partials_range + stitch (fields.py:55-92), bitwise."""
+        nc = self.nc
+        sh = self._sh()
+        with torch.cuda.stream(self.stream):
+            for k, s in enumerate(self.sp):
+                if s.deposit < 0:
+                    continue
+                base = self.raw.data_ptr() + s.deposit * 2 * nc * 8
+                _lib.check(self.lib.pb_deposit_partials(s.arr["x"].data_ptr(), self.offs[k].data_ptr(),
+                                                        self.counts[k].data_ptr(), nc, base, base + nc * 8,
+                                                        sh), "pb_deposit_partials")
+            _lib.check(self.lib.pb_rho_from_partials(self.raw.data_ptr(), self._coef_c, self.ndep, nc,
+                                                     self.field_bc, self.left.data_ptr(),
+                                                     self.right.data_ptr(), self.rho.data_ptr(), sh),
+                       "pb_rho_from_partials")
+        return self.rho
+
+    def collide(self, step: int) -> int:
+        """collision_phase (collisions.py:310-351); returns newborn pairs."""
+        if not self.roles:
+            return 0
+        e, n, i = self.roles
+        se, sn, si = self.sp[e], self.sp[n], self.sp[i]
+        self.cparams.step_key = collide_step_key(self.cfg.seed, step)
+        cap = min(se.cap - se.n, si.cap - si.n)
+        with torch.cuda.stream(self.stream):
+            self.counters.zero_()
+            pe, pn, pi = se.pb(), sn.pb(), si.pb()
+            _lib.check(self.lib.pb_collide(
+                ctypes.byref(pe), ctypes.byref(pn), ctypes.byref(pi),
+                self.offs[e].data_ptr(), self.counts[e].data_ptr(), self.offs[n].data_ptr(),
+                self.counts[n].data_ptr(), self.nc, ctypes.byref(self.cparams),
+                self.nb_per_cell.data_ptr(), self.nb_k.data_ptr(), cap, self.counters.data_ptr(),
+                self._sh()), "pb_collide")
+        self.stream.synchronize()
+        ctr = self.counters.cpu().numpy()
+        if ctr[_CTR_OVERFLOW]:
+            raise EngineError(f"collision pass overflow ({int(ctr[_CTR_OVERFLOW])} events): newborn "
+                              "capacity or dt-guard depth exceeded")
+        self.tally_last = tuple(int(v) for v in ctr[:4])
+        self.tally_total += ctr[:4]
+        return int(ctr[_CTR_NEWBORN])
+
+    def push(self, e: torch.Tensor = None, newborns: int = 0):
+        """Push + transfer + canonical resort of every species."""
+        if e is None:
+            e = self.e
+        roles = self.roles or (-1, -1, -1)
+        with torch.cuda.stream(self.stream):
+            for k, s in enumerate(self.sp):
+                tail = newborns if k in (roles[0], roles[2]) else 0
+                cv = _lib.PbCanon()
+                cv.n_old = s.n
+                cv.n_tail = tail
+                cv.offs = self.offs[k].data_ptr()
+                cv.counts = self.counts[k].data_ptr()
+                cv.newborn_per_cell = self.nb_per_cell.data_ptr() if tail else None
+                cv.newborn_k = self.nb_k.data_ptr() if tail else None
+                dst = s.spare()
+                a, b = s.pb(s.n + tail), dst.pb(s.n + tail)
+                _lib.check(self.lib.pb_canonical_resort(
+                    ctypes.byref(a), ctypes.byref(b), ctypes.byref(cv), e.data_ptr(), self.nc, self.bc, k,
+                    self.status.data_ptr(), self.canon_scratch.data_ptr(), self.canon_scratch.numel(),
+                    self._sh()), "pb_canonical_resort")
+                s.swap_with_spare()
+            news = torch.stack([o[self.nc] for o in self.offs]).cpu()
+        for s, nn in zip(self.sp, news.tolist()):
+            s.n = int(nn)
+            if s.absorbing:
+                s.n_dev.fill_(s.n)
+        self._arr = None
+
+    def resort(self):
+        pass  # the canonical resort is part of push()
+
+    def step(self, timed: bool = False):
+        caller = torch.cuda.current_stream(self.device)
+        self.stream.wait_stream(caller)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if timed else None
+        mark = (lambda k: ev[k].record(self.stream)) if timed else (lambda k: None)
+        mark(0)
+        rho = self.density()
+        mark(1)
+        e = self.field(rho)
+        if self.cfg.field_solve and self.cfg.smoothing_passes > 0:
+            rho = self.rho_s
+        mark(2)
+        newborns = self.collide(self.step_index + 1)
+        mark(3)
+        self.push(e, newborns)
+        mark(4)
+        if timed:
+            self.phase_events.append(ev)
+        self.step_index += 1
+        caller.wait_stream(self.stream)
+        if self.check_every and self.step_index % self.check_every == 0:
+            self.sync()
+        return rho, e
+
+    def phase_seconds(self) -> dict:
+        """deposit / solve (smooth + Poisson + E) / collide / mover (push +
+        canonical resort) from CUDA events on the engine stream."""
+        self.stream.synchronize()
+        out = {k: 0.0 for k in ("deposit", "smooth", "solve", "gather", "collide", "mover",
+                                "resort", "migrate")}
+        for ev in self.phase_events:
+            out["deposit"] += ev[0].elapsed_time(ev[1]) * 1e-3
+            out["solve"] += ev[1].elapsed_time(ev[2]) * 1e-3
+            out["collide"] += ev[2].elapsed_time(ev[3]) * 1e-3
+            out["mover"] += ev[3].elapsed_time(ev[4]) * 1e-3
+        return out
+
+    def mover_ms(self) -> list:
+        self.stream.synchronize()
+        return [ev[3].elapsed_time(ev[4]) for ev in self.phase_events]
+
+    def capture(self):
+        raise EngineError("the canonical-order engine syncs every step; it is not graph-captured")
+
+    def replay(self, steps: int = 1):
+        for _ in range(steps):
+            self.step()
+
+    def totals(self) -> list:
+        return [s.n for s in self.sp]
+
+    def sync(self):
+        super().sync()
+        if self.absorbing:
+            self.last_live = [s.n for s in self.sp]

@@ -9,29 +9,9 @@
 // splitmix64 is integer arithmetic (pkg/src/picmc/rng.py:56-116), so x is
 // bit-exact; log/sin/cos are CUDA's (a few ulp from NumPy's).
 #include "common.cuh"
+#include "rng.cuh"
 
 namespace pb {
-
-constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
-
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  return z ^ (z >> 31);
-}
-
-__device__ __forceinline__ uint64_t derive(uint64_t key, uint64_t n) {
-  return mix64(key + (n + 1) * kGolden);
-}
-
-__device__ __forceinline__ double uniform(uint64_t key, uint64_t c) {
-  return __dmul_rn((double)(derive(key, c) >> 11), 0x1p-53);
-}
-
-__device__ __forceinline__ double uniform_open(uint64_t key, uint64_t c) {
-  return __dmul_rn(__dadd_rn((double)(derive(key, c) >> 11), 0.5),
-                   0x1p-53);
-}
 
 __global__ void k_init(pb_species s, uint64_t skey, int64_t cell_lo,
                        int64_t ncells, int64_t ppc0, double vstd) {

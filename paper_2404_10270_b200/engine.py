@@ -91,13 +91,15 @@ def species_kind(sp, b_field) -> int:
 class Engine:
     """One GPU's share of a run: its particle shard plus a grid replica."""
 
+    supports_collisions = False  # CanonicalEngine (canonical.py) runs them
+
     def __init__(self, config, device=None, *, rank: int = 0, world: int = 1,
                  group=None, init: str = "host", check_every: int = 1):
         config.validate()
-        if config.collisions is not None and config.collisions.enabled:
+        if config.collisions is not None and config.collisions.enabled and not self.supports_collisions:
             raise ConfigError(
-                "collisions are not on the device hot path (SURVEY.md 8f); "
-                "disable [collisions] for the B200 engine"
+                "collisions need the canonical slot order: run them through "
+                "CanonicalEngine / run_simulation (SURVEY.md 8f)"
             )
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 engine needs a CUDA device; there is no CPU fallback")
@@ -137,7 +139,8 @@ class Engine:
             boris = boris_coefficients(spd, config.consts, self.b_field) if kind == _lib.PB_KIND_BORIS else None
             with torch.cuda.stream(self.stream):
                 self.sp.append(DeviceSpecies(spd, nloc, self.device, kind=kind, deposit=dep,
-                                             kick_coef=kick, boris=boris, absorbing=self.absorbing))
+                                             kick_coef=kick, boris=boris, absorbing=self.absorbing,
+                                             cap=self._species_cap(isp, nloc)))
         self.ndep = ndep
         self._coef_c = (ctypes.c_double * max(ndep, 1))(*self.coef_dep)
         nc = self.nc
@@ -176,6 +179,9 @@ class Engine:
         self._load(init)
 
     # -- setup ------------------------------------------------------------------
+    def _species_cap(self, isp: int, nloc: int) -> int:
+        return nloc
+
     def _load(self, init: str):
         cfg = self.cfg
         with torch.cuda.stream(self.stream):

@@ -14,6 +14,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
+from .canonical import CanonicalEngine
 from .engine import PHASE_KEYS, Engine
 
 BACKEND = "cuda"
@@ -97,28 +98,34 @@ def _global_totals(engine):
 def run_simulation(config, on_step=None, *, rank=0, world=1, group=None,
                    device=None, init="host") -> RunMetrics:
     """Execute n_steps of the cycle on the GPU; returns timers and diagnostics."""
-    engine = Engine(config, device=device, rank=rank, world=world, group=group, init=init)
+    canonical = config.canonical() if hasattr(config, "canonical") else False
+    cls = CanonicalEngine if canonical else Engine
+    engine = cls(config, device=device, rank=rank, world=world, group=group, init=init)
     names = [sp.name for sp in config.species]
     zero = CollisionTally()
     diagnostics = [_diag_row(0, names, _global_totals(engine), zero)]
+    tally_sum = CollisionTally()
     t0 = time.perf_counter()
     for step in range(1, config.n_steps + 1):
         rho, e = engine.step(timed=True)
-        diagnostics.append(_diag_row(step, names, _global_totals(engine), CollisionTally()))
+        tally = CollisionTally(*engine.tally_last) if canonical else CollisionTally()
+        tally_sum.merge(tally)
+        diagnostics.append(_diag_row(step, names, _global_totals(engine), tally))
         if on_step is not None:
             on_step(step, {
                 "rho": rho.cpu().numpy().copy(),
                 "e_field": e.cpu().numpy().copy(),
                 "stores": _LazyStores(engine),
                 "partition": engine.partition,
-                "tally": CollisionTally(),
+                "tally": tally,
             })
     engine.sync()
     phase = engine.phase_seconds()
     phase["total"] = time.perf_counter() - t0 if config.n_steps > 0 else 0.0
     metrics = RunMetrics(
         phase_seconds=phase, diagnostics=diagnostics, config_hash=config.config_hash(),
-        worker_count=world, layout="flat_soa", backend=BACKEND, tally=CollisionTally(),
+        worker_count=world, layout="canonical_soa" if canonical else "flat_soa", backend=BACKEND,
+        tally=tally_sum,
         absorbed={n: engine.absorbed[k].tolist() for k, n in enumerate(names)},
     )
     if config.out_dir is not None and rank == 0:

@@ -27,7 +27,7 @@ class DeviceSpecies:
     FIELDS = ("x", "vx", "vy", "vz")
 
     def __init__(self, sp, n: int, device, *, kind: int, deposit: int,
-                 kick_coef: float = 0.0, boris=None, absorbing: bool = False):
+                 kick_coef: float = 0.0, boris=None, absorbing: bool = False, cap: int = None):
         self.sp = sp
         self.name = sp.name
         self.device = device
@@ -39,7 +39,9 @@ class DeviceSpecies:
         self.boris = boris  # (t[3], s[3]) or None
         self.absorbing = absorbing
         self.has_yp = bool(sp.track_transverse)
-        alloc = max(self.n, 1)
+        # cap > n leaves room for collision newborns (canonical mode).
+        self.cap = max(int(cap) if cap is not None else self.n, self.n)
+        alloc = max(self.cap, 1)
         self.arr = {f: torch.empty(alloc, dtype=F64, device=device) for f in self.FIELDS}
         if self.has_yp:
             self.arr["yp"] = torch.empty(alloc, dtype=F64, device=device)

@@ -254,6 +254,150 @@ def gen_mover_multistep(picmc):
     np.savez_compressed(os.path.join(HERE, "mover_multistep.npz"), **out)
 
 
+def gen_collision_runs(picmc):
+    """run_simulation with Monte Carlo collisions: the
+    final stores in slot order, per-step rho and tallies.  Rates are boosted
+    over the desk values so every event kind fires; "guard" makes the summed
+    probability exceed 0.1 so the dt-halving substeps run."""
+    from conftest import table_collisions
+    from picmc.decomposition import merge_stores
+    from picmc.harness import run_simulation
+
+    runs = {
+        "run_collide_periodic": (dict(nc=32, ppc0=16, n_steps=25),
+                                 dict(rate_elastic=5e-10, rate_excitation=5e-11,
+                                      rate_ionization=5e-10, threshold_ev=10.2)),
+        "run_collide_guard": (dict(nc=24, ppc0=12, n_steps=15, field_solve=True, smoothing_passes=1),
+                              dict(rate_elastic=1.5e-9, rate_excitation=4e-10,
+                                   rate_ionization=1.5e-9, threshold_ev=30.0)),
+        "run_collide_desk": (dict(nc=40, ppc0=10, n_steps=30),
+                             dict()),
+    }
+    for name, (kw, rk) in runs.items():
+        cfg = small_config(collisions=table_collisions(**rk), **kw)
+        hist = {"rho": [], "e": []}
+        box = {}
+
+        def probe(step, st, hist=hist, box=box):
+            hist["rho"].append(st["rho"].copy())
+            hist["e"].append(st["e_field"].copy())
+            box["stores"], box["partition"] = st["stores"], st["partition"]
+            if step == 1:
+                box["first"] = flatten_store(merge_stores(st["stores"], st["partition"], cfg.grid))
+
+        m = run_simulation(cfg, on_step=probe)
+        final = merge_stores(box["stores"], box["partition"], cfg.grid)
+        out = flatten_store(final)
+        out.update({f"step1_{k}": v for k, v in box["first"].items()})
+        out["rho"] = np.array(hist["rho"])
+        out["e_field"] = np.array(hist["e"])
+        out["totals"] = np.array([[r[f"total_{s.name}"] for s in cfg.species] for r in m.diagnostics])
+        out["tallies"] = np.array([[r["elastic"], r["excitation"], r["ionization"], r["suppressed"]]
+                                   for r in m.diagnostics])
+        out["config"] = np.array(config_record(cfg))
+        c = cfg.collisions
+        out["collisions"] = np.array(json.dumps({
+            "electron": c.electron, "neutral": c.neutral, "ion": c.ion,
+            "rates": [c.rates.rate_elastic_m3s, c.rates.rate_excitation_m3s,
+                      c.rates.rate_ionization_m3s, c.rates.excitation_threshold_ev]}))
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+        print(name, m.tally)
+
+
+def gen_collision_kats(picmc):
+    """collision_phase on the reference test stores
+    (pkg/tests/test_collisions.py:45-66): suppression, the dt guard, mixed
+    events, heavy ionization.  Records the store before and after (slot
+    order) and the tally."""
+    from test_collisions import CONSTS, ROLES, _rate_for, _store
+    from picmc.collisions import CollisionRates, collision_phase, step_stream_key
+
+    cases = {
+        "suppressed": (dict(nc=2, ne=400, nn=2, seed=15), {2: 40.0},
+                       CollisionRates(rate_ionization_m3s=_rate_for(0.08, 80.0)), (5, 0)),
+        "guard": (dict(nc=2, ne=2000, nn=50, seed=17), {},
+                  CollisionRates(rate_elastic_m3s=_rate_for(0.5, 50.0)), (7, 0)),
+        "mixed": (dict(seed=18, ne=250, nn=40), {},
+                  CollisionRates(rate_elastic_m3s=_rate_for(0.02, 40.0),
+                                 rate_excitation_m3s=_rate_for(0.01, 40.0),
+                                 rate_ionization_m3s=_rate_for(0.03, 40.0),
+                                 excitation_threshold_ev=10.2), (8, 3)),
+        "ionize": (dict(seed=16, ne=300, nn=50), {},
+                   CollisionRates(rate_ionization_m3s=_rate_for(0.05, 50.0)), (6, 0)),
+        "guard_ionize": (dict(nc=3, ne=600, nn=60, seed=19), {},
+                         CollisionRates(rate_elastic_m3s=_rate_for(0.2, 60.0),
+                                        rate_excitation_m3s=_rate_for(0.1, 60.0),
+                                        rate_ionization_m3s=_rate_for(0.3, 60.0),
+                                        excitation_threshold_ev=10.2), (9, 2)),
+    }
+    out = {}
+    for name, (kw, weights, rates, (seed, step)) in cases.items():
+        store = _store(**kw)
+        for isp, w in weights.items():
+            store.weights[isp] = w
+        before = flatten_store(store)
+        tally = collision_phase(store, rates, CONSTS, ROLES, step_stream_key(seed, step))
+        after = flatten_store(store)
+        out.update({f"{name}_in_{k}": v for k, v in before.items()})
+        out.update({f"{name}_out_{k}": v for k, v in after.items()})
+        out[f"{name}_nc"] = np.array(store.grid.nc)
+        out[f"{name}_weights"] = np.array(store.weights)
+        out[f"{name}_rates"] = np.array([rates.rate_elastic_m3s, rates.rate_excitation_m3s,
+                                         rates.rate_ionization_m3s, rates.excitation_threshold_ev])
+        out[f"{name}_key"] = np.array(step_stream_key(seed, step), dtype=np.uint64)
+        out[f"{name}_tally"] = np.array([tally.elastic, tally.excitation, tally.ionization,
+                                         tally.suppressed])
+        out[f"{name}_masses"] = np.array([sp.mass_kg for sp in store.species])
+        print(name, tally)
+    out["roles"] = np.array([ROLES.electron, ROLES.neutral, ROLES.ion])
+    out["dt_s"] = np.array(CONSTS.dt_s)
+    np.savez_compressed(os.path.join(HERE, "collision_kats.npz"), **out)
+
+
+def gen_desk_criterion01(picmc):
+    """The reference's own acceptance criterion 01 scenario
+    (pkg/tests/test_acceptance.py:73-117): pkg/configs/desk.toml run to the
+    ODE half-depletion step.  Records per-step diagnostics, the last rho and
+    SHA-256 digests of the final stores (slot order) -- compact but exact."""
+    import hashlib
+    import math
+    from dataclasses import replace
+
+    from picmc.config import load_config
+    from picmc.decomposition import merge_stores
+    from picmc.harness import run_simulation
+
+    cfg = load_config(os.path.join(REF, "configs", "desk.toml"))
+    w_over_dx = cfg.densities_m3[2] / cfg.ppc0
+    r = w_over_dx * cfg.collisions.rates.rate_ionization_m3s * cfg.consts.dt_s
+    ne, nn, steps = float(cfg.ppc0), float(cfg.ppc0), 0
+    while nn > 0.5 * cfg.ppc0:
+        ev = ne * -math.expm1(-nn * r)
+        nn -= ev
+        ne += ev
+        steps += 1
+    cfg = replace(cfg, n_steps=steps, out_dir=None)
+    box = {}
+
+    def probe(step, st):
+        if step == steps:
+            box["rho"] = st["rho"].copy()
+            box["final"] = merge_stores(st["stores"], st["partition"], cfg.grid)
+
+    m = run_simulation(cfg, on_step=probe)
+    flat = flatten_store(box["final"])
+    digests = {k: hashlib.sha256(np.ascontiguousarray(v).tobytes()).hexdigest() for k, v in flat.items()}
+    names = [s.name for s in cfg.species]
+    np.savez_compressed(
+        os.path.join(HERE, "run_desk_criterion01.npz"),
+        steps=np.array(steps), ode_nn=np.array(nn),
+        totals=np.array([[row[f"total_{n}"] for n in names] for row in m.diagnostics]),
+        tallies=np.array([[row["elastic"], row["excitation"], row["ionization"], row["suppressed"]]
+                          for row in m.diagnostics]),
+        rho_last=box["rho"], digests=np.array(json.dumps(digests, sort_keys=True)))
+    print("desk criterion 01:", steps, "steps", m.diagnostics[-1])
+
+
 if __name__ == "__main__":
     ref = import_reference()
     gen_backend(ref)
@@ -263,6 +407,9 @@ if __name__ == "__main__":
     gen_runs(ref)
     gen_fields(ref)
     gen_mover_multistep(ref)
+    gen_collision_runs(ref)
+    gen_collision_kats(ref)
+    gen_desk_criterion01(ref)
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

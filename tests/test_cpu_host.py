@@ -55,9 +55,13 @@ def test_engine_fails_loudly_without_gpu():
     from paper_2404_10270_b200 import Engine, load_config
     from paper_2404_10270_b200 import backend
 
-    cfg = load_config(os.path.join(ROOT, "configs", "desk.toml"))
+    cfg = load_config(os.path.join(ROOT, "configs", "c2_ionization_100k.toml"))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         Engine(cfg)
+    from paper_2404_10270_b200 import CanonicalEngine
+
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        CanonicalEngine(load_config(os.path.join(ROOT, "configs", "desk.toml")))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         backend.deposit_partials(np.zeros(4), np.zeros(2, dtype=np.int64), np.zeros(2, dtype=np.int64))
 
@@ -75,14 +79,32 @@ def test_configs_load_and_validate():
     from paper_2404_10270_b200 import load_config
 
     names = sorted(f for f in os.listdir(os.path.join(ROOT, "configs")) if f.endswith(".toml"))
-    assert len(names) == 5
+    assert len(names) == 6
     cfgs = {n: load_config(os.path.join(ROOT, "configs", n)) for n in names}
+    for n in ("desk.toml", "c1_desk_ppc100.toml"):
+        assert cfgs[n].canonical() and cfgs[n].collisions.rates.rate_ionization_m3s == 2.5e-11
+    assert cfgs["c1_desk_ppc100.toml"].ppc0 == 100 and cfgs["desk.toml"].ppc0 == 10
+    assert not cfgs["c2_ionization_100k.toml"].canonical()
     c3 = cfgs["c3_sheath_absorbing.toml"]
     assert c3.particle_boundary == "absorbing" and c3.boundary == "dirichlet" and c3.sort_every == 50
     c4 = cfgs["c4_sol_boris.toml"]
     assert c4.b_field_t == (0.2, 0.0, 2.0)
     c2 = cfgs["c2_ionization_100k.toml"]
     assert c2.grid.nc * c2.ppc0 * len(c2.species) == 30_000_000
+
+
+def test_slot_order_validation():
+    from dataclasses import replace
+
+    from paper_2404_10270_b200 import ConfigError, load_config
+
+    desk = load_config(os.path.join(ROOT, "configs", "desk.toml"))
+    with pytest.raises(ConfigError, match="collisions need slot_order"):
+        replace(desk, slot_order="fast").validate()
+    with pytest.raises(ConfigError, match="slot_order must be"):
+        replace(desk, slot_order="sorted").validate()
+    assert replace(desk, collisions=None).canonical() is False
+    assert replace(desk, collisions=None, slot_order="canonical").canonical() is True
 
 
 def test_strict_loader_rejects_unknown_keys():
