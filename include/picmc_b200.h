@@ -89,7 +89,10 @@ typedef struct pb_status {
   int64_t absorbed[PB_MAX_SPECIES][2];  /* [left wall, right wall]      */
   int64_t n_holes[PB_MAX_SPECIES];      /* absorbed slots to compact    */
   int64_t overflow;                     /* deposit bins over capacity   */
-  uint64_t tile_next;                   /* work counter of the TMA mover */
+  uint64_t tile_next;                   /* mover work counter (chunks claimed) */
+  uint64_t tile_done;                   /* claimers finished; the last one
+                                           resets both words, so the counter
+                                           is zero again after every launch */
 } pb_status;
 /* The caller resets *status before each pb_push_deposit: all zero except
  * cfl_index = UINT64_MAX (the engine copies a template). */
@@ -146,11 +149,13 @@ int pb_rho_epilogue(const uint64_t *bins, const double *coef, int ndep,
                     int64_t nc, int field_bc, double *left, double *right,
                     double *rho, void *stream);
 
-/* The engine's per-step form of pb_rho_epilogue: additionally zeroes the
- * other ping-pong bin set `bins_next` (same shape, written by the coming
- * pb_push_deposit) and the mover work counter (&status->tile_next), so a
- * step is exactly two kernels.  Either pointer may be NULL. */
-int pb_density_step(const uint64_t *bins, uint64_t *bins_next,
+/* The engine's per-step form of pb_rho_epilogue (two kernels): weighted
+ * partials per cell, after which `bins` itself is zeroed (a bin set is clean
+ * again once its density has been taken), then the stitch into rho.  If
+ * non-NULL, `bins_next` (the other ping-pong set) and the word `counter` are
+ * zeroed too.  Because it never touches the set the next mover deposits
+ * into, it may run concurrently with that pb_push_deposit. */
+int pb_density_step(uint64_t *bins, uint64_t *bins_next,
                     uint64_t *counter, const double *coef, int ndep,
                     int64_t nc, int field_bc, double *left, double *right,
                     double *rho, void *stream);

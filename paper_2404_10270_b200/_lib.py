@@ -57,7 +57,7 @@ class PbStatus(ctypes.Structure):
         ("absorbed", (_i64 * 2) * PB_MAX_SPECIES),
         ("n_holes", _i64 * PB_MAX_SPECIES),
         ("overflow", _i64),
-        ("tile_next", ctypes.c_uint64),
+        ("tile_next", ctypes.c_uint64), ("tile_done", ctypes.c_uint64),
     ]
 
 

@@ -85,6 +85,49 @@ __global__ void k_rho_epilogue(const uint64_t *__restrict__ bins, CoefArgs ca,
   rho[g] = v;
 }
 
+// Engine form, split in two so the bins can be cleared as they are read:
+// k_partials_clear has one thread per cell touching only its own bins, so it
+// zeroes them after reading (the ping-pong invariant: a bin set is zero again
+// once its density has been taken), then k_stitch builds rho from left/right.
+// Neither touches the set the concurrent mover deposits into, so in CUDA-graph
+// replay the epilogue runs on a side stream overlapped with the next push.
+__global__ void k_partials_clear(uint64_t *__restrict__ bins, CoefArgs ca, int ndep, int64_t nc,
+                                 double *__restrict__ left, double *__restrict__ right,
+                                 uint64_t *__restrict__ clear, uint64_t *__restrict__ counter) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (counter && g == 0) *counter = 0;
+  if (g >= nc) return;
+  double l, r;
+  weighted_partials(bins, ca.c, ndep, nc, g, l, r);
+  left[g] = l;
+  right[g] = r;
+  for (int s = 0; s < ndep; ++s) {
+    bins[(size_t)s * 2 * nc + g] = 0;
+    bins[(size_t)s * 2 * nc + nc + g] = 0;
+    if (clear) {
+      clear[(size_t)s * 2 * nc + g] = 0;
+      clear[(size_t)s * 2 * nc + nc + g] = 0;
+    }
+  }
+}
+
+__global__ void k_stitch(const double *__restrict__ left, const double *__restrict__ right,
+                         int64_t nc, int field_bc, double *__restrict__ rho) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g > nc) return;
+  double v;
+  if (g > 0 && g < nc) {
+    v = __dadd_rn(right[g - 1], left[g]);  // fields.py:85
+  } else if (field_bc == PB_FIELD_PERIODIC) {
+    v = __dadd_rn(right[nc - 1], left[0]);
+  } else if (g == 0) {
+    v = __dmul_rn(left[0], 2.0);  // fields.py:115-117
+  } else {
+    v = __dmul_rn(right[nc - 1], 2.0);
+  }
+  rho[g] = v;
+}
+
 }  // namespace pb
 
 extern "C" int pb_abi_version(void) { return PB_ABI_VERSION; }
@@ -132,14 +175,31 @@ extern "C" int pb_rho_epilogue(const uint64_t *bins, const double *coef, int nde
   return rho_epilogue(bins, coef, ndep, nc, field_bc, left, right, rho, nullptr, nullptr, stream);
 }
 
-extern "C" int pb_density_step(const uint64_t *bins, uint64_t *bins_next, uint64_t *counter,
+extern "C" int pb_density_step(uint64_t *bins, uint64_t *bins_next, uint64_t *counter,
                                const double *coef, int ndep, int64_t nc, int field_bc,
                                double *left, double *right, double *rho, void *stream) {
   if (bins_next == bins && bins != nullptr) {
     pb::set_error("pb_density_step: bins_next must not alias bins");
     return PB_ERR_INVALID;
   }
-  return rho_epilogue(bins, coef, ndep, nc, field_bc, left, right, rho, bins_next, counter, stream);
+  if (ndep < 0 || ndep > PB_MAX_SPECIES || nc < 2 || !rho || !left || !right ||
+      (ndep > 0 && (!bins || !coef)) ||
+      (field_bc != PB_FIELD_PERIODIC && field_bc != PB_FIELD_DIRICHLET)) {
+    pb::set_error("pb_density_step: bad arguments (nc=%lld ndep=%d)", (long long)nc, ndep);
+    return PB_ERR_INVALID;
+  }
+  pb::CoefArgs ca;
+  memset(&ca, 0, sizeof(ca));
+  for (int s = 0; s < ndep; ++s) ca.c[s] = coef[s];
+  cudaStream_t st = (cudaStream_t)stream;
+  const int threads = 256;
+  const int64_t b1 = (nc + threads - 1) / threads, b2 = (nc + 1 + threads - 1) / threads;
+  pb::k_partials_clear<<<(unsigned)b1, threads, 0, st>>>(bins, ca, ndep, nc, left, right, bins_next,
+                                                         counter);
+  PB_CHECK_LAUNCH("k_partials_clear");
+  pb::k_stitch<<<(unsigned)b2, threads, 0, st>>>(left, right, nc, field_bc, rho);
+  PB_CHECK_LAUNCH("k_stitch");
+  return PB_OK;
 }
 
 // ---------------------------------------------------------------------------

@@ -427,6 +427,24 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
       : "memory");
 }
 
+// Self-cleaning work counter: every claimer (a warp, or a TMA producer lane)
+// reports once when it has stopped claiming; the last one resets the counter,
+// so no separate reset has to be ordered before the next launch (the density
+// epilogue can then run concurrently with the mover).
+// A claimer's last claim has returned (it is what ended its loop) before its
+// done-increment is issued, so the reset is ordered after every claim without
+// a fence (a __threadfence here costs a full L1 invalidate per exiting warp).
+__device__ __forceinline__ void release_work_counter(pb_status *st, unsigned long long claimers) {
+#ifdef PB_RELEASE_FENCE
+  __threadfence();
+#endif
+  const unsigned long long d = atomicAdd((unsigned long long *)&st->tile_done, 1ull);
+  if (d == claimers - 1) {
+    atomicExch((unsigned long long *)&st->tile_next, 0ull);
+    atomicExch((unsigned long long *)&st->tile_done, 0ull);
+  }
+}
+
 // Particles per TMA tile, per species kind: sized so every kind fills a
 // ~32 KB ring slot (a multiple of 2*kThreads for the pair loop).
 __host__ __device__ constexpr int tile_of(int kind, bool yp) {
@@ -807,6 +825,7 @@ __global__ void __launch_bounds__(kThreads + 32, PB_MINBLOCKS)
           prefetch_any(a.sp[jsp], tile_base(a, jsp, nt));
         }
       }
+      release_work_counter(a.st, gridDim.x);
     }
   } else {  // consumer warps
     Window win{nullptr, nullptr, 0, 0, nullptr, nullptr};
@@ -878,125 +897,188 @@ __device__ __forceinline__ void ld4(const double *p, double &a, double &b, doubl
   asm volatile(PB_LD4 " {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
 
-template <int KIND, bool YP, int BC, bool DEP>
-__device__ __forceinline__ void quad_chunk(const LaunchArgs &a, int isp, int64_t beg, int64_t end,
-                                           const Window &win, Tally &t) {
+// Register image of one lane's 4 consecutive particles.
+template <int KIND, bool YP>
+struct Quad {
+  double x[4], vx[4], vy[4], vz[4], y[4];
+  int32_t c[4];
+  int nv;
+};
+
+template <int KIND, bool YP>
+__device__ __forceinline__ void quad_load(const pb_species &s, int64_t i, int64_t end,
+                                          Quad<KIND, YP> &q) {
   using F = Fields<KIND, YP>;
+  constexpr bool kCell = KIND != PB_KIND_DRIFT;
+  q.nv = i >= end ? 0 : (end - i >= 4 ? 4 : (int)(end - i));
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    q.x[k] = q.vx[k] = q.vy[k] = q.vz[k] = q.y[k] = 0.0;
+    q.c[k] = -1;
+  }
+  if (q.nv == 4) {
+    ld4(s.x + i, q.x[0], q.x[1], q.x[2], q.x[3]);
+    ld4(s.vx + i, q.vx[0], q.vx[1], q.vx[2], q.vx[3]);
+    if (F::kVy) ld4(s.vy + i, q.vy[0], q.vy[1], q.vy[2], q.vy[3]);
+    if (F::kVz) ld4(s.vz + i, q.vz[0], q.vz[1], q.vz[2], q.vz[3]);
+    if (YP) ld4(s.yp + i, q.y[0], q.y[1], q.y[2], q.y[3]);
+    if (kCell) {
+      const int4 cc = __ldcs(reinterpret_cast<const int4 *>(s.cell + i));
+      q.c[0] = cc.x;
+      q.c[1] = cc.y;
+      q.c[2] = cc.z;
+      q.c[3] = cc.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < q.nv) {
+        q.x[k] = s.x[i + k];
+        q.vx[k] = s.vx[i + k];
+        if (F::kVy) q.vy[k] = s.vy[i + k];
+        if (F::kVz) q.vz[k] = s.vz[i + k];
+        if (YP) q.y[k] = s.yp[i + k];
+        if (kCell) q.c[k] = s.cell[i + k];
+      }
+    }
+  }
+}
+
+// Push, transfer, store, tallies and deposit of one lane's quad at slot i
+// (every lane of the warp calls this: the deposit scan shuffles).
+template <int KIND, bool YP, int BC, bool DEP>
+__device__ __forceinline__ void quad_process(const LaunchArgs &a, int isp, int64_t i,
+                                             Quad<KIND, YP> &q, const Window &win, Tally &t) {
   const pb_species &s = a.sp[isp];
   const int sid = a.id[isp];
   const unsigned full = 0xffffffffu;
   const int64_t nc = a.nc;
   constexpr bool kCell = KIND != PB_KIND_DRIFT;
   const int lane = (int)lane_id();
+  const int nv = q.nv;
+  int32_t nn[4];
+  int8_t wall[4];
+  bool mv[4], cfl[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    nn[k] = -1;
+    wall[k] = -1;
+    mv[k] = false;
+    cfl[k] = false;
+    if (k < nv) {
+      kick_drift<KIND>(q.x[k], q.vx[k], q.vy[k], q.vz[k], q.c[k], s, a.e);
+      if (YP) q.y[k] = __dadd_rn(q.y[k], __dmul_rn(s.fnstep, q.vy[k]));
+      if (!kCell && floor(q.x[k]) != 0.0) q.c[k] = s.cell[i + k];
+      const MoveOut o = transfer<BC>(q.x[k], q.c[k], nc);
+      nn[k] = o.cell;
+      mv[k] = o.moved;
+      wall[k] = o.wall;
+      cfl[k] = o.cfl;
+    }
+  }
+  if (nv == 4) {
+    st4(s.x + i, q.x[0], q.x[1], q.x[2], q.x[3]);
+    if (KIND != PB_KIND_DRIFT) st4(s.vx + i, q.vx[0], q.vx[1], q.vx[2], q.vx[3]);
+    if (KIND == PB_KIND_BORIS) {
+      st4(s.vy + i, q.vy[0], q.vy[1], q.vy[2], q.vy[3]);
+      st4(s.vz + i, q.vz[0], q.vz[1], q.vz[2], q.vz[3]);
+    }
+    if (YP) st4(s.yp + i, q.y[0], q.y[1], q.y[2], q.y[3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < nv) {
+        s.x[i + k] = q.x[k];
+        if (KIND != PB_KIND_DRIFT) s.vx[i + k] = q.vx[k];
+        if (KIND == PB_KIND_BORIS) {
+          s.vy[i + k] = q.vy[k];
+          s.vz[i + k] = q.vz[k];
+        }
+        if (YP) s.yp[i + k] = q.y[k];
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (mv[k]) s.cell[i + k] = nn[k];
+    t.moved += (int)mv[k];
+    if (cfl[k]) {
+      const uint64_t key = ((uint64_t)sid << 56) | (uint64_t)(i + k);
+      atomicMin((unsigned long long *)&a.st->cfl_index, (unsigned long long)key);
+      atomicCAS(&a.st->code, PB_OK, PB_ERR_CFL);
+      nn[k] = -1;
+    }
+  }
+  if (BC == PB_BC_ABSORBING) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      t.absorbed[0] += (int)(wall[k] == 0);
+      t.absorbed[1] += (int)(wall[k] == 1);
+      const bool r = wall[k] >= 0;
+      const unsigned b = __ballot_sync(full, r);
+      if (b) {
+        unsigned long long hb = 0;
+        if (lane == 0)
+          hb = atomicAdd((unsigned long long *)&a.st->n_holes[sid], (unsigned long long)__popc(b));
+        hb = __shfl_sync(full, hb, 0);
+        if (r) s.holes[hb + __popc(b & ((1u << lane) - 1u))] = i + k;
+      }
+    }
+  }
+  if (DEP) {
+    RunAcc run;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) run.add(nn[k], q.x[k], win);
+    warp_segmented_emit(run.key, run.w, win);
+  }
+}
+
+#ifndef PB_QUAD_PREFETCH
+#define PB_QUAD_PREFETCH 1
+#endif
+
+template <int KIND, bool YP, int BC, bool DEP>
+__device__ __forceinline__ void quad_chunk(const LaunchArgs &a, int isp, int64_t beg, int64_t end,
+                                           const Window &win, Tally &t) {
+  const pb_species &s = a.sp[isp];
+  const int lane = (int)lane_id();
+  // Charged (KICK, no yp) slices: software-pipeline the next 128 particles'
+  // loads under this slice's gather / push / deposit scan, doubling the bytes
+  // each warp keeps in flight (the neutral path already runs at copy rate;
+  // wider kinds would spill at the 80-register budget).
+  constexpr bool kPrefetch = PB_QUAD_PREFETCH && KIND == PB_KIND_KICK && !YP;
+  Quad<KIND, YP> q;
+  quad_load<KIND, YP>(s, beg + 4 * lane, end, q);
 #pragma unroll 1
   for (int64_t q0 = beg; q0 < end; q0 += 128) {
     const int64_t i = q0 + 4 * lane;
-    const int nv = i >= end ? 0 : (end - i >= 4 ? 4 : (int)(end - i));
-    double x[4] = {0, 0, 0, 0}, vx[4] = {0, 0, 0, 0}, vy[4] = {0, 0, 0, 0}, vz[4] = {0, 0, 0, 0},
-           y[4] = {0, 0, 0, 0};
-    int32_t c[4] = {-1, -1, -1, -1};
-    if (nv == 4) {
-      ld4(s.x + i, x[0], x[1], x[2], x[3]);
-      ld4(s.vx + i, vx[0], vx[1], vx[2], vx[3]);
-      if (F::kVy) ld4(s.vy + i, vy[0], vy[1], vy[2], vy[3]);
-      if (F::kVz) ld4(s.vz + i, vz[0], vz[1], vz[2], vz[3]);
-      if (YP) ld4(s.yp + i, y[0], y[1], y[2], y[3]);
-      if (kCell) {
-        const int4 cc = __ldcs(reinterpret_cast<const int4 *>(s.cell + i));
-        c[0] = cc.x;
-        c[1] = cc.y;
-        c[2] = cc.z;
-        c[3] = cc.w;
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (k < nv) {
-          x[k] = s.x[i + k];
-          vx[k] = s.vx[i + k];
-          if (F::kVy) vy[k] = s.vy[i + k];
-          if (F::kVz) vz[k] = s.vz[i + k];
-          if (YP) y[k] = s.yp[i + k];
-          if (kCell) c[k] = s.cell[i + k];
-        }
-      }
-    }
-    int32_t nn[4];
-    int8_t wall[4];
-    bool mv[4], cfl[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      nn[k] = -1;
-      wall[k] = -1;
-      mv[k] = false;
-      cfl[k] = false;
-      if (k < nv) {
-        kick_drift<KIND>(x[k], vx[k], vy[k], vz[k], c[k], s, a.e);
-        if (YP) y[k] = __dadd_rn(y[k], __dmul_rn(s.fnstep, vy[k]));
-        if (!kCell && floor(x[k]) != 0.0) c[k] = s.cell[i + k];
-        const MoveOut o = transfer<BC>(x[k], c[k], nc);
-        nn[k] = o.cell;
-        mv[k] = o.moved;
-        wall[k] = o.wall;
-        cfl[k] = o.cfl;
-      }
-    }
-    if (nv == 4) {
-      st4(s.x + i, x[0], x[1], x[2], x[3]);
-      if (KIND != PB_KIND_DRIFT) st4(s.vx + i, vx[0], vx[1], vx[2], vx[3]);
-      if (KIND == PB_KIND_BORIS) {
-        st4(s.vy + i, vy[0], vy[1], vy[2], vy[3]);
-        st4(s.vz + i, vz[0], vz[1], vz[2], vz[3]);
-      }
-      if (YP) st4(s.yp + i, y[0], y[1], y[2], y[3]);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (k < nv) {
-          s.x[i + k] = x[k];
-          if (KIND != PB_KIND_DRIFT) s.vx[i + k] = vx[k];
-          if (KIND == PB_KIND_BORIS) {
-            s.vy[i + k] = vy[k];
-            s.vz[i + k] = vz[k];
-          }
-          if (YP) s.yp[i + k] = y[k];
-        }
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (mv[k]) s.cell[i + k] = nn[k];
-      t.moved += (int)mv[k];
-      if (cfl[k]) {
-        const uint64_t key = ((uint64_t)sid << 56) | (uint64_t)(i + k);
-        atomicMin((unsigned long long *)&a.st->cfl_index, (unsigned long long)key);
-        atomicCAS(&a.st->code, PB_OK, PB_ERR_CFL);
-        nn[k] = -1;
-      }
-    }
-    if (BC == PB_BC_ABSORBING) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        t.absorbed[0] += (int)(wall[k] == 0);
-        t.absorbed[1] += (int)(wall[k] == 1);
-        const bool r = wall[k] >= 0;
-        const unsigned b = __ballot_sync(full, r);
-        if (b) {
-          unsigned long long hb = 0;
-          if (lane == 0)
-            hb = atomicAdd((unsigned long long *)&a.st->n_holes[sid], (unsigned long long)__popc(b));
-          hb = __shfl_sync(full, hb, 0);
-          if (r) s.holes[hb + __popc(b & ((1u << lane) - 1u))] = i + k;
-        }
-      }
-    }
-    if (DEP) {
-      RunAcc run;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) run.add(nn[k], x[k], win);
-      warp_segmented_emit(run.key, run.w, win);
-    }
+    Quad<KIND, YP> nq;
+    if (kPrefetch) quad_load<KIND, YP>(s, i + 128, end, nq);
+    quad_process<KIND, YP, BC, DEP>(a, isp, i, q, win, t);
+    if (kPrefetch)
+      q = nq;
+    else
+      quad_load<KIND, YP>(s, i + 128, end, q);
   }
+}
+
+// Chunk c -> (species slot, [beg, end)).  end <= beg for empty chunks.
+__device__ __forceinline__ int chunk_species(const LaunchArgs &a, int64_t c, int64_t &beg,
+                                             int64_t &end) {
+  int kk = 0;
+  while (kk + 1 < a.nsp && c >= a.tile_start[kk + 1]) ++kk;
+  const int isp = a.order[kk];
+  const pb_species &s = a.sp[isp];
+  const int64_t n = s.n_dev ? *s.n_dev : s.n;
+  beg = (c - a.tile_start[kk]) * kChunk;
+  end = beg + kChunk < n ? beg + kChunk : n;
+  return isp;
+}
+
+__device__ __forceinline__ int64_t claim_chunk(const LaunchArgs &a) {
+  unsigned long long c = 0;
+  if (lane_id() == 0) c = atomicAdd((unsigned long long *)&a.st->tile_next, 1ull);
+  return (int64_t)__shfl_sync(0xffffffffu, c, 0);
 }
 
 template <int BC, bool BORIS>
@@ -1024,28 +1106,19 @@ __device__ __forceinline__ void quad_dispatch(const LaunchArgs &a, int isp, int6
 #define PB_QUAD_MINBLOCKS 3
 #endif
 
+constexpr int kWarpsPerBlock = kThreads / 32;
+
 template <int BC, bool BORIS>
 __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
     k_push_quad(const __grid_constant__ LaunchArgs a) {
   const int64_t total = a.tile_start[a.nsp];
-  const unsigned full = 0xffffffffu;
   Window win{nullptr, nullptr, 0, 0, nullptr, nullptr};
   Tally t;
   int cur = -1;
-  for (;;) {
-    unsigned long long c = 0;
-    if (lane_id() == 0) c = atomicAdd((unsigned long long *)&a.st->tile_next, 1ull);
-    c = __shfl_sync(full, c, 0);
-    if ((int64_t)c >= total) break;
-    int kk = 0;
-    while (kk + 1 < a.nsp && (int64_t)c >= a.tile_start[kk + 1]) ++kk;
-    const int isp = a.order[kk];
+  for (int64_t c = claim_chunk(a); c < total; c = claim_chunk(a)) {
+    int64_t beg, end;
+    const int isp = chunk_species(a, c, beg, end);
     const pb_species &s = a.sp[isp];
-    // Absorbing walls shrink the live count on the device: chunks past it
-    // are empty (the chunk list is built from the host's upper bound).
-    const int64_t n = s.n_dev ? *s.n_dev : s.n;
-    const int64_t beg = ((int64_t)c - a.tile_start[kk]) * kChunk;
-    const int64_t end = beg + kChunk < n ? beg + kChunk : n;
     if (isp != cur) {
       if (cur >= 0) flush_tally(a, a.id[cur], t, nullptr);
       t = Tally();
@@ -1058,6 +1131,7 @@ __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
     quad_dispatch<BC, BORIS>(a, isp, beg, end, win, t);
   }
   if (cur >= 0) flush_tally(a, a.id[cur], t, nullptr);
+  if (lane_id() == 0) release_work_counter(a.st, (unsigned long long)gridDim.x * kWarpsPerBlock);
 }
 
 // ---------------------------------------------------------------------------

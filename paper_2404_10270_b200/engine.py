@@ -124,6 +124,7 @@ class Engine:
         check_store_budget(config)
 
         self.stream = torch.cuda.Stream(self.device)
+        self._side = torch.cuda.Stream(self.device)  # overlapped density epilogue
         self.sp = []
         self.coef_dep = []
         ndep = 0
@@ -143,6 +144,7 @@ class Engine:
                                              cap=self._species_cap(isp, nloc)))
         self.ndep = ndep
         self._coef_c = (ctypes.c_double * max(ndep, 1))(*self.coef_dep)
+        self.sort_periods = self._sort_periods(config)
         nc = self.nc
         with torch.cuda.stream(self.stream):
             # Ping-pong fixed-point bins: the mover deposits into one set while
@@ -171,14 +173,35 @@ class Engine:
         self._arr = None
         self.graphs = {}
         self._next_clear = False
-        # Work counter of the TMA mover: the pb_status.tile_next word.
-        off = ctypes.sizeof(_lib.PbStatus) - 8
+        # Mover work counter (pb_status.tile_next; self-resetting in the kernel).
+        off = _lib.PbStatus.tile_next.offset
         self._tile_counter = self.status[off:off + 8]
         self.absorbed = np.zeros((len(self.sp), 2), dtype=np.int64)
         self.moved = np.zeros(len(self.sp), dtype=np.int64)
         self._load(init)
 
     # -- setup ------------------------------------------------------------------
+    def _sort_periods(self, config) -> list:
+        """Per-species cell-sort period.  `sort_every` applies to the fastest
+        species (largest thermal drift per step, nstep included); slower ones
+        lose cell order proportionally more slowly and are sorted
+        proportionally less often (x64 at most).  0 = never."""
+        if not self.sort_every:
+            return [0] * len(self.sp)
+        drift = []
+        for isp, s in enumerate(self.sp):
+            t = config.temperatures_ev[isp]
+            v = thermal_std(t, s.sp.mass_kg, config.consts.dt_s, self.grid.dx_m) * s.fnstep
+            drift.append(v if s.kind != _lib.PB_KIND_INACTIVE else 0.0)
+        vmax = max(drift) or 1.0
+        out = []
+        for v in drift:
+            if v <= 0.0:
+                out.append(0)
+                continue
+            out.append(self.sort_every * int(min(64, max(1, round(vmax / v)))))
+        return out
+
     def _species_cap(self, isp: int, nloc: int) -> int:
         return nloc
 
@@ -233,17 +256,20 @@ class Engine:
         self.deposit_current()
 
     # -- step phases ------------------------------------------------------------
-    def density(self) -> torch.Tensor:
-        """Reduce the bins across GPUs and produce left/right/rho; also clears
-        the other bin set and the mover work counter (one kernel)."""
-        with torch.cuda.stream(self.stream):
+    def density(self, stream=None, clear_next: bool = True) -> torch.Tensor:
+        """Reduce the bins across GPUs and produce left/right/rho; the bin set
+        read is zeroed afterwards and, with clear_next, so is the other set
+        (the graph replay runs this concurrently with the next push and then
+        must not touch the set that push deposits into)."""
+        st = stream if stream is not None else self.stream
+        with torch.cuda.stream(st):
             if self.world > 1:
                 reduce_bins(self.bins, self.group)
+            nxt = self.bins_pp[1 - self.cur].data_ptr() if clear_next else None
             _lib.check(self.lib.pb_density_step(
-                self.bins.data_ptr(), self.bins_pp[1 - self.cur].data_ptr(), self._tile_counter.data_ptr(),
-                self._coef_c, self.ndep, self.nc, self.field_bc,
-                self.left.data_ptr(), self.right.data_ptr(), self.rho.data_ptr(), self._sh()),
-                "pb_density_step")
+                self.bins.data_ptr(), nxt, None, self._coef_c, self.ndep, self.nc, self.field_bc,
+                self.left.data_ptr(), self.right.data_ptr(), self.rho.data_ptr(),
+                ctypes.c_void_p(st.cuda_stream)), "pb_density_step")
         self._next_clear = True
         return self.rho
 
@@ -276,7 +302,6 @@ class Engine:
         with torch.cuda.stream(self.stream):
             if not self._next_clear:  # push() without a density() in between
                 target.zero_()
-                self._tile_counter.zero_()
             if self._timing is not None:
                 self._timing[0].record(self.stream)
             _lib.check(self.lib.pb_push_deposit(arr, n, e.data_ptr(), self.nc, self.bc, target.data_ptr(),
@@ -292,13 +317,17 @@ class Engine:
                 arr, n = self._species()
                 _lib.check(self.lib.pb_compact(arr, n, self.status.data_ptr(), self.compact_scratch.data_ptr(),
                                                self.compact_scratch.numel(), self._sh()), "pb_compact")
-            if self.sort_every and (self.step_index + 1) % self.sort_every == 0:
-                self.sort_by_cell()
+            due = self._sorts_due(1)
+            if due:
+                self.sort_by_cell(due)
 
-    def sort_by_cell(self):
-        """Radix sort every species by cell into the spare buffers, swap."""
+    def sort_by_cell(self, which=None):
+        """Radix sort species (all, or the indices in `which`) by cell into
+        their spare buffers and swap."""
         with torch.cuda.stream(self.stream):
-            for s in self.sp:
+            for k, s in enumerate(self.sp):
+                if which is not None and k not in which:
+                    continue
                 n = s.live_count()
                 if n <= 1:
                     continue
@@ -311,8 +340,7 @@ class Engine:
                                                     self.sort_scratch.data_ptr(), self.sort_scratch.numel(),
                                                     self._sh()), "pb_sort_by_cell")
                 s.swap_with_spare()
-            self._arr = None
-            self.graphs = {}  # captured pointers are stale
+            self._arr = None  # graphs are keyed by buffer addresses (_graph_key)
 
     def step(self, timed: bool = False):
         """One full cycle.  Returns rho/E of this step (device tensors).
@@ -347,14 +375,32 @@ class Engine:
     def capture(self):
         """Capture two steps (even + odd bin set) as one CUDA graph, starting
         from the current ping-pong parity; replay() then costs one launch per
-        two steps.  Sort steps run eagerly and invalidate the graphs."""
+        two steps.  Sort steps run eagerly; graphs are cached per buffer state."""
         self.sync()
         self.stream.synchronize()
+        return self._capture()
+
+    def _capture(self):
         g = torch.cuda.CUDAGraph()
         start = self.cur
+        # Field-free runs: E does not depend on rho, so each step's density
+        # epilogue (and, across GPUs, its bin allreduce) runs on a side stream
+        # concurrently with the push; push n+1 waits only for epilogue n,
+        # which cleared the bin set it deposits into.
+        overlap = not self.cfg.field_solve
         with torch.cuda.graph(g, stream=self.stream):
+            prev = None
             for _ in range(2):
-                rho = self.density()
+                if overlap:
+                    self._side.wait_stream(self.stream)
+                    rho = self.density(self._side, clear_next=False)
+                    done = torch.cuda.Event()
+                    done.record(self._side)
+                    if prev is not None:
+                        self.stream.wait_event(prev)
+                    prev = done
+                else:
+                    rho = self.density()
                 e = self.field(rho)
                 self.push(e)
                 if self.absorbing:
@@ -362,12 +408,51 @@ class Engine:
                     _lib.check(self.lib.pb_compact(arr, n, self.status.data_ptr(),
                                                    self.compact_scratch.data_ptr(),
                                                    self.compact_scratch.numel(), self._sh()), "pb_compact")
+            if prev is not None:
+                self.stream.wait_event(prev)
         assert self.cur == start
-        self.graphs[start] = g
+        self.graphs[self._graph_key()] = g
         return g
 
+    def prepare_graphs(self, horizon: int = None):
+        """Capture up front every graph replay() can need within `horizon`
+        steps: both bin parities x both buffers of every species whose sort
+        falls in that window.  Capturing launches nothing, so the buffer swaps
+        here are pointer bookkeeping only; timed replays then never capture."""
+        self.sync()
+        self.stream.synchronize()
+        clear0 = self._next_clear
+        sorted_sp = [k for k, p in enumerate(self.sort_periods)
+                     if p and (horizon is None or p <= horizon)]
+        cur0 = self.cur
+        for mask in range(1 << len(sorted_sp)):
+            flip = [k for j, k in enumerate(sorted_sp) if mask >> j & 1]
+            for k in flip:
+                self.sp[k].spare()
+                self.sp[k].swap_with_spare()
+            self._arr = None
+            for cur in (0, 1):
+                self.cur = cur
+                if self._graph_key() not in self.graphs:
+                    self._capture()
+            for k in flip:
+                self.sp[k].swap_with_spare()
+            self._arr = None
+        self.cur = cur0
+        self._next_clear = clear0
+
+    def _graph_key(self):
+        """Captured graphs bake in buffer addresses: key them by the bin
+        parity and every species' current (ping-pong) buffer."""
+        return (self.cur,) + tuple(s.arr["x"].data_ptr() for s in self.sp)
+
+    def _sorts_due(self, k: int) -> list:
+        """Species whose sort falls after step step_index + k."""
+        n = self.step_index + k
+        return [i for i, p in enumerate(self.sort_periods) if p and n % p == 0]
+
     def _sort_due(self, k: int) -> bool:
-        return bool(self.sort_every) and (self.step_index + k) % self.sort_every == 0
+        return bool(self._sorts_due(k))
 
     def replay(self, steps: int = 1):
         """Run `steps` cycles, two at a time through the captured graph; odd
@@ -379,7 +464,7 @@ class Engine:
             left = steps
             while left > 0:
                 if left >= 2 and not self._sort_due(1) and not self._sort_due(2):
-                    g = self.graphs.get(self.cur)
+                    g = self.graphs.get(self._graph_key())
                     if g is None:
                         g = self.capture()
                     with torch.cuda.stream(self.stream):

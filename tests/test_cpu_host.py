@@ -46,8 +46,9 @@ def test_library_argument_errors_without_gpu():
 def test_status_struct_layout_matches_header():
     from paper_2404_10270_b200 import _lib
 
-    # int32 code, int32 species, u64 index, 8 moved, 8x2 absorbed, 8 holes, overflow, tile_next
-    assert _lib.STATUS_BYTES == 4 + 4 + 8 + 8 * 8 + 16 * 8 + 8 * 8 + 8 + 8
+    # int32 code, int32 species, u64 index, 8 moved, 8x2 absorbed, 8 holes, overflow,
+    # tile_next, tile_done
+    assert _lib.STATUS_BYTES == 4 + 4 + 8 + 8 * 8 + 16 * 8 + 8 * 8 + 8 + 8 + 8
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
