@@ -251,29 +251,32 @@ def run_ours(args, rank, world, local_rank):
         ms, push_ms = float(t[0]), float(t[1])
     value = pushes_rank * world / (ms * 1e-3)
 
-    # e2e: the public step API driven from the host, per step: H2D of an
-    # E-field array from pinned memory, the step, D2H of rho + live totals.
+    # e2e: the public host-driven API (Engine.run_pipelined): every step copies
+    # its E-field input H2D from pinned host memory and its rho result D2H into
+    # pinned host memory, which the host reads (one step late, while the GPU
+    # runs the next step).
     nodes = nc_total + 1
     e_host = torch.zeros(nodes, dtype=torch.float64).pin_memory()
-    rho_host = torch.empty(nodes, dtype=torch.float64).pin_memory()
-    e2e_steps = max(3, min(args.steps, 200))
+    e2e_steps = max(3, min(args.steps, 400))
+    seen = []
+
+    def on_result(k, rho_host):
+        seen.append(float(rho_host[k % nodes]))
+
+    eng.run_pipelined(4, e_source=lambda k: e_host, on_result=None)  # warm the pinned ring
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(eng.stream)
-    for _ in range(e2e_steps):
-        with torch.cuda.stream(eng.stream):
-            eng.e.copy_(e_host, non_blocking=True)
-        rho, _ = eng.step()
-        with torch.cuda.stream(eng.stream):
-            rho_host.copy_(rho, non_blocking=True)
-        eng.stream.synchronize()
-        _ = float(rho_host[0])
+    w0 = time.perf_counter()
+    eng.run_pipelined(e2e_steps, e_source=lambda k: e_host, on_result=on_result)
     t1.record(eng.stream)
     torch.cuda.synchronize(dev)
-    e2e_ms = t0.elapsed_time(t1) / e2e_steps
+    wall_ms = (time.perf_counter() - w0) * 1e3 / e2e_steps
+    e2e_ms = max(t0.elapsed_time(t1) / e2e_steps, wall_ms)
+    assert len(seen) == e2e_steps
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -332,7 +335,8 @@ def run_ours(args, rank, world, local_rank):
         },
         "e2e": {"value": e2e_value, "unit": "particle-pushes/s", "h2d_bytes_per_step": nodes * 8,
                 "d2h_bytes_per_step": nodes * 8,
-                "path": "Engine.step() public API: E-field H2D (pinned) + step + rho D2H, synced per step"},
+                "path": "Engine.run_pipelined(): per step E-field H2D from pinned memory + step + rho D2H "
+                        "into pinned memory read by the host (one step late, overlapped); max(device, wall)"},
         "gpu_launches": args.steps * launches_per_step + n_sorts * 2,
         "sol_probe": {"ms": sol_ms, "actual_bytes": actual_bytes, "gbs": actual_bytes / (sol_ms * 1e-3) / 1e9,
                       "mover_actual_gbs": actual_bytes / (push_ms * 1e-3) / 1e9,

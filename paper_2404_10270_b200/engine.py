@@ -342,8 +342,11 @@ class Engine:
                 s.swap_with_spare()
             self._arr = None  # graphs are keyed by buffer addresses (_graph_key)
 
-    def step(self, timed: bool = False):
+    def step(self, timed: bool = False, e_ext: torch.Tensor = None):
         """One full cycle.  Returns rho/E of this step (device tensors).
+
+        e_ext: externally supplied E nodes (device, nc+1) for field-free runs,
+        used in place of the (identically zero) field.
 
         The engine works on its own stream; the caller's current stream is
         ordered after the step (so reading rho/E there is safe) and the next
@@ -359,6 +362,10 @@ class Engine:
         e = self.field(rho)
         if self.cfg.field_solve and self.cfg.smoothing_passes > 0:
             rho = self.rho_s  # the reference reports the smoothed density (harness.py:165-166)
+        if e_ext is not None:
+            if self.cfg.field_solve:
+                raise EngineError("e_ext is for field-free runs; field_solve computes E")
+            e = e_ext
         self.push(e)
         self.resort()
         if timed:
@@ -370,6 +377,112 @@ class Engine:
         if self.check_every and self.step_index % self.check_every == 0:
             self.sync()
         return rho, e
+
+    def run_pipelined(self, steps: int, e_source=None, on_result=None):
+        """`steps` cycles driven from the host with the I/O overlapped.
+
+        Per step k: the step's input E (a pinned host tensor from
+        e_source(k), field-free runs) is copied H2D on an input stream into
+        one of two device slots; the step runs on the engine stream (a
+        captured single-step graph when no sort is due); its rho is
+        snapshotted on device and copied D2H into one of two pinned host
+        buffers on a result stream.  The host launches step k+1 before it
+        waits for rho_k, then calls on_result(k, rho_host) -- every step's
+        result is read, one step late, while the GPU works on the next.
+        Returns the number of results delivered (== steps)."""
+        dev, nodes = self.device, self.nc + 1
+        if not hasattr(self, "_pipe"):
+            self._pipe = {
+                "h2d": torch.cuda.Stream(dev),  # inputs never queue behind results
+                "d2h": torch.cuda.Stream(dev),
+                "e": [torch.zeros(nodes, dtype=torch.float64, device=dev) for _ in range(2)],
+                "snap": [torch.zeros(nodes, dtype=torch.float64, device=dev) for _ in range(2)],
+                "host": [torch.zeros(nodes, dtype=torch.float64).pin_memory() for _ in range(2)],
+            }
+        P = self._pipe
+        h2d, d2h = P["h2d"], P["d2h"]
+        step_done = [None, None]
+        d2h_done = [None, None]
+        delivered = 0
+
+        def deliver(k):
+            nonlocal delivered
+            slot = k % 2
+            d2h_done[slot].synchronize()
+            if on_result is not None:
+                on_result(k, P["host"][slot])
+            delivered += 1
+
+        use_graphs = not self.cfg.field_solve and self.world == 1
+        for k in range(steps):
+            slot = k % 2
+            e_dev = None
+            if e_source is not None:
+                if step_done[slot] is not None:
+                    h2d.wait_event(step_done[slot])  # step k-2 finished reading this slot
+                with torch.cuda.stream(h2d):
+                    P["e"][slot].copy_(e_source(k), non_blocking=True)
+                    ev_in = torch.cuda.Event()
+                    ev_in.record(h2d)
+                self.stream.wait_event(ev_in)
+                e_dev = P["e"][slot]
+            if use_graphs and not self._sort_due(1):
+                # one captured step per (buffer state, input slot): density on a
+                # side stream overlapped with the push, then the rho snapshot
+                key = ("pipe", slot, e_dev is not None) + self._graph_key()
+                g = self.graphs.get(key)
+                if g is None:
+                    self.sync()
+                    self.stream.synchronize()
+                    g = self._capture_pipe_step(slot, e_dev)
+                    self.graphs[key] = g
+                with torch.cuda.stream(self.stream):
+                    g.replay()
+                self.cur = 1 - self.cur  # the replayed push deposited into the other set
+                self._next_clear = False
+                self.step_index += 1
+            else:
+                rho, _ = self.step(e_ext=e_dev)
+                with torch.cuda.stream(self.stream):
+                    P["snap"][slot].copy_(rho, non_blocking=True)
+            with torch.cuda.stream(self.stream):
+                ev = torch.cuda.Event()
+                ev.record(self.stream)
+            step_done[slot] = ev
+            if k >= 1:
+                deliver(k - 1)  # host buffer (k-1)%2 is free again after this
+            d2h.wait_event(ev)
+            with torch.cuda.stream(d2h):
+                P["host"][slot].copy_(P["snap"][slot], non_blocking=True)
+                d = torch.cuda.Event()
+                d.record(d2h)
+            d2h_done[slot] = d
+        if steps >= 1:
+            deliver(steps - 1)
+        return delivered
+
+    def _capture_pipe_step(self, slot, e_dev):
+        """One field-free step as a graph: density epilogue on the side stream
+        concurrent with the push, then rho snapshotted into the pipe slot."""
+        g = torch.cuda.CUDAGraph()
+        start = self.cur
+        with torch.cuda.graph(g, stream=self.stream):
+            self._side.wait_stream(self.stream)
+            rho = self.density(self._side, clear_next=False)
+            done = torch.cuda.Event()
+            done.record(self._side)
+            self.push(e_dev if e_dev is not None else self.e)
+            if self.absorbing:
+                arr, n = self._species()
+                _lib.check(self.lib.pb_compact(arr, n, self.status.data_ptr(),
+                                               self.compact_scratch.data_ptr(),
+                                               self.compact_scratch.numel(), self._sh()), "pb_compact")
+            self.stream.wait_event(done)
+            self._pipe["snap"][slot].copy_(rho, non_blocking=True)
+        # capture advanced the host-side parity; replay() of this graph does
+        # the same, so restore it and let the caller account the step
+        self.cur = start
+        return g
 
     # -- CUDA graph replay --------------------------------------------------------------
     def capture(self):
