@@ -304,7 +304,7 @@ def run_ours(args, rank, world, local_rank):
     peak, peak_kind = measured_peak()
     achieved = alg_bytes / (push_ms * 1e-3) / 1e9
     traffic = committed_traffic()
-    launches_per_step = 2
+    launches_per_step = 3  # k_partials_clear + k_stitch (density) + k_push_quad
     # our kernels per sort: k_iota + k_permute (the radix passes are CUB's)
     n_sorts = sum(args.steps // p for p in eng.sort_periods if p)
     out = {

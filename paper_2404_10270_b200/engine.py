@@ -125,6 +125,7 @@ class Engine:
 
         self.stream = torch.cuda.Stream(self.device)
         self._side = torch.cuda.Stream(self.device)  # overlapped density epilogue
+        self._epi_prev = None  # event: last side-stream epilogue (eager overlap)
         self.sp = []
         self.coef_dep = []
         ndep = 0
@@ -354,11 +355,29 @@ class Engine:
         updates never race the caller's reads)."""
         caller = torch.cuda.current_stream(self.device)
         self.stream.wait_stream(caller)
+        # Field-free runs: E does not depend on rho, so the density epilogue
+        # (and across GPUs the bin allreduce) runs on a side stream while the
+        # push runs; push n waits only for epilogue n-1, which cleared the bin
+        # set it deposits into.  With a field solve the cycle is serial.
+        overlap = not self.cfg.field_solve
         if timed:
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
             self._timing = (ev[1], ev[2])
             ev[0].record(self.stream)
-        rho = self.density()
+        if overlap:
+            self._side.wait_stream(self.stream)
+            if timed:
+                ev[4].record(self._side)
+            rho = self.density(self._side, clear_next=False)
+            done = torch.cuda.Event(enable_timing=timed)
+            done.record(self._side)
+            if timed:
+                ev[5] = done
+            if self._epi_prev is not None:
+                self.stream.wait_event(self._epi_prev)
+            self._epi_prev = done
+        else:
+            rho = self.density()
         e = self.field(rho)
         if self.cfg.field_solve and self.cfg.smoothing_passes > 0:
             rho = self.rho_s  # the reference reports the smoothed density (harness.py:165-166)
@@ -370,10 +389,14 @@ class Engine:
         self.resort()
         if timed:
             ev[3].record(self.stream)
+            if not overlap:
+                ev[4] = ev[5] = None
             self.phase_events.append(ev)
             self._timing = None
         self.step_index += 1
         caller.wait_stream(self.stream)
+        if overlap:
+            caller.wait_stream(self._side)
         if self.check_every and self.step_index % self.check_every == 0:
             self.sync()
         return rho, e
@@ -436,13 +459,17 @@ class Engine:
                     self.stream.synchronize()
                     g = self._capture_pipe_step(slot, e_dev)
                     self.graphs[key] = g
+                if self._epi_prev is not None:
+                    self.stream.wait_event(self._epi_prev)
                 with torch.cuda.stream(self.stream):
                     g.replay()
+                self._epi_prev = None
                 self.cur = 1 - self.cur  # the replayed push deposited into the other set
                 self._next_clear = False
                 self.step_index += 1
             else:
                 rho, _ = self.step(e_ext=e_dev)
+                self.stream.wait_stream(self._side)  # rho may come from the side stream
                 with torch.cuda.stream(self.stream):
                     P["snap"][slot].copy_(rho, non_blocking=True)
             with torch.cuda.stream(self.stream):
@@ -576,12 +603,15 @@ class Engine:
         try:
             left = steps
             while left > 0:
-                if left >= 2 and not self._sort_due(1) and not self._sort_due(2):
+                if self.world == 1 and left >= 2 and not self._sort_due(1) and not self._sort_due(2):
                     g = self.graphs.get(self._graph_key())
                     if g is None:
                         g = self.capture()
+                    if self._epi_prev is not None:  # an eager epilogue may still be clearing
+                        self.stream.wait_event(self._epi_prev)
                     with torch.cuda.stream(self.stream):
                         g.replay()
+                    self._epi_prev = None  # the graph joined its epilogues
                     self.step_index += 2
                     left -= 2
                 else:
@@ -598,6 +628,7 @@ class Engine:
         """Wait for enqueued work, fold the sticky device status into the
         host tallies, raise the first recorded error, and reset the status."""
         self.stream.synchronize()
+        self._side.synchronize()
         raw = self.status.cpu().numpy()
         st = decode_status(raw)
         for k in range(len(self.sp)):
@@ -632,16 +663,22 @@ class Engine:
     def phase_seconds(self) -> dict:
         """Per-phase seconds of the timed steps, from CUDA events: "mover" is
         the fused push+deposit launch, "deposit" the bin reduction and
-        density epilogue, "resort" compaction / sort."""
+        density epilogue (on the side stream when overlapped with the push),
+        "resort" compaction / sort."""
         self.stream.synchronize()
+        self._side.synchronize()
         out = {k: 0.0 for k in PHASE_KEYS}
         for ev in self.phase_events:
             total = ev[0].elapsed_time(ev[3]) * 1e-3
             mover = ev[1].elapsed_time(ev[2]) * 1e-3
             pre = ev[0].elapsed_time(ev[1]) * 1e-3
             out["mover"] += mover
-            out["deposit"] += pre
-            out["resort"] += total - mover - pre
+            if ev[4] is not None:
+                out["deposit"] += ev[4].elapsed_time(ev[5]) * 1e-3
+                out["resort"] += max(0.0, total - mover - pre)
+            else:
+                out["deposit"] += pre
+                out["resort"] += total - mover - pre
         return out
 
     def mover_ms(self) -> list:
