@@ -63,11 +63,42 @@ def make_config(nc_total, sort_every):
     )
 
 
-def species_alg_bytes(sp):
+def species_alg_bytes(sp, boris=False):
     if not sp.active_mover:
         return 0.0
-    key = "kick" if sp.charged else "drift"
+    key = ("boris" if boris else "kick") if sp.charged else "drift"
     return ALG_BYTES[key + ("_yp" if sp.track_transverse else "")]
+
+
+# BASELINE.json configs: c2 is the default bench line; the others are run with
+# --workload for the record (profiles/), from the TOML files in configs/.
+WORKLOADS = {
+    "c2": ("config 2: 1D3V unmagnetized, desk species e-/D+/D(yp), E=0 (field solve off)", "weak", None),
+    "c3": ("config 3: bounded sheath, absorbing walls + compaction, Dirichlet field solve, cell sort",
+           "weak", "configs/c3_sheath_absorbing.toml"),
+    "c4": ("config 4: magnetized SOL slab, Boris push, 3 species, 100M particles total, field solve",
+           "strong", "configs/c4_sol_boris.toml"),
+    "c5": ("config 5: 1M cells, 1B particles total (e-/D+/D), field solve off", "strong",
+           "configs/c5_weak_1m.toml"),
+}
+
+
+def workload_config(name, world, sort_every):
+    from dataclasses import replace
+
+    from paper_2404_10270_b200 import load_config
+
+    desc, scaling, path = WORKLOADS[name]
+    if path is None:
+        return make_config(NC_PER_GPU * world, sort_every), desc, scaling
+    cfg = load_config(os.path.join(ROOT, path))
+    if scaling == "weak" and world > 1:
+        cfg = cfg.scaled_for_workers(world)
+    # throughput runs use the parallel Poisson solve; the bitwise serial one
+    # ("exact") is for parity runs (tests)
+    cfg = replace(cfg, max_store_mb=1 << 20, n_steps=0, worker_count=1, poisson="scan",
+                  sort_every=cfg.sort_every if sort_every is None else sort_every)
+    return cfg, desc, scaling
 
 
 # ---------------------------------------------------------------------------
@@ -212,24 +243,25 @@ def run_ours(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    nc_total = NC_PER_GPU * world
-    cfg = make_config(nc_total, args.sort_every)
+    cfg, desc, scaling = workload_config(args.workload, world, args.sort_every)
+    nc_total = cfg.grid.nc
     eng = Engine(cfg, device=dev, rank=rank, world=world, group=None, init="device", check_every=0)
     torch.cuda.synchronize(dev)
     pushes_rank = sum(s.n for s in eng.sp if s.kind != 0)
-    alg_bytes = sum(s.n * species_alg_bytes(s.sp) for s in eng.sp)
+    boris = cfg.b_field_t is not None
+    alg_bytes = sum(s.n * species_alg_bytes(s.sp, boris) for s in eng.sp)
 
     # Every CUDA graph the timed replay can need (bin parity x sort buffer
     # state) is captured before timing; periodic sorts run eagerly.
     eng.prepare_graphs(args.warmup + args.steps)
-    eng.replay(args.warmup)
-    eng.sync()
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
-        time.sleep(0.3)
+        time.sleep(0.3)  # sampler start-up; the warm-up below brings the clocks back up
+        eng.replay(args.warmup)
+        eng.sync()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
         start.record(eng.stream)
         eng.replay(args.steps)
         end.record(eng.stream)
@@ -249,7 +281,12 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([ms, push_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, push_ms = float(t[0]), float(t[1])
-    value = pushes_rank * world / (ms * 1e-3)
+    pushes_total = pushes_rank * world
+    if world > 1:
+        t = torch.tensor([pushes_rank], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        pushes_total = int(t.item())
+    value = pushes_total / (ms * 1e-3)
 
     # e2e: the public host-driven API (Engine.run_pipelined): every step copies
     # its E-field input H2D from pinned host memory and its rho result D2H into
@@ -259,11 +296,13 @@ def run_ours(args, rank, world, local_rank):
     e_host = torch.zeros(nodes, dtype=torch.float64).pin_memory()
     e2e_steps = max(3, min(args.steps, 400))
     seen = []
+    # field-solve workloads compute E on device: their per-step input is none
+    e_src = None if cfg.field_solve else (lambda k: e_host)
 
     def on_result(k, rho_host):
         seen.append(float(rho_host[k % nodes]))
 
-    eng.run_pipelined(4, e_source=lambda k: e_host, on_result=None)  # warm the pinned ring
+    eng.run_pipelined(4, e_source=e_src, on_result=None)  # warm the pinned ring
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -271,7 +310,7 @@ def run_ours(args, rank, world, local_rank):
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(eng.stream)
     w0 = time.perf_counter()
-    eng.run_pipelined(e2e_steps, e_source=lambda k: e_host, on_result=on_result)
+    eng.run_pipelined(e2e_steps, e_source=e_src, on_result=on_result)
     t1.record(eng.stream)
     torch.cuda.synchronize(dev)
     wall_ms = (time.perf_counter() - w0) * 1e3 / e2e_steps
@@ -281,7 +320,7 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t[0])
-    e2e_value = pushes_rank * world / (e2e_ms * 1e-3)
+    e2e_value = pushes_total / (e2e_ms * 1e-3)
 
     # Speed-of-light probe (last: it overwrites particle state): the same
     # read/write byte mix streamed with a trivial update and no physics.
@@ -290,6 +329,7 @@ def run_ours(args, rank, world, local_rank):
     actual_bytes = 0.0
     for s in eng.sp:
         actual_bytes += s.n * (36.0 if s.kind != 1 else (48.0 if s.has_yp else 24.0))
+    # (the probe streams the c2 byte mix: x, vx [, vy, yp] and cell per species)
     torch.cuda.synchronize(dev)
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(2):
@@ -304,7 +344,13 @@ def run_ours(args, rank, world, local_rank):
     peak, peak_kind = measured_peak()
     achieved = alg_bytes / (push_ms * 1e-3) / 1e9
     traffic = committed_traffic()
-    launches_per_step = 3  # k_partials_clear + k_stitch (density) + k_push_quad
+    # k_partials_clear + k_stitch (density) + k_push_quad; field solve: one
+    # k_smooth_pass per pass + one Poisson kernel + k_efield; walls: k_compact
+    launches_per_step = 3
+    if cfg.field_solve:
+        launches_per_step += cfg.smoothing_passes + 2
+    if eng.absorbing:
+        launches_per_step += 1
     # our kernels per sort: k_iota + k_permute (the radix passes are CUB's)
     n_sorts = sum(args.steps // p for p in eng.sort_periods if p)
     out = {
@@ -316,16 +362,19 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling,
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (device init_plasma with the reference splitmix64 streams, seed 20260819)",
         "config": {
-            "workload": "config 2: 1D3V unmagnetized, desk species e-/D+/D(yp), E=0 (field solve off)",
-            "nc_per_gpu": NC_PER_GPU, "nc_total": nc_total, "ppc0_per_species": PPC0,
-            "particles_per_gpu": pushes_rank, "particles_total": pushes_rank * world,
-            "sort_every": args.sort_every, "sort_periods": eng.sort_periods, "parallelism": f"particle shards x{world}, replicated grid",
-            "l2": "inputs 1.12 GB/GPU >> 126 MB L2; no flush needed",
+            "workload": desc,
+            "nc_per_gpu": nc_total // world if scaling == "weak" else nc_total, "nc_total": nc_total,
+            "ppc0_per_species": cfg.ppc0,
+            "particles_per_gpu": pushes_rank, "particles_total": pushes_total,
+            "sort_every": cfg.sort_every, "sort_periods": eng.sort_periods,
+            "parallelism": f"particle shards x{world}, replicated grid",
+            "l2": (f"inputs {alg_bytes / 1e9:.2f} GB/GPU vs 126 MB L2" +
+                   ("; no flush needed" if alg_bytes > 4 * 126e6 else "; L2-resident, roofline not meaningful")),
         },
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -333,7 +382,8 @@ def run_ours(args, rank, world, local_rank):
             "alg_bytes_per_launch": alg_bytes, "push_ms": push_ms,
             "traffic": None if traffic is None else traffic.get("dram_bytes_per_launch"),
         },
-        "e2e": {"value": e2e_value, "unit": "particle-pushes/s", "h2d_bytes_per_step": nodes * 8,
+        "e2e": {"value": e2e_value, "unit": "particle-pushes/s",
+                "h2d_bytes_per_step": 0 if cfg.field_solve else nodes * 8,
                 "d2h_bytes_per_step": nodes * 8,
                 "path": "Engine.run_pipelined(): per step E-field H2D from pinned memory + step + rho D2H "
                         "into pinned memory read by the host (one step late, overlapped); max(device, wall)"},
@@ -351,7 +401,9 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sort-every", type=int, default=100)
+    ap.add_argument("--sort-every", type=int, default=None,
+                    help="base cell-sort period (default: 100 for c2, the TOML value otherwise)")
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -380,9 +432,11 @@ def main():
 
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.sort_every is None and args.workload == "c2":
+        args.sort_every = 100
     out, clocks = run_ours(args, rank, world, local_rank)
     out["clocks"] = clocks
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c2":
         out["cpu_baseline"] = cpu_reference_rate(target_seconds=args.cpu_seconds)
     if rank == 0:
         print(json.dumps(out), flush=True)

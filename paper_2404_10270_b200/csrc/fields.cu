@@ -165,102 +165,178 @@ __device__ __forceinline__ DD dd_add(DD a, DD b) {
 }
 __device__ __forceinline__ DD dd_of(double v) { return {v, 0.0}; }
 
-constexpr int kScanThreads = 1024;
+// ---- multi-block scan solve ------------------------------------------------
+// Closed-form pivots d_k = -(k+2)/(k+1) turn the two Thomas sweeps into
+//   z_k = sum_{i<=k} (i+1) rhs_i,  y_k = z_k/(k+1)          (forward)
+//   w_k = sum_{i>=k} -y_i/(i+2),   x_k = (k+1) w_k          (backward)
+// Both are prefix sums, done with double-double accumulation over a grid of
+// 2048-element tiles: per-tile DD partials, then every block adds the
+// partials before it (deterministic order) and scans its own tile.
+constexpr int kMbThreads = 256;
+constexpr int kMbPer = 8;
+constexpr int kMbTile = kMbThreads * kMbPer;
 
-// Block-wide exclusive scan of one DD per thread (Kogge-Stone in smem).
-__device__ DD block_exclusive_scan(DD v, DD *sm) {
-  const int t = threadIdx.x;
-  sm[t] = v;
+__device__ DD mb_block_reduce(DD v, DD *sm) {
+  sm[threadIdx.x] = v;
   __syncthreads();
-  for (int d = 1; d < kScanThreads; d <<= 1) {
-    DD o = t >= d ? sm[t - d] : dd_of(0.0);
-    __syncthreads();
-    if (t >= d) sm[t] = dd_add(o, sm[t]);
-    __syncthreads();
-  }
-  DD incl = sm[t];
-  DD excl = t > 0 ? sm[t - 1] : dd_of(0.0);
-  __syncthreads();
-  (void)incl;
-  return excl;
-}
-
-__device__ DD block_sum(const double *a, int64_t n, DD *sm) {
-  DD acc = dd_of(0.0);
-  for (int64_t i = threadIdx.x; i < n; i += kScanThreads) acc = dd_add(acc, dd_of(a[i]));
-  sm[threadIdx.x] = acc;
-  __syncthreads();
-  for (int d = kScanThreads / 2; d > 0; d >>= 1) {
+  for (int d = kMbThreads / 2; d > 0; d >>= 1) {
     if ((int)threadIdx.x < d) sm[threadIdx.x] = dd_add(sm[threadIdx.x], sm[threadIdx.x + d]);
     __syncthreads();
   }
-  DD r = sm[0];
+  const DD r = sm[0];
   __syncthreads();
   return r;
 }
 
-__global__ void __launch_bounds__(kScanThreads)
-    k_poisson_scan(const double *__restrict__ rho, double *phi, int64_t nc, double scale,
-                   int field_bc, double phi_left, double phi_right, double *scratch) {
-  __shared__ DD sm[kScanThreads];
-  const int64_t n = nc - 1;  // unknowns: nodes 1..nc-1
-  double *y = scratch;
-  double mean = 0.0;
-  if (field_bc == PB_FIELD_PERIODIC) {
-    const DD s = block_sum(rho, nc, sm);
-    mean = __ddiv_rn(s.hi + s.lo, (double)nc);
-  }
-  const int64_t per = (n + kScanThreads - 1) / kScanThreads;
-  const int64_t lo = (int64_t)threadIdx.x * per;
-  const int64_t hi = lo + per < n ? lo + per : n;
-  auto rhs = [&](int64_t k) -> double {
-    if (field_bc == PB_FIELD_PERIODIC) return __dmul_rn(-__dsub_rn(rho[k + 1], mean), scale);
-    double r = __dmul_rn(-rho[k + 1], scale);
-    if (k == 0) r = __dsub_rn(r, phi_left);
-    if (k == n - 1) r = __dsub_rn(r, phi_right);
-    return r;
-  };
-  // Pass 1: z = prefix sum of (k+1) rhs_k ; y_k = z_k / (k+1)
-  DD seg = dd_of(0.0);
-  for (int64_t k = lo; k < hi; ++k) seg = dd_add(seg, dd_of(__dmul_rn((double)(k + 1), rhs(k))));
-  DD off = block_exclusive_scan(seg, sm);
-  for (int64_t k = lo; k < hi; ++k) {
-    off = dd_add(off, dd_of(__dmul_rn((double)(k + 1), rhs(k))));
-    y[k] = __ddiv_rn(__dadd_rn(off.hi, off.lo), (double)(k + 1));
-  }
+// Exclusive scan over threads in order t (rev = false) or NT-1-t (rev = true).
+__device__ DD mb_block_excl(DD v, DD *sm, bool rev) {
+  const int t = rev ? kMbThreads - 1 - (int)threadIdx.x : (int)threadIdx.x;
+  sm[t] = v;
   __syncthreads();
-  // Pass 2: w = suffix sum of -y_k/(k+2) ; x_k = (k+1) w_k  (reversed ranks)
-  const int r = kScanThreads - 1 - (int)threadIdx.x;
-  const int64_t lo2 = (int64_t)r * per;
-  const int64_t hi2 = lo2 + per < n ? lo2 + per : n;
-  seg = dd_of(0.0);
-  for (int64_t k = hi2 - 1; k >= lo2; --k) seg = dd_add(seg, dd_of(-__ddiv_rn(y[k], (double)(k + 2))));
-  off = block_exclusive_scan(seg, sm);
-  for (int64_t k = hi2 - 1; k >= lo2; --k) {
-    off = dd_add(off, dd_of(-__ddiv_rn(y[k], (double)(k + 2))));
-    phi[k + 1] = __dmul_rn((double)(k + 1), __dadd_rn(off.hi, off.lo));
+  for (int d = 1; d < kMbThreads; d <<= 1) {
+    const DD o = t >= d ? sm[t - d] : dd_of(0.0);
+    __syncthreads();
+    if (t >= d) sm[t] = dd_add(o, sm[t]);
+    __syncthreads();
   }
+  const DD ex = t > 0 ? sm[t - 1] : dd_of(0.0);
   __syncthreads();
-  if (field_bc == PB_FIELD_PERIODIC) {
-    if (threadIdx.x == 0) phi[0] = 0.0;
-    __syncthreads();
-    const DD s = block_sum(phi, nc, sm);
-    const double shift = __ddiv_rn(s.hi + s.lo, (double)nc);
-    for (int64_t j = threadIdx.x; j < nc; j += kScanThreads) phi[j] = __dsub_rn(phi[j], shift);
-    __syncthreads();
-    if (threadIdx.x == 0) phi[nc] = phi[0];
-  } else if (threadIdx.x == 0) {
-    phi[0] = phi_left;
-    phi[nc] = phi_right;
+  return ex;
+}
+
+// Sum of part[lo, hi) in index order (each block computes the same value).
+__device__ DD mb_sum_parts(const DD *part, int64_t lo, int64_t hi, DD *sm) {
+  DD acc = dd_of(0.0);
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kMbThreads) acc = dd_add(acc, part[i]);
+  return mb_block_reduce(acc, sm);
+}
+
+struct PoissonArgs {
+  const double *rho;
+  double *phi;
+  double *y;
+  DD *p0, *p1, *p2, *p3;  // per-tile partials: rho, forward, backward, phi
+  int64_t nc, n;
+  int nt;                 // tiles over the n unknowns
+  int ntc;                // tiles over the nc nodes
+  double scale, phi_left, phi_right;
+  int field_bc;
+};
+
+__device__ __forceinline__ double mb_mean(const PoissonArgs &a, DD *sm) {
+  if (a.field_bc != PB_FIELD_PERIODIC) return 0.0;
+  const DD s = mb_sum_parts(a.p0, 0, a.ntc, sm);
+  return __ddiv_rn(__dadd_rn(s.hi, s.lo), (double)a.nc);
+}
+
+__device__ __forceinline__ double mb_rhs(const PoissonArgs &a, int64_t k, double mean) {
+  if (a.field_bc == PB_FIELD_PERIODIC) return __dmul_rn(-__dsub_rn(a.rho[k + 1], mean), a.scale);
+  double r = __dmul_rn(-a.rho[k + 1], a.scale);
+  if (k == 0) r = __dsub_rn(r, a.phi_left);
+  if (k == a.n - 1) r = __dsub_rn(r, a.phi_right);
+  return r;
+}
+
+// tile partial sums of src[0, len) -> part[blockIdx.x]
+__global__ void __launch_bounds__(kMbThreads) k_mb_tile_sum(const double *__restrict__ src,
+                                                            int64_t len, DD *part) {
+  __shared__ DD sm[kMbThreads];
+  const int64_t base = (int64_t)blockIdx.x * kMbTile + (int64_t)threadIdx.x * kMbPer;
+  DD acc = dd_of(0.0);
+  for (int j = 0; j < kMbPer; ++j)
+    if (base + j < len) acc = dd_add(acc, dd_of(src[base + j]));
+  const DD r = mb_block_reduce(acc, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = r;
+}
+
+__global__ void __launch_bounds__(kMbThreads) k_mb_fwd_part(const PoissonArgs a) {
+  __shared__ DD sm[kMbThreads];
+  const double mean = mb_mean(a, sm);
+  const int64_t base = (int64_t)blockIdx.x * kMbTile + (int64_t)threadIdx.x * kMbPer;
+  DD acc = dd_of(0.0);
+  for (int j = 0; j < kMbPer; ++j) {
+    const int64_t k = base + j;
+    if (k < a.n) acc = dd_add(acc, dd_of(__dmul_rn((double)(k + 1), mb_rhs(a, k, mean))));
+  }
+  const DD r = mb_block_reduce(acc, sm);
+  if (threadIdx.x == 0) a.p1[blockIdx.x] = r;
+}
+
+__global__ void __launch_bounds__(kMbThreads) k_mb_fwd_scan(const PoissonArgs a) {
+  __shared__ DD sm[kMbThreads];
+  const double mean = mb_mean(a, sm);
+  const DD before = mb_sum_parts(a.p1, 0, blockIdx.x, sm);
+  const int64_t base = (int64_t)blockIdx.x * kMbTile + (int64_t)threadIdx.x * kMbPer;
+  double v[kMbPer];
+  DD loc = dd_of(0.0);
+  for (int j = 0; j < kMbPer; ++j) {
+    const int64_t k = base + j;
+    v[j] = k < a.n ? __dmul_rn((double)(k + 1), mb_rhs(a, k, mean)) : 0.0;
+    loc = dd_add(loc, dd_of(v[j]));
+  }
+  DD off = dd_add(before, mb_block_excl(loc, sm, false));
+  DD bsum = dd_of(0.0);
+  for (int j = 0; j < kMbPer; ++j) {
+    const int64_t k = base + j;
+    if (k >= a.n) break;
+    off = dd_add(off, dd_of(v[j]));
+    const double y = __ddiv_rn(__dadd_rn(off.hi, off.lo), (double)(k + 1));
+    a.y[k] = y;
+    bsum = dd_add(bsum, dd_of(-__ddiv_rn(y, (double)(k + 2))));
+  }
+  const DD r = mb_block_reduce(bsum, sm);
+  if (threadIdx.x == 0) a.p2[blockIdx.x] = r;
+}
+
+__global__ void __launch_bounds__(kMbThreads) k_mb_bwd_scan(const PoissonArgs a) {
+  __shared__ DD sm[kMbThreads];
+  const DD after = mb_sum_parts(a.p2, blockIdx.x + 1, a.nt, sm);
+  const int64_t base = (int64_t)blockIdx.x * kMbTile + (int64_t)threadIdx.x * kMbPer;
+  double u[kMbPer];
+  DD loc = dd_of(0.0);
+  for (int j = kMbPer - 1; j >= 0; --j) {
+    const int64_t k = base + j;
+    u[j] = k < a.n ? -__ddiv_rn(a.y[k], (double)(k + 2)) : 0.0;
+    loc = dd_add(loc, dd_of(u[j]));
+  }
+  DD off = dd_add(after, mb_block_excl(loc, sm, true));
+  for (int j = kMbPer - 1; j >= 0; --j) {
+    const int64_t k = base + j;
+    if (k >= a.n) continue;
+    off = dd_add(off, dd_of(u[j]));
+    a.phi[k + 1] = __dmul_rn((double)(k + 1), __dadd_rn(off.hi, off.lo));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (a.field_bc == PB_FIELD_PERIODIC) {
+      a.phi[0] = 0.0;
+    } else {
+      a.phi[0] = a.phi_left;
+      a.phi[a.nc] = a.phi_right;
+    }
   }
 }
+
+// periodic: phi[0..nc] -= mean(phi[:nc]); phi[nc] = phi[0]
+__global__ void __launch_bounds__(kMbThreads) k_mb_shift(const PoissonArgs a) {
+  __shared__ DD sm[kMbThreads];
+  const DD s = mb_sum_parts(a.p3, 0, a.ntc, sm);
+  const double shift = __ddiv_rn(__dadd_rn(s.hi, s.lo), (double)a.nc);
+  for (int64_t j = (int64_t)blockIdx.x * kMbThreads + threadIdx.x; j <= a.nc;
+       j += (int64_t)gridDim.x * kMbThreads) {
+    if (j < a.nc) a.phi[j] = __dsub_rn(a.phi[j], shift);
+  }
+}
+
+__global__ void k_mb_wrap(double *phi, int64_t nc) { phi[nc] = phi[0]; }
 
 static unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace pb
 
 extern "C" size_t pb_field_scratch_bytes(int64_t nc) {
-  return 3 * (size_t)(nc + 1) * sizeof(double);
+  // smoothing ping-pong + the scan solve's y and DD tile partials
+  const size_t tiles = (size_t)((nc + 1 + pb::kMbTile - 1) / pb::kMbTile) + 1;
+  return 3 * (size_t)(nc + 1) * sizeof(double) + 4 * tiles * sizeof(pb::DD) + 256;
 }
 
 extern "C" int pb_smooth_density(const double *rho, double *out, int64_t nc,
@@ -330,9 +406,38 @@ extern "C" int pb_solve_poisson_scan(const double *rho, double *phi, int64_t nc,
     return PB_ERR_INVALID;
   }
   const double scale = (dx * dx) / eps0;
-  pb::k_poisson_scan<<<1, pb::kScanThreads, 0, (cudaStream_t)stream>>>(
-      rho, phi, nc, scale, field_bc, phi_left, phi_right, (double *)scratch);
-  PB_CHECK_LAUNCH("k_poisson_scan");
+  cudaStream_t st = (cudaStream_t)stream;
+  pb::PoissonArgs a;
+  a.rho = rho;
+  a.phi = phi;
+  a.nc = nc;
+  a.n = nc - 1;
+  a.nt = (int)((a.n + pb::kMbTile - 1) / pb::kMbTile);
+  a.ntc = (int)((nc + pb::kMbTile - 1) / pb::kMbTile);
+  a.scale = scale;
+  a.phi_left = phi_left;
+  a.phi_right = phi_right;
+  a.field_bc = field_bc;
+  a.y = (double *)scratch;
+  size_t off = ((size_t)(nc + 1) * sizeof(double) + 255) & ~(size_t)255;
+  pb::DD *parts = (pb::DD *)((char *)scratch + off);
+  const int ptile = a.ntc + 1;
+  a.p0 = parts;
+  a.p1 = parts + ptile;
+  a.p2 = parts + 2 * ptile;
+  a.p3 = parts + 3 * ptile;
+  if (field_bc == PB_FIELD_PERIODIC) {
+    pb::k_mb_tile_sum<<<a.ntc, pb::kMbThreads, 0, st>>>(rho, nc, a.p0);
+  }
+  pb::k_mb_fwd_part<<<a.nt, pb::kMbThreads, 0, st>>>(a);
+  pb::k_mb_fwd_scan<<<a.nt, pb::kMbThreads, 0, st>>>(a);
+  pb::k_mb_bwd_scan<<<a.nt, pb::kMbThreads, 0, st>>>(a);
+  if (field_bc == PB_FIELD_PERIODIC) {
+    pb::k_mb_tile_sum<<<a.ntc, pb::kMbThreads, 0, st>>>(phi, nc, a.p3);
+    pb::k_mb_shift<<<a.ntc, pb::kMbThreads, 0, st>>>(a);
+    pb::k_mb_wrap<<<1, 1, 0, st>>>(phi, nc);
+  }
+  PB_CHECK_LAUNCH("poisson scan");
   return PB_OK;
 }
 

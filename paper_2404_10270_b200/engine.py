@@ -436,7 +436,7 @@ class Engine:
                 on_result(k, P["host"][slot])
             delivered += 1
 
-        use_graphs = not self.cfg.field_solve and self.world == 1
+        use_graphs = self.world == 1 and (e_source is None or not self.cfg.field_solve)
         for k in range(steps):
             slot = k % 2
             e_dev = None
@@ -489,22 +489,33 @@ class Engine:
         return delivered
 
     def _capture_pipe_step(self, slot, e_dev):
-        """One field-free step as a graph: density epilogue on the side stream
-        concurrent with the push, then rho snapshotted into the pipe slot."""
+        """One step as a graph: field-free runs put the density epilogue on
+        the side stream concurrent with the push; field-solve runs are serial
+        (density -> smooth -> Poisson -> E -> push).  Then rho is snapshotted
+        into the pipe slot."""
         g = torch.cuda.CUDAGraph()
         start = self.cur
+        overlap = not self.cfg.field_solve
         with torch.cuda.graph(g, stream=self.stream):
-            self._side.wait_stream(self.stream)
-            rho = self.density(self._side, clear_next=False)
-            done = torch.cuda.Event()
-            done.record(self._side)
-            self.push(e_dev if e_dev is not None else self.e)
+            if overlap:
+                self._side.wait_stream(self.stream)
+                rho = self.density(self._side, clear_next=False)
+                done = torch.cuda.Event()
+                done.record(self._side)
+                e = e_dev if e_dev is not None else self.e
+            else:
+                rho = self.density()
+                e = self.field(rho)
+                if self.cfg.smoothing_passes > 0:
+                    rho = self.rho_s
+            self.push(e)
             if self.absorbing:
                 arr, n = self._species()
                 _lib.check(self.lib.pb_compact(arr, n, self.status.data_ptr(),
                                                self.compact_scratch.data_ptr(),
                                                self.compact_scratch.numel(), self._sh()), "pb_compact")
-            self.stream.wait_event(done)
+            if overlap:
+                self.stream.wait_event(done)
             self._pipe["snap"][slot].copy_(rho, non_blocking=True)
         # capture advanced the host-side parity; replay() of this graph does
         # the same, so restore it and let the caller account the step

@@ -437,3 +437,29 @@ def test_run_pipelined_matches_eager_steps(cuda, sort_every):
     for x, y in zip(a.download(), b.download()):
         assert np.array_equal(oracle.canonical(x.cell, x.fields()), oracle.canonical(y.cell, y.fields()))
     assert any(isinstance(k, tuple) and k[0] == "pipe" for k in b.graphs)
+
+
+def test_run_pipelined_field_solve_absorbing(cuda):
+    """Field-solve + absorbing walls through the pipelined loop (single-step
+    graphs, serial density -> Poisson -> E -> push -> compaction) deliver the
+    eager steps' rho sequence bit for bit."""
+    from paper_2404_10270_b200 import Engine
+
+    cfg = _mk_config(nc=64, ppc0=16, field_solve=True, smoothing_passes=1, boundary="dirichlet",
+                     particle_boundary="absorbing", phi_left=2.0, phi_right=-1.0)
+    flats = _random_flats(cfg, 13, vscale=0.4)
+    a = Engine(cfg, device=cuda, check_every=0)
+    b = Engine(cfg, device=cuda, check_every=0)
+    a.upload(flats)
+    b.upload(flats)
+    want = []
+    for _ in range(6):
+        rho, _ = a.step()
+        want.append(rho.cpu().numpy().copy())
+    got = {}
+    b.run_pipelined(6, on_result=lambda k, r: got.__setitem__(k, r.numpy().copy()))
+    for k in range(6):
+        assert bits_equal(got[k], want[k]), k
+    a.sync()
+    b.sync()
+    assert np.array_equal(a.absorbed, b.absorbed) and a.absorbed.sum() > 0

@@ -157,6 +157,14 @@ def test_poisson_scan_matches_reference_and_exact(cuda):
             ref = g[f"n{nc}_{bc}_phi"]
             assert np.max(np.abs(phi - ref)) <= 1e-12 * np.max(np.abs(ref)), (nc, bc)
     rng = np.random.default_rng(5)
+    for nc in (3, 2048, 2049, 4097, 6001):  # tile-boundary sizes of the multi-block scan
+        rho = 30.0 * rng.standard_normal(nc + 1)
+        rho[nc] = rho[0]
+        for code in (0, 1):
+            a = solve(lib.pb_solve_poisson_scan, rho, nc, code)
+            b = solve(lib.pb_solve_poisson, rho, nc, code)
+            assert np.max(np.abs(a - b)) <= 1e-10 * np.max(np.abs(b)), (nc, code)
+            assert a[nc] == a[0] or code == 1
     nc = 100_000
     rho = 30.0 * rng.standard_normal(nc + 1) + 5.0 * np.sin(np.arange(nc + 1) * 2e-4)
     rho[nc] = rho[0]
