@@ -80,7 +80,7 @@ def test_configs_load_and_validate():
     from paper_2404_10270_b200 import load_config
 
     names = sorted(f for f in os.listdir(os.path.join(ROOT, "configs")) if f.endswith(".toml"))
-    assert len(names) == 6
+    assert len(names) == 7
     cfgs = {n: load_config(os.path.join(ROOT, "configs", n)) for n in names}
     for n in ("desk.toml", "c1_desk_ppc100.toml"):
         assert cfgs[n].canonical() and cfgs[n].collisions.rates.rate_ionization_m3s == 2.5e-11
