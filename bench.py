@@ -351,7 +351,7 @@ def run_ours(args, rank, world, local_rank):
         launches_per_step += cfg.smoothing_passes + 2
     if eng.absorbing:
         launches_per_step += 1
-    # our kernels per sort: k_iota + k_permute (the radix passes are CUB's)
+    # our kernels per sort: k_cell_count + k_cell_scatter (the scan is CUB's)
     n_sorts = sum(args.steps // p for p in eng.sort_periods if p)
     out = {
         "metric": METRIC,

@@ -167,8 +167,9 @@ size_t pb_compact_scratch_bytes(int64_t n);
 int pb_compact(const pb_species *sp, int nsp, pb_status *status,
                void *scratch, size_t scratch_bytes, void *stream);
 
-/* Periodic sort by cell: stable radix sort of (cell, slot) then a gather
- * permutation of every field into the `dst` species buffers (ping-pong).
+/* Periodic sort by cell: counting sort (cell histogram, exclusive scan,
+ * scatter of every field) into the `dst` species buffers (ping-pong).  Order
+ * within a cell is arbitrary (the engine's physics is order independent).
  * `scratch` needs pb_sort_scratch_bytes(n, nc) bytes. */
 size_t pb_sort_scratch_bytes(int64_t n, int64_t nc);
 int pb_sort_by_cell(const pb_species *src, const pb_species *dst, int64_t nc,

@@ -522,8 +522,11 @@ struct RunAcc {
   }
 };
 
+#ifndef PB_ST4
+#define PB_ST4 "st.global.cs.v4.f64"
+#endif
 __device__ __forceinline__ void st4(double *p, double a, double b, double c, double d) {
-  asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+  asm volatile(PB_ST4 " [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
                : "memory");
 }
 
@@ -888,7 +891,10 @@ __global__ void __launch_bounds__(kThreads + 32, PB_MINBLOCKS)
 // Deposit: thread-local run of the quad, then one warp segmented scan per
 // 128 particles, global u64 atomics from the segment tails.
 // ---------------------------------------------------------------------------
-constexpr int kChunk = 2048;
+#ifndef PB_CHUNK
+#define PB_CHUNK 2048
+#endif
+constexpr int kChunk = PB_CHUNK;
 
 #ifndef PB_LD4
 #define PB_LD4 "ld.global.cs.v4.f64"

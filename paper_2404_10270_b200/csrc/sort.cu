@@ -4,13 +4,17 @@
 // pays for it every step in resort/commit (pkg/src/picmc/mover.py:113-195,
 // pkg/src/picmc/core.py:192-240: ~133 ns/particle on the CPU).  The flat
 // device store instead carries a cell index per particle and restores cell
-// order only every S steps: a stable LSD radix sort of (cell, slot) over
-// ceil(log2 nc) bits, then one gather pass that permutes every field into
-// the ping-pong buffers.  Particle state is unchanged by the sort, and the
-// fixed-point deposit is order independent, so physics is bitwise identical
-// for any sort period.
+// order only every S steps with a counting sort: a cell histogram
+// (warp-aggregated atomics), an exclusive scan into per-cell cursors, and one
+// scatter pass that writes every field to its cell's range of the ping-pong
+// buffers (lanes of a warp sharing a cell take consecutive slots, so the
+// writes of nearly-sorted data stay coalesced).  Order within a cell is
+// arbitrary; particle state is unchanged by the sort and the fixed-point
+// deposit is order independent, so physics is bitwise identical for any sort
+// period.  ~0.8 GB of traffic for 10M electrons, vs ~1.7 GB for the LSD
+// radix sort + gather it replaced.
 #include <cub/block/block_scan.cuh>
-#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
 
@@ -18,41 +22,58 @@ namespace pb {
 
 static inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
-static int key_bits(int64_t nc) {
-  int b = 1;
-  while (b < 31 && ((int64_t)1 << b) < nc) ++b;
-  return b;
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
 }
 
-__global__ void k_iota(uint32_t *v, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    v[i] = (uint32_t)i;
-}
-
-struct PermArgs {
-  const double *src[5];
-  double *dst[5];
-  int nf;
-};
-
-__global__ void k_permute(PermArgs pa, const uint32_t *__restrict__ perm,
-                          int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t p = perm[i];
-#pragma unroll
-    for (int f = 0; f < 5; ++f)
-      if (f < pa.nf) pa.dst[f][i] = __ldg(pa.src[f] + p);
+// Per-cell counts; lanes holding the same cell add once per warp.
+__global__ void k_cell_count(const int32_t *__restrict__ cell, int64_t n, uint32_t *counts) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x; b < n; b += stride) {
+    const int64_t i = b + threadIdx.x;
+    const int32_t c = i < n ? __ldg(cell + i) : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, c);
+    if (c >= 0 && (threadIdx.x & 31) == (unsigned)(__ffs(grp) - 1))
+      atomicAdd(&counts[c], (uint32_t)__popc(grp));
   }
 }
 
-static size_t radix_temp_bytes(int64_t n, int64_t nc) {
+struct ScatterArgs {
+  const double *src[5];
+  double *dst[5];
+  int nf;
+  const int32_t *cell;
+  int32_t *cell_out;
+  uint32_t *cursor;
+  int64_t n;
+};
+
+__global__ void k_cell_scatter(const __grid_constant__ ScatterArgs a) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const unsigned lane = threadIdx.x & 31;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x; b < a.n; b += stride) {
+    const int64_t i = b + threadIdx.x;
+    const int32_t c = i < a.n ? __ldg(a.cell + i) : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, c);
+    const unsigned leader = (unsigned)(__ffs(grp) - 1);
+    uint32_t base = 0;
+    if (c >= 0 && lane == leader) base = atomicAdd(&a.cursor[c], (uint32_t)__popc(grp));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (c < 0) continue;
+    const uint32_t pos = base + (uint32_t)__popc(grp & lanemask_lt());
+#pragma unroll
+    for (int f = 0; f < 5; ++f)
+      if (f < a.nf) a.dst[f][pos] = __ldg(a.src[f] + i);
+    a.cell_out[pos] = c;
+  }
+}
+
+static size_t scan_temp_bytes(int64_t nc) {
   size_t t = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, t, (const uint32_t *)nullptr,
-                                  (uint32_t *)nullptr, (const uint32_t *)nullptr,
-                                  (uint32_t *)nullptr, (int)(n > 0 ? n : 1), 0,
-                                  key_bits(nc));
+  cub::DeviceScan::ExclusiveSum(nullptr, t, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                (int)nc);
   return t;
 }
 
@@ -123,21 +144,20 @@ __global__ void __launch_bounds__(kCompactThreads)
 }  // namespace pb
 
 extern "C" size_t pb_sort_scratch_bytes(int64_t n, int64_t nc) {
-  if (n < 1) n = 1;
-  return 2 * pb::align256((size_t)n * sizeof(uint32_t)) +
-         pb::align256(pb::radix_temp_bytes(n, nc));
+  (void)n;
+  if (nc < 1) nc = 1;
+  return 2 * pb::align256((size_t)nc * sizeof(uint32_t)) + pb::align256(pb::scan_temp_bytes(nc));
 }
 
-extern "C" int pb_sort_by_cell(const pb_species *src, const pb_species *dst,
-                               int64_t nc, void *scratch, size_t scratch_bytes,
-                               void *stream) {
+extern "C" int pb_sort_by_cell(const pb_species *src, const pb_species *dst, int64_t nc,
+                               void *scratch, size_t scratch_bytes, void *stream) {
   if (!src || !dst) {
     pb::set_error("pb_sort_by_cell: NULL species");
     return PB_ERR_INVALID;
   }
   const int64_t n = src->n;
   if (n <= 0) return PB_OK;
-  if (n > 0x7fffffffLL || nc < 1 || nc > 0x7fffffffLL) {
+  if (n > 0xffffffffLL || nc < 1 || nc > 0x7fffffffLL) {
     pb::set_error("pb_sort_by_cell: n=%lld nc=%lld out of range", (long long)n,
                   (long long)nc);
     return PB_ERR_INVALID;
@@ -148,30 +168,34 @@ extern "C" int pb_sort_by_cell(const pb_species *src, const pb_species *dst,
   }
   cudaStream_t st = (cudaStream_t)stream;
   char *p = (char *)scratch;
-  uint32_t *iota = (uint32_t *)p;
-  p += pb::align256((size_t)n * sizeof(uint32_t));
-  uint32_t *perm = (uint32_t *)p;
-  p += pb::align256((size_t)n * sizeof(uint32_t));
-  size_t tb = pb::radix_temp_bytes(n, nc);
-  pb::k_iota<<<148 * 8, 256, 0, st>>>(iota, n);
-  PB_CHECK_LAUNCH("k_iota");
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(
-      p, tb, (const uint32_t *)src->cell, (uint32_t *)dst->cell, iota, perm,
-      (int)n, 0, pb::key_bits(nc), st);
-  if (e != cudaSuccess) return pb::cuda_status(e, "DeviceRadixSort::SortPairs");
-  pb::PermArgs pa;
+  uint32_t *counts = (uint32_t *)p;
+  p += pb::align256((size_t)nc * sizeof(uint32_t));
+  uint32_t *cursor = (uint32_t *)p;
+  p += pb::align256((size_t)nc * sizeof(uint32_t));
+  cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)nc * sizeof(uint32_t), st);
+  if (e != cudaSuccess) return pb::cuda_status(e, "cudaMemsetAsync");
+  pb::k_cell_count<<<148 * 8, 256, 0, st>>>(src->cell, n, counts);
+  PB_CHECK_LAUNCH("k_cell_count");
+  size_t tb = pb::scan_temp_bytes(nc);
+  e = cub::DeviceScan::ExclusiveSum(p, tb, counts, cursor, (int)nc, st);
+  if (e != cudaSuccess) return pb::cuda_status(e, "DeviceScan::ExclusiveSum");
+  pb::ScatterArgs a;
   int nf = 0;
-  pa.src[nf] = src->x; pa.dst[nf++] = dst->x;
-  pa.src[nf] = src->vx; pa.dst[nf++] = dst->vx;
-  pa.src[nf] = src->vy; pa.dst[nf++] = dst->vy;
-  pa.src[nf] = src->vz; pa.dst[nf++] = dst->vz;
+  a.src[nf] = src->x; a.dst[nf++] = dst->x;
+  a.src[nf] = src->vx; a.dst[nf++] = dst->vx;
+  a.src[nf] = src->vy; a.dst[nf++] = dst->vy;
+  a.src[nf] = src->vz; a.dst[nf++] = dst->vz;
   if (src->yp && dst->yp) {
-    pa.src[nf] = src->yp;
-    pa.dst[nf++] = dst->yp;
+    a.src[nf] = src->yp;
+    a.dst[nf++] = dst->yp;
   }
-  pa.nf = nf;
-  pb::k_permute<<<148 * 8, 256, 0, st>>>(pa, perm, n);
-  PB_CHECK_LAUNCH("k_permute");
+  a.nf = nf;
+  a.cell = src->cell;
+  a.cell_out = dst->cell;
+  a.cursor = cursor;
+  a.n = n;
+  pb::k_cell_scatter<<<148 * 8, 256, 0, st>>>(a);
+  PB_CHECK_LAUNCH("k_cell_scatter");
   return PB_OK;
 }
 

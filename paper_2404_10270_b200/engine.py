@@ -570,6 +570,8 @@ class Engine:
         steps: both bin parities x both buffers of every species whose sort
         falls in that window.  Capturing launches nothing, so the buffer swaps
         here are pointer bookkeeping only; timed replays then never capture."""
+        if self.world > 1:
+            return  # multi-GPU steps replay eagerly: no NCCL collectives inside graphs
         self.sync()
         self.stream.synchronize()
         clear0 = self._next_clear
