@@ -121,6 +121,11 @@ class ClockSampler:
                  "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi's NVML start-up can stall the GPU for tens of ms: let
+            # it finish (first sample in) before anything is timed
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 10.0:
+                time.sleep(0.02)
         except OSError:
             self.proc = None
         return self
@@ -262,14 +267,29 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
+        graphs_before = len(eng.graphs)
         start.record(eng.stream)
-        eng.replay(args.steps)
+        # windows of 200 steps (events between graph launches cost nothing) to
+        # show whether a slow run is uniformly slow or had a hiccup
+        marks, left = [], args.steps
+        while left > 0:
+            k = min(200, left)
+            eng.replay(k)
+            left -= k
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(eng.stream)
+            marks.append((k, ev))
         end.record(eng.stream)
         torch.cuda.synchronize(dev)
+        graphs_timed = len(eng.graphs) - graphs_before
     eng.sync()
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(end) / args.steps
+    win_ms, prev = [], start
+    for k, ev in marks:
+        win_ms.append(prev.elapsed_time(ev) / k)
+        prev = ev
     # The mover kernel alone: CUDA events on the engine stream right around the
     # pb_push_deposit launch, over eager steps (host stays ahead of the GPU).
     eng.phase_events.clear()
@@ -388,6 +408,9 @@ def run_ours(args, rank, world, local_rank):
                 "path": "Engine.run_pipelined(): per step E-field H2D from pinned memory + step + rho D2H "
                         "into pinned memory read by the host (one step late, overlapped); max(device, wall)"},
         "gpu_launches": args.steps * launches_per_step + n_sorts * 2,
+        "timing_windows_ms": {"steps_per_window": 200, "min": min(win_ms), "median": float(np.median(win_ms)),
+                              "max": max(win_ms), "argmax": int(np.argmax(win_ms)),
+                              "graphs_captured_in_timed_region": graphs_timed},
         "sol_probe": {"ms": sol_ms, "actual_bytes": actual_bytes, "gbs": actual_bytes / (sol_ms * 1e-3) / 1e9,
                       "mover_actual_gbs": actual_bytes / (push_ms * 1e-3) / 1e9,
                       "note": "pb_stream_sol: same bytes (incl. cell index), trivial update, no deposit"},

@@ -39,6 +39,10 @@ struct LaunchArgs {
   int push;  // 0: deposit only (no mover)
   int order[PB_MAX_SPECIES];             // TMA kernel: species order of the tile list
   int64_t tile_start[PB_MAX_SPECIES + 1];  // TMA kernel: prefix of full tiles
+  // quad kernel chunk interleave: the first rr_chunks chunks go round-robin
+  // over the species (rr_each per species), the rest species by species
+  int64_t rr_chunks, rr_each;
+  int64_t tail_start[PB_MAX_SPECIES + 1];
   const double *e;
   int64_t nc;
   uint64_t *bins;
@@ -1072,11 +1076,19 @@ __device__ __forceinline__ void quad_chunk(const LaunchArgs &a, int isp, int64_t
 __device__ __forceinline__ int chunk_species(const LaunchArgs &a, int64_t c, int64_t &beg,
                                              int64_t &end) {
   int kk = 0;
-  while (kk + 1 < a.nsp && c >= a.tile_start[kk + 1]) ++kk;
+  int64_t local;
+  if (c < a.rr_chunks) {
+    kk = (int)(c % a.nsp);
+    local = c / a.nsp;
+  } else {
+    const int64_t r = c - a.rr_chunks;
+    while (kk + 1 < a.nsp && r >= a.tail_start[kk + 1]) ++kk;
+    local = a.rr_each + (r - a.tail_start[kk]);
+  }
   const int isp = a.order[kk];
   const pb_species &s = a.sp[isp];
   const int64_t n = s.n_dev ? *s.n_dev : s.n;
-  beg = (c - a.tile_start[kk]) * kChunk;
+  beg = local * kChunk;
   end = beg + kChunk < n ? beg + kChunk : n;
   return isp;
 }
@@ -1147,6 +1159,7 @@ static int g_sm_count = 0;
 static int g_use_tma = -1;  // 0 ldg, 1 tma, 2 quad
 
 typedef void (*LdgFn)(LaunchArgs);
+static int g_interleave = -1;
 typedef void (*TmaFn)(LaunchArgs, int, int, int);
 static int g_stages = 0;
 static int g_ahead = -1;
@@ -1279,10 +1292,25 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
         order[j - 1] = tmp;
       }
     a.tile_start[0] = 0;
+    int64_t min_chunks = -1;
     for (int k = 0; k < a.nsp; ++k) {
       a.order[k] = order[k];
-      a.tile_start[k + 1] = a.tile_start[k] + (a.sp[order[k]].n + kChunk - 1) / kChunk;
+      const int64_t nk = (a.sp[order[k]].n + kChunk - 1) / kChunk;
+      a.tile_start[k + 1] = a.tile_start[k] + nk;
+      if (min_chunks < 0 || nk < min_chunks) min_chunks = nk;
     }
+    // Interleave the species' chunks (round-robin while every species has
+    // some): charged chunks are latency-heavier than neutral ones, and a mix
+    // keeps the memory system busy (PB_INTERLEAVE=0: species by species).
+    if (g_interleave < 0) {
+      const char *env = getenv("PB_INTERLEAVE");
+      g_interleave = env ? atoi(env) != 0 : 1;
+    }
+    a.rr_each = g_interleave ? min_chunks : 0;
+    a.rr_chunks = a.rr_each * a.nsp;
+    a.tail_start[0] = 0;
+    for (int k = 0; k < a.nsp; ++k)
+      a.tail_start[k + 1] = a.tail_start[k] + (a.tile_start[k + 1] - a.tile_start[k]) - a.rr_each;
     LdgFn fn = bc == PB_BC_PERIODIC
                    ? (boris ? k_push_quad<PB_BC_PERIODIC, true> : k_push_quad<PB_BC_PERIODIC, false>)
                    : (boris ? k_push_quad<PB_BC_ABSORBING, true> : k_push_quad<PB_BC_ABSORBING, false>);
