@@ -239,7 +239,7 @@ typedef struct pb_collide_params {
  * appended at e->n + t and ion->n + t with cell set, newborn_k[t] = event
  * index within the cell, newborn_per_cell[j] = pairs born in cell j.
  * counters (device u64[6]): elastic, excitation, ionization, suppressed,
- * newborns, overflow (must be zeroed by the caller). */
+ * newborns, overflow (zeroed by the call). */
 int pb_collide(const pb_species *e, const pb_species *neutral,
                const pb_species *ion, const int64_t *e_offs,
                const int64_t *e_counts, const int64_t *n_offs,
@@ -266,6 +266,15 @@ int pb_canonical_resort(const pb_species *src, const pb_species *dst,
                         const pb_canon *cv, const double *e_nodes, int64_t nc,
                         int particle_bc, int species_id, pb_status *status,
                         void *scratch, size_t scratch_bytes, void *stream);
+
+/* pb_canonical_resort for species 0..nsp-1 (cv[k], species id k) in one
+ * call, then the new live counts (offs[nc] of each) into the host array
+ * n_new[nsp].  Synchronises the stream. */
+int pb_canonical_step(const pb_species *src, const pb_species *dst,
+                      const pb_canon *cv, int nsp, const double *e_nodes,
+                      int64_t nc, int particle_bc, pb_status *status,
+                      void *scratch, size_t scratch_bytes, int64_t *n_new,
+                      void *stream);
 
 /* Weighted partials + stitched rho from fp64 per-species partials
  * raw[ndep][2][nc] (L then R, as pb_deposit_partials produces them):

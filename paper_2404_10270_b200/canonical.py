@@ -136,7 +136,6 @@ class CanonicalEngine(Engine):
         self.cparams.step_key = collide_step_key(self.cfg.seed, step)
         cap = min(se.cap - se.n, si.cap - si.n)
         with torch.cuda.stream(self.stream):
-            self.counters.zero_()
             pe, pn, pi = se.pb(), sn.pb(), si.pb()
             _lib.check(self.lib.pb_collide(
                 ctypes.byref(pe), ctypes.byref(pn), ctypes.byref(pi),
@@ -144,7 +143,7 @@ class CanonicalEngine(Engine):
                 self.counts[n].data_ptr(), self.nc, ctypes.byref(self.cparams),
                 self.nb_per_cell.data_ptr(), self.nb_k.data_ptr(), cap, self.counters.data_ptr(),
                 self._sh()), "pb_collide")
-        self.stream.synchronize()
+        self.stream.synchronize()  # the copy below runs on the caller's stream
         ctr = self.counters.cpu().numpy()
         if ctr[_CTR_OVERFLOW]:
             raise EngineError(f"collision pass overflow ({int(ctr[_CTR_OVERFLOW])} events): newborn "
@@ -154,29 +153,32 @@ class CanonicalEngine(Engine):
         return int(ctr[_CTR_NEWBORN])
 
     def push(self, e: torch.Tensor = None, newborns: int = 0):
-        """Push + transfer + canonical resort of every species."""
+        """Push + transfer + canonical resort of every species (one C call)."""
         if e is None:
             e = self.e
         roles = self.roles or (-1, -1, -1)
-        with torch.cuda.stream(self.stream):
-            for k, s in enumerate(self.sp):
-                tail = newborns if k in (roles[0], roles[2]) else 0
-                cv = _lib.PbCanon()
-                cv.n_old = s.n
-                cv.n_tail = tail
-                cv.offs = self.offs[k].data_ptr()
-                cv.counts = self.counts[k].data_ptr()
-                cv.newborn_per_cell = self.nb_per_cell.data_ptr() if tail else None
-                cv.newborn_k = self.nb_k.data_ptr() if tail else None
-                dst = s.spare()
-                a, b = s.pb(s.n + tail), dst.pb(s.n + tail)
-                _lib.check(self.lib.pb_canonical_resort(
-                    ctypes.byref(a), ctypes.byref(b), ctypes.byref(cv), e.data_ptr(), self.nc, self.bc, k,
-                    self.status.data_ptr(), self.canon_scratch.data_ptr(), self.canon_scratch.numel(),
-                    self._sh()), "pb_canonical_resort")
-                s.swap_with_spare()
-            news = torch.stack([o[self.nc] for o in self.offs]).cpu()
-        for s, nn in zip(self.sp, news.tolist()):
+        nsp = len(self.sp)
+        src = (_lib.PbSpecies * nsp)()
+        dst = (_lib.PbSpecies * nsp)()
+        cvs = (_lib.PbCanon * nsp)()
+        for k, s in enumerate(self.sp):
+            tail = newborns if k in (roles[0], roles[2]) else 0
+            cv = cvs[k]
+            cv.n_old = s.n
+            cv.n_tail = tail
+            cv.offs = self.offs[k].data_ptr()
+            cv.counts = self.counts[k].data_ptr()
+            cv.newborn_per_cell = self.nb_per_cell.data_ptr() if tail else None
+            cv.newborn_k = self.nb_k.data_ptr() if tail else None
+            src[k] = s.pb(s.n + tail)
+            dst[k] = s.spare().pb(s.n + tail)
+        news = (ctypes.c_int64 * nsp)()
+        _lib.check(self.lib.pb_canonical_step(
+            src, dst, cvs, nsp, e.data_ptr(), self.nc, self.bc, self.status.data_ptr(),
+            self.canon_scratch.data_ptr(), self.canon_scratch.numel(), news, self._sh()),
+            "pb_canonical_step")
+        for s, nn in zip(self.sp, news):
+            s.swap_with_spare()
             s.n = int(nn)
             if s.absorbing:
                 s.n_dev.fill_(s.n)

@@ -466,6 +466,8 @@ extern "C" int pb_collide(const pb_species *e, const pb_species *neutral, const 
   a.nc = nc;
   a.p = *params;
   a.ctr = (unsigned long long *)counters;
+  cudaError_t ze = cudaMemsetAsync(counters, 0, 6 * sizeof(uint64_t), (cudaStream_t)stream);
+  if (ze != cudaSuccess) return pb::cuda_status(ze, "cudaMemsetAsync");
   const int threads = 256;
   int64_t blocks = (nc + 7) / 8;
   if (blocks > 148 * 64) blocks = 148 * 64;
@@ -596,6 +598,33 @@ extern "C" int pb_canonical_resort(const pb_species *src, const pb_species *dst,
                                                        dst->cell, cv->counts);
   PB_CHECK_LAUNCH("k_canon_gather");
   return pb::offsets_from_counts(cv->counts, cv->offs, nc, scan_tmp, st);
+}
+
+// All species of a step in one call (one host round trip instead of one per
+// species): pb_canonical_resort for each, then the new live counts
+// (offs[nc] of every species) copied to the host array n_new; synchronises
+// the stream.
+extern "C" int pb_canonical_step(const pb_species *src, const pb_species *dst, const pb_canon *cv,
+                                 int nsp, const double *e_nodes, int64_t nc, int particle_bc,
+                                 pb_status *status, void *scratch, size_t scratch_bytes,
+                                 int64_t *n_new, void *stream) {
+  if (nsp < 0 || nsp > PB_MAX_SPECIES || (nsp > 0 && (!src || !dst || !cv || !n_new))) {
+    pb::set_error("pb_canonical_step: bad arguments");
+    return PB_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int k = 0; k < nsp; ++k) {
+    const int rc = pb_canonical_resort(&src[k], &dst[k], &cv[k], e_nodes, nc, particle_bc, k,
+                                       status, scratch, scratch_bytes, stream);
+    if (rc) return rc;
+  }
+  for (int k = 0; k < nsp; ++k) {
+    const cudaError_t e = cudaMemcpyAsync(&n_new[k], cv[k].offs + nc, sizeof(int64_t),
+                                          cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return pb::cuda_status(e, "cudaMemcpyAsync");
+  }
+  const cudaError_t e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? PB_OK : pb::cuda_status(e, "cudaStreamSynchronize");
 }
 
 // Weighted partials + stitch from per-species fp64 partials (the bitwise
