@@ -124,6 +124,15 @@ int pb_deposit_partials(const double *x, const int64_t *offs,
 int pb_gather(const double *nodes, const double *x, const int64_t *offs,
               const int64_t *counts, int64_t nc, double *out, void *stream);
 
+/* fused_move_aos / fused_move_table (_kernels.pyx:105-152): the same
+ * arithmetic on a row-major table (ncols >= 4, columns x, vx, vy, vz[, yp]);
+ * per cell j rows [starts[j], starts[j]+counts[j]).  A single cell's table
+ * (fused_move_table) is nc = 1 with accel = {aj, aj1}. */
+int pb_fused_move_aos(double *tab, int64_t ncols, const int64_t *starts,
+                      const int64_t *counts, int64_t nc,
+                      const double *accel_or_null, double fnstep, int has_yp,
+                      void *stream);
+
 /* ---- device-resident engine (flat SoA + cell index) ---------------------- */
 
 /* One mover step for `nsp` species, fused: gather E, kick (or Boris), drift,

@@ -78,6 +78,30 @@ void or_gather(const double *nodes, const double *x, const int64_t *offs,
   }
 }
 
+/* fused_move_aos, _kernels.pyx:128-152 (fused_move_table is nc = 1) */
+void or_fused_move_aos(double *tab, int64_t ncols, const int64_t *starts,
+                       const int64_t *counts, int64_t nc, const double *accel,
+                       double fnstep, int has_yp) {
+  for (int64_t j = 0; j < nc; ++j) {
+    double aj = 0.0, daj = 0.0;
+    if (accel) {
+      aj = accel[j];
+      daj = accel[j + 1] - aj;
+    }
+    for (int64_t i = starts[j]; i < starts[j] + counts[j]; ++i) {
+      double *r = tab + i * ncols;
+      double v = r[1];
+      if (accel) {
+        const double atemp = aj + r[0] * daj;
+        v = r[1] + atemp;
+        r[1] = v;
+      }
+      r[0] = r[0] + fnstep * v;
+      if (has_yp) r[4] = r[4] + fnstep * r[2];
+    }
+  }
+}
+
 /* ---- flat layout: one mover step ----------------------------------------- */
 
 enum { OR_DRIFT = 1, OR_KICK = 2, OR_BORIS = 3 };

@@ -87,6 +87,7 @@ _SIGS = {
     "pb_fused_move": (ctypes.c_int, [_p, _p, _p, _p, _p, _p, _p, _i64, _f64, _p]),
     "pb_deposit_partials": (ctypes.c_int, [_p, _p, _p, _i64, _p, _p, _p]),
     "pb_gather": (ctypes.c_int, [_p, _p, _p, _p, _i64, _p, _p]),
+    "pb_fused_move_aos": (ctypes.c_int, [_p, _i64, _p, _p, _i64, _p, _f64, ctypes.c_int, _p]),
     "pb_push_deposit": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int, _p,
                                        _i64, ctypes.c_int, _p, _p, _p]),
     "pb_deposit_only": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int,

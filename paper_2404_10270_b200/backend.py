@@ -131,3 +131,53 @@ def fused_move(accel_nodes, x, vx, vy, yp, offs, counts, fnstep):
                                  _ptr(cd), nc, float(fnstep), _stream()), "fused_move")
     st.finish()
     return None
+
+
+def _table(tab, has_yp):
+    """Stage a (n, ncols) float64 C-contiguous table (numpy or CUDA tensor)."""
+    if isinstance(tab, torch.Tensor):
+        if not tab.is_cuda or tab.dtype != torch.float64 or not tab.is_contiguous() or tab.dim() != 2:
+            raise ValueError("tab: expected a contiguous 2-D CUDA float64 tensor")
+        return tab, None
+    if not isinstance(tab, np.ndarray):
+        raise TypeError("tab: expected a numpy array or CUDA tensor")
+    if tab.dtype != np.float64:
+        raise ValueError(f"Buffer dtype mismatch for tab: expected float64, got {tab.dtype}")
+    if tab.ndim != 2 or not tab.flags.c_contiguous:
+        raise ValueError("tab: ndarray is not C-contiguous 2-D")
+    if tab.shape[1] < (5 if has_yp else 4):
+        raise ValueError("tab: needs columns x, vx, vy, vz[, yp]")
+    return torch.from_numpy(tab).to(_dev()), tab
+
+
+def fused_move_aos(tab, starts, counts, accel_nodes, fnstep, has_accel, has_yp):
+    """fused_move over a cell-major array-of-structs table (columns x, vx,
+    vy, vz[, yp]) in place (_kernels.pyx:128-152)."""
+    lib = _lib.load()
+    t, host = _table(tab, has_yp)
+    st = _Stage()
+    sd = st.put(starts, np.int64, "starts")
+    cd = st.put(counts, np.int64, "counts")
+    ad = st.put(accel_nodes, np.float64, "accel_nodes") if has_accel else None
+    nc = int(cd.shape[0])
+    if ad is not None and int(ad.shape[0]) < nc + 1:
+        raise ValueError("accel_nodes must have len(counts)+1 entries")
+    _lib.check(lib.pb_fused_move_aos(_ptr(t), int(t.shape[1]), _ptr(sd), _ptr(cd), nc, _ptr(ad),
+                                     float(fnstep), int(bool(has_yp)), _stream()), "fused_move_aos")
+    st.finish()
+    if host is not None:
+        host[...] = t.cpu().numpy()
+    return None
+
+
+def fused_move_table(tab, aj, aj1, fnstep, has_accel, has_yp):
+    """fused_move over one cell's table with node accelerations aj, aj1
+    (_kernels.pyx:105-125)."""
+    n = int(tab.shape[0])
+    if n == 0:
+        return None
+    dev = _dev()
+    starts = torch.zeros(1, dtype=torch.int64, device=dev)
+    counts = torch.full((1,), n, dtype=torch.int64, device=dev)
+    accel = torch.tensor([float(aj), float(aj1)], dtype=torch.float64, device=dev)
+    return fused_move_aos(tab, starts, counts, accel, fnstep, has_accel, has_yp)

@@ -20,3 +20,5 @@ BACKEND = _cuda.BACKEND_NAME
 deposit_partials = _cuda.deposit_partials
 gather = _cuda.gather
 fused_move = _cuda.fused_move
+fused_move_table = _cuda.fused_move_table
+fused_move_aos = _cuda.fused_move_aos

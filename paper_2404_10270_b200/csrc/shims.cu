@@ -108,6 +108,38 @@ static unsigned shim_grid(int64_t nc) {
   return (unsigned)blocks;
 }
 
+// fused_move_aos / fused_move_table (pkg/src/picmc/backends/_kernels.pyx:105-152):
+// the same arithmetic on a row-major table with columns x, vx, vy, vz[, yp].
+__global__ void k_fused_move_aos(double *tab, int64_t ncols, const int64_t *__restrict__ starts,
+                                 const int64_t *__restrict__ counts, int64_t nc,
+                                 const double *__restrict__ accel, double fnstep, int has_yp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int64_t nw = (int64_t)gridDim.x * kWarps;
+  for (int64_t j = w0; j < nc; j += nw) {
+    const int64_t base = starts[j];
+    const int64_t cnt = counts[j];
+    double aj = 0.0, daj = 0.0;
+    if (accel) {
+      aj = accel[j];
+      daj = __dsub_rn(accel[j + 1], aj);
+    }
+    for (int64_t i = lane; i < cnt; i += 32) {
+      double *r = tab + (base + i) * ncols;
+      double v;
+      if (accel) {
+        const double atemp = __dadd_rn(aj, __dmul_rn(r[0], daj));
+        v = __dadd_rn(r[1], atemp);
+        r[1] = v;
+      } else {
+        v = r[1];
+      }
+      r[0] = __dadd_rn(r[0], __dmul_rn(fnstep, v));
+      if (has_yp) r[4] = __dadd_rn(r[4], __dmul_rn(fnstep, r[2]));
+    }
+  }
+}
+
 }  // namespace pb
 
 extern "C" int pb_fused_move(const double *accel_or_null, double *x,
@@ -180,5 +212,21 @@ extern "C" int pb_gather(const double *nodes, const double *x,
   cudaError_t le = cudaGetLastError();
   cudaFreeAsync(buf, st);
   if (le != cudaSuccess) return pb::cuda_status(le, "k_gather");
+  return PB_OK;
+}
+
+extern "C" int pb_fused_move_aos(double *tab, int64_t ncols, const int64_t *starts,
+                                 const int64_t *counts, int64_t nc, const double *accel_or_null,
+                                 double fnstep, int has_yp, void *stream) {
+  if (nc < 0 || (nc > 0 && (!tab || !starts || !counts)) || ncols < (has_yp ? 5 : 4)) {
+    pb::set_error("pb_fused_move_aos: bad arguments (ncols=%lld)", (long long)ncols);
+    return PB_ERR_INVALID;
+  }
+  if (nc == 0) return PB_OK;
+  int64_t blocks = (nc + pb::kWarps - 1) / pb::kWarps;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  pb::k_fused_move_aos<<<(unsigned)blocks, pb::kShimThreads, 0, (cudaStream_t)stream>>>(
+      tab, ncols, starts, counts, nc, accel_or_null, fnstep, has_yp);
+  PB_CHECK_LAUNCH("k_fused_move_aos");
   return PB_OK;
 }

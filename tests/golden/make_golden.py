@@ -81,6 +81,16 @@ def gen_backend(picmc):
                 out[f"s{seed}_move_a{wa}y{wy}_vx"] = a[1]
                 if wy:
                     out[f"s{seed}_move_a{wa}y{wy}_yp"] = a[3]
+        # layout-study kernels (_kernels.pyx:105-152) on the same particles
+        tab = np.stack([x, vx, vy, np.zeros_like(x), yp], axis=1).copy()
+        for wa in (0, 1):
+            for wy in (0, 1):
+                t = tab.copy()
+                k.fused_move_aos(t, offs, counts, accel, 3.0, bool(wa), bool(wy))
+                out[f"s{seed}_aos_a{wa}y{wy}"] = t
+        t = tab[: int(counts[0])].copy()
+        k.fused_move_table(t, 0.3, -0.2, 2.0, True, True)
+        out[f"s{seed}_table"] = t
     np.savez_compressed(os.path.join(HERE, "backend_kernels.npz"), **out)
 
 

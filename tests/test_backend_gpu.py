@@ -113,3 +113,30 @@ def test_dtype_and_contiguity_errors(cu):
         cu.deposit_partials(x.astype(np.float32), offs, counts)
     with pytest.raises(ValueError):
         cu.deposit_partials(x[::2], offs, counts)
+
+
+@pytest.mark.parametrize("seed", range(5))
+@pytest.mark.parametrize("with_accel", [True, False])
+@pytest.mark.parametrize("with_yp", [True, False])
+def test_fused_move_aos_and_table_bitwise(seed, with_accel, with_yp, cu):
+    """The layout-study kernels (_kernels.pyx:105-152) vs the reference's
+    compiled outputs (golden), numpy and CUDA-tensor inputs."""
+    import torch
+
+    from conftest import load_golden
+
+    g = load_golden("backend_kernels.npz")
+    x, vx, vy, yp, offs, counts = packed(seed)
+    accel = g[f"s{seed}_accel"]
+    tab = np.stack([x, vx, vy, np.zeros_like(x), yp], axis=1).copy()
+    t = tab.copy()
+    cu.fused_move_aos(t, offs, counts, accel, 3.0, with_accel, with_yp)
+    want = g[f"s{seed}_aos_a{int(with_accel)}y{int(with_yp)}"]
+    assert bits_equal(t.ravel(), want.ravel())
+    td = torch.from_numpy(tab.copy()).cuda()
+    cu.fused_move_aos(td, torch.from_numpy(offs).cuda(), torch.from_numpy(counts).cuda(),
+                      torch.from_numpy(accel).cuda(), 3.0, with_accel, with_yp)
+    assert bits_equal(td.cpu().numpy().ravel(), want.ravel())
+    t = tab[: int(counts[0])].copy()
+    cu.fused_move_table(t, 0.3, -0.2, 2.0, True, True)
+    assert bits_equal(t.ravel(), g[f"s{seed}_table"].ravel())

@@ -218,3 +218,24 @@ def test_periodic_run_restatement_matches_reference_run():
         ref = {n: g[f"sp{k}_{n}"] for n in flats[k].fields()}
         assert np.array_equal(oracle.canonical(flats[k].cell, flats[k].fields()),
                               oracle.canonical(g[f"sp{k}_cell"], ref))
+
+
+def test_oracle_layout_kernels_match_reference():
+    """fused_move_aos / fused_move_table restatements vs the reference's
+    compiled kernels' outputs (golden)."""
+    from conftest import load_golden, packed
+    from oracle import oracle
+
+    g = load_golden("backend_kernels.npz")
+    for seed in range(5):
+        x, vx, vy, yp, offs, counts = packed(seed)
+        accel = g[f"s{seed}_accel"]
+        tab = np.stack([x, vx, vy, np.zeros_like(x), yp], axis=1).copy()
+        for wa in (0, 1):
+            for wy in (0, 1):
+                t = tab.copy()
+                oracle.fused_move_aos(t, offs, counts, accel, 3.0, bool(wa), bool(wy))
+                assert np.array_equal(t.view(np.uint64), g[f"s{seed}_aos_a{wa}y{wy}"].view(np.uint64))
+        t = tab[: int(counts[0])].copy()
+        oracle.fused_move_table(t, 0.3, -0.2, 2.0, True, True)
+        assert np.array_equal(t.view(np.uint64), g[f"s{seed}_table"].view(np.uint64))
