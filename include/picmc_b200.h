@@ -78,7 +78,19 @@ typedef struct pb_species {
   double kick_coef;         /* q dt^2/(m dx), velocity_kick_coef (mover.py:38-40) */
   double boris_t[3];        /* q B dt / (2 m)                             */
   double boris_s[3];        /* 2 t / (1 + |t|^2)                          */
+  /* Optional compressed cell index read by the production mover instead of
+   * `cell` (1 byte instead of 4 per charged particle): cell8[i] =
+   * cell[i] - chunk_base[i / PB_CELL8_CHUNK], or PB_CELL8_ESCAPE when that
+   * does not fit (then cell[i] is read).  `cell` stays authoritative and is
+   * written for every mover; NULL = not used.  Rebuild with pb_cell8_build
+   * after anything reorders a species. */
+  int8_t *cell8;
+  int32_t *chunk_base;
 } pb_species;
+
+#define PB_CELL8_CHUNK 2048
+#define PB_CELL8_ESCAPE (-128)
+#define PB_CELL8_MARGIN 32 /* chunk_base = first cell of the chunk - margin */
 
 /* Device-resident step status, read by the host at the step's sync point. */
 typedef struct pb_status {
@@ -144,6 +156,10 @@ int pb_fused_move_aos(double *tab, int64_t ncols, const int64_t *starts,
 int pb_push_deposit(const pb_species *sp, int nsp, const double *e_nodes,
                     int64_t nc, int particle_bc, uint64_t *bins,
                     pb_status *status, void *stream);
+
+/* Rebuild cell8 / chunk_base of a species from its cell array (slots
+ * [0, sp->n)). */
+int pb_cell8_build(const pb_species *sp, void *stream);
 
 /* Standalone fixed-point deposit of current positions (step-0 deposit and
  * inactive charged species). */

@@ -33,6 +33,7 @@ PB_FIELD_PERIODIC = 0
 PB_FIELD_DIRICHLET = 1
 
 PB_MAX_SPECIES = 8
+PB_CELL8_CHUNK = 2048
 PB_DEPOSIT_FRAC_BITS = 48
 
 _p = ctypes.c_void_p
@@ -47,6 +48,7 @@ class PbSpecies(ctypes.Structure):
         ("cell", _p), ("n_dev", _p), ("n", _i64), ("holes", _p),
         ("kind", _i32), ("deposit", _i32), ("fnstep", _f64),
         ("kick_coef", _f64), ("boris_t", _f64 * 3), ("boris_s", _f64 * 3),
+        ("cell8", _p), ("chunk_base", _p),
     ]
 
 
@@ -90,6 +92,7 @@ _SIGS = {
     "pb_fused_move_aos": (ctypes.c_int, [_p, _i64, _p, _p, _i64, _p, _f64, ctypes.c_int, _p]),
     "pb_push_deposit": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int, _p,
                                        _i64, ctypes.c_int, _p, _p, _p]),
+    "pb_cell8_build": (ctypes.c_int, [ctypes.POINTER(PbSpecies), _p]),
     "pb_deposit_only": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int,
                                        _i64, _p, _p, _p]),
     "pb_rho_epilogue": (ctypes.c_int, [_p, ctypes.POINTER(_f64), ctypes.c_int, _i64,

@@ -189,8 +189,14 @@ __device__ __forceinline__ void handle_pair(const LaunchArgs &a,
       }
       if (YP) YPp[i] = q.y0;
     }
-    if (m0) s.cell[i] = n0;
-    if (m1) s.cell[i + 1] = n1;
+    if (m0) {
+      s.cell[i] = n0;
+      if (s.cell8) s.cell8[i] = (int8_t)PB_CELL8_ESCAPE;
+    }
+    if (m1) {
+      s.cell[i + 1] = n1;
+      if (s.cell8) s.cell8[i + 1] = (int8_t)PB_CELL8_ESCAPE;
+    }
     t.moved += (int)m0 + (int)m1;
     if (BC == PB_BC_ABSORBING) {
       t.absorbed[0] += (int)(w0 == 0) + (int)(w1 == 0);
@@ -608,7 +614,10 @@ __device__ __forceinline__ void consume_tile_quads(const LaunchArgs &a, int isp,
     if (YP) st4(s.yp + i, y[0], y[1], y[2], y[3]);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      if (mv[k]) s.cell[i + k] = nn[k];
+      if (mv[k]) {
+        s.cell[i + k] = nn[k];
+        if (s.cell8) s.cell8[i + k] = (int8_t)PB_CELL8_ESCAPE;
+      }
       t.moved += (int)mv[k];
       if (cfl[k]) {
         const uint64_t key = ((uint64_t)sid << 56) | (uint64_t)(i + k);
@@ -912,8 +921,14 @@ template <int KIND, bool YP>
 struct Quad {
   double x[4], vx[4], vy[4], vz[4], y[4];
   int32_t c[4];
+  int32_t base;  // chunk_base of the quad's chunk (cell8 in use)
   int nv;
 };
+
+__device__ __forceinline__ int8_t cell8_encode(int32_t cell, int32_t base) {
+  const int32_t d = cell - base;
+  return (d > PB_CELL8_ESCAPE && d <= 127) ? (int8_t)d : (int8_t)PB_CELL8_ESCAPE;
+}
 
 template <int KIND, bool YP>
 __device__ __forceinline__ void quad_load(const pb_species &s, int64_t i, int64_t end,
@@ -926,6 +941,7 @@ __device__ __forceinline__ void quad_load(const pb_species &s, int64_t i, int64_
     q.x[k] = q.vx[k] = q.vy[k] = q.vz[k] = q.y[k] = 0.0;
     q.c[k] = -1;
   }
+  q.base = 0;
   if (q.nv == 4) {
     ld4(s.x + i, q.x[0], q.x[1], q.x[2], q.x[3]);
     ld4(s.vx + i, q.vx[0], q.vx[1], q.vx[2], q.vx[3]);
@@ -933,13 +949,25 @@ __device__ __forceinline__ void quad_load(const pb_species &s, int64_t i, int64_
     if (F::kVz) ld4(s.vz + i, q.vz[0], q.vz[1], q.vz[2], q.vz[3]);
     if (YP) ld4(s.yp + i, q.y[0], q.y[1], q.y[2], q.y[3]);
     if (kCell) {
-      const int4 cc = __ldcs(reinterpret_cast<const int4 *>(s.cell + i));
-      q.c[0] = cc.x;
-      q.c[1] = cc.y;
-      q.c[2] = cc.z;
-      q.c[3] = cc.w;
+      if (s.cell8) {
+        // 4 compressed cells in one 32-bit load; escapes read the full index
+        q.base = __ldg(s.chunk_base + i / PB_CELL8_CHUNK);
+        const int packed = __ldcs(reinterpret_cast<const int *>(s.cell8 + i));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int8_t o = (int8_t)((packed >> (8 * k)) & 0xff);
+          q.c[k] = o == PB_CELL8_ESCAPE ? s.cell[i + k] : q.base + (int32_t)o;
+        }
+      } else {
+        const int4 cc = __ldcs(reinterpret_cast<const int4 *>(s.cell + i));
+        q.c[0] = cc.x;
+        q.c[1] = cc.y;
+        q.c[2] = cc.z;
+        q.c[3] = cc.w;
+      }
     }
   } else {
+    if (kCell && s.cell8 && q.nv > 0) q.base = __ldg(s.chunk_base + i / PB_CELL8_CHUNK);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (k < q.nv) {
@@ -1010,7 +1038,11 @@ __device__ __forceinline__ void quad_process(const LaunchArgs &a, int isp, int64
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    if (mv[k]) s.cell[i + k] = nn[k];
+    if (mv[k]) {
+      s.cell[i + k] = nn[k];
+      if (kCell && s.cell8)
+        s.cell8[i + k] = nn[k] >= 0 ? cell8_encode(nn[k], q.base) : (int8_t)PB_CELL8_ESCAPE;
+    }
     t.moved += (int)mv[k];
     if (cfl[k]) {
       const uint64_t key = ((uint64_t)sid << 56) | (uint64_t)(i + k);

@@ -70,6 +70,26 @@ __global__ void k_cell_scatter(const __grid_constant__ ScatterArgs a) {
   }
 }
 
+__device__ __forceinline__ int8_t cell8_of(int32_t cell, int32_t base) {
+  const int32_t d = cell - base;
+  return (cell >= 0 && d > PB_CELL8_ESCAPE && d <= 127) ? (int8_t)d : (int8_t)PB_CELL8_ESCAPE;
+}
+
+// chunk_base = first cell of each PB_CELL8_CHUNK-slot chunk minus a margin
+// (cell-sorted chunks then fit in int8 offsets with room for drift);
+// cell8 = cell - chunk_base or the escape.
+__global__ void k_cell8_build(const int32_t *__restrict__ cell, int64_t n,
+                              int8_t *__restrict__ cell8, int32_t *__restrict__ chunk_base) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c0 = (i / PB_CELL8_CHUNK) * PB_CELL8_CHUNK;
+    const int32_t first = __ldg(cell + c0);
+    const int32_t base = (first >= 0 ? first : 0) - PB_CELL8_MARGIN;
+    if (i == c0) chunk_base[i / PB_CELL8_CHUNK] = base;
+    cell8[i] = cell8_of(cell[i], base);
+  }
+}
+
 static size_t scan_temp_bytes(int64_t nc) {
   size_t t = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, t, (const uint32_t *)nullptr, (uint32_t *)nullptr,
@@ -133,6 +153,7 @@ __global__ void __launch_bounds__(kCompactThreads)
     s.vz[h] = s.vz[src];
     if (s.yp) s.yp[h] = s.yp[src];
     s.cell[h] = s.cell[src];
+    if (s.cell8) s.cell8[h] = cell8_of(s.cell[src], s.chunk_base[h / PB_CELL8_CHUNK]);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -234,5 +255,17 @@ extern "C" int pb_compact(const pb_species *sp, int nsp, pb_status *status,
   a.st = status;
   pb::k_compact<<<a.nsp, pb::kCompactThreads, 0, (cudaStream_t)stream>>>(a);
   PB_CHECK_LAUNCH("k_compact");
+  return PB_OK;
+}
+
+extern "C" int pb_cell8_build(const pb_species *sp, void *stream) {
+  if (!sp || !sp->cell) {
+    pb::set_error("pb_cell8_build: NULL species/cell");
+    return PB_ERR_INVALID;
+  }
+  if (!sp->cell8 || !sp->chunk_base || sp->n <= 0) return PB_OK;
+  pb::k_cell8_build<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(sp->cell, sp->n, sp->cell8,
+                                                                sp->chunk_base);
+  PB_CHECK_LAUNCH("k_cell8_build");
   return PB_OK;
 }

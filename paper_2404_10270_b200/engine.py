@@ -20,6 +20,7 @@ replicated grid, so nothing migrates between GPUs.
 
 import ctypes
 import math
+import os
 import time
 from dataclasses import dataclass
 
@@ -92,6 +93,7 @@ class Engine:
     """One GPU's share of a run: its particle shard plus a grid replica."""
 
     supports_collisions = False  # CanonicalEngine (canonical.py) runs them
+    use_cell8 = os.environ.get("PB_CELL8", "1") != "0"
 
     def __init__(self, config, device=None, *, rank: int = 0, world: int = 1,
                  group=None, init: str = "host", check_every: int = 1):
@@ -139,10 +141,15 @@ class Engine:
                 self.coef_dep.append(spd.charge_c * macro_weight(config, isp) / self.grid.dx_m)
             kick = velocity_kick_coef(spd, config.consts, self.grid.dx_m) if spd.charged else 0.0
             boris = boris_coefficients(spd, config.consts, self.b_field) if kind == _lib.PB_KIND_BORIS else None
+            # The mover reads a 1-byte cell offset instead of the 4-byte index
+            # for charged species dense enough that a 2048-particle chunk spans
+            # well under 127 cells (pb_species.cell8).
+            cell8 = (self.use_cell8 and kind in (_lib.PB_KIND_KICK, _lib.PB_KIND_BORIS)
+                     and int(config.ppc0) >= 32)
             with torch.cuda.stream(self.stream):
                 self.sp.append(DeviceSpecies(spd, nloc, self.device, kind=kind, deposit=dep,
                                              kick_coef=kick, boris=boris, absorbing=self.absorbing,
-                                             cap=self._species_cap(isp, nloc)))
+                                             cap=self._species_cap(isp, nloc), cell8=cell8))
         self.ndep = ndep
         self._coef_c = (ctypes.c_double * max(ndep, 1))(*self.coef_dep)
         self.sort_periods = self._sort_periods(config)
@@ -238,9 +245,19 @@ class Engine:
         """The bin set holding the latest deposit (read by the next density())."""
         return self.bins_pp[self.cur]
 
+    def rebuild_cell8(self, which=None):
+        """Recompute the compressed cell index after a reorder or upload."""
+        with torch.cuda.stream(self.stream):
+            for k, s in enumerate(self.sp):
+                if s.cell8 is None or (which is not None and k not in which):
+                    continue
+                pbs = s.pb(s.live_count() if s.absorbing else None)
+                _lib.check(self.lib.pb_cell8_build(ctypes.byref(pbs), self._sh()), "pb_cell8_build")
+
     def deposit_current(self):
         """Fixed-point deposit of the current positions into the bins
         (the reference's step-start deposit, harness.py:148-160)."""
+        self.rebuild_cell8()
         arr, n = self._species()
         with torch.cuda.stream(self.stream):
             self.bins.zero_()
@@ -341,6 +358,9 @@ class Engine:
                                                     self.sort_scratch.data_ptr(), self.sort_scratch.numel(),
                                                     self._sh()), "pb_sort_by_cell")
                 s.swap_with_spare()
+                if s.cell8 is not None:
+                    pbs = s.pb(n)
+                    _lib.check(self.lib.pb_cell8_build(ctypes.byref(pbs), self._sh()), "pb_cell8_build")
             self._arr = None  # graphs are keyed by buffer addresses (_graph_key)
 
     def step(self, timed: bool = False, e_ext: torch.Tensor = None):

@@ -27,7 +27,8 @@ class DeviceSpecies:
     FIELDS = ("x", "vx", "vy", "vz")
 
     def __init__(self, sp, n: int, device, *, kind: int, deposit: int,
-                 kick_coef: float = 0.0, boris=None, absorbing: bool = False, cap: int = None):
+                 kick_coef: float = 0.0, boris=None, absorbing: bool = False, cap: int = None,
+                 cell8: bool = False):
         self.sp = sp
         self.name = sp.name
         self.device = device
@@ -46,6 +47,10 @@ class DeviceSpecies:
         if self.has_yp:
             self.arr["yp"] = torch.empty(alloc, dtype=F64, device=device)
         self.cell = torch.empty(alloc, dtype=torch.int32, device=device)
+        # compressed cell index for the production mover (pb_species.cell8)
+        self.cell8 = torch.empty(alloc, dtype=torch.int8, device=device) if cell8 else None
+        nchunk = (alloc + _lib.PB_CELL8_CHUNK - 1) // _lib.PB_CELL8_CHUNK
+        self.chunk_base = torch.empty(nchunk, dtype=torch.int32, device=device) if cell8 else None
         self.n_dev = torch.full((1,), self.n, dtype=torch.int64, device=device)
         self.holes = torch.empty(alloc if absorbing else 1, dtype=torch.int64, device=device)
         self._spare = None  # ping-pong buffers for the cell sort
@@ -92,6 +97,9 @@ class DeviceSpecies:
             for k in range(3):
                 s.boris_t[k] = t[k]
                 s.boris_s[k] = sv[k]
+        if self.cell8 is not None:
+            s.cell8 = self.cell8.data_ptr()
+            s.chunk_base = self.chunk_base.data_ptr()
         return s
 
     def spare(self) -> "DeviceSpecies":
@@ -101,6 +109,9 @@ class DeviceSpecies:
             other.__dict__.update(self.__dict__)
             other.arr = {k: torch.empty_like(v) for k, v in self.arr.items()}
             other.cell = torch.empty_like(self.cell)
+            if self.cell8 is not None:
+                other.cell8 = torch.empty_like(self.cell8)
+                other.chunk_base = torch.empty_like(self.chunk_base)
             other._spare = None
             self._spare = other
         return self._spare
@@ -109,6 +120,8 @@ class DeviceSpecies:
         sp = self._spare
         self.arr, sp.arr = sp.arr, self.arr
         self.cell, sp.cell = sp.cell, self.cell
+        self.cell8, sp.cell8 = sp.cell8, self.cell8
+        self.chunk_base, sp.chunk_base = sp.chunk_base, self.chunk_base
 
 
 def species_array(species: list, n_host=None):

@@ -82,15 +82,21 @@ def _compare_arrays(dev, ref):
 
 
 @pytest.mark.parametrize("with_field", [False, True])
-def test_push_deposit_bitwise_vs_oracle(cuda, with_field):
+@pytest.mark.parametrize("dense", [False, True])
+def test_push_deposit_bitwise_vs_oracle(cuda, with_field, dense):
+    """dense: 64 particles per cell over 300 cells, so charged species use
+    the 1-byte compressed cell index (pb_species.cell8) -- multi-cell jumps
+    across the periodic seam exercise its escapes."""
     import torch
 
     from oracle import oracle
     from paper_2404_10270_b200 import Engine
 
-    cfg = _mk_config()
+    cfg = _mk_config(nc=300, ppc0=64) if dense else _mk_config()
     eng = Engine(cfg, device=cuda, check_every=0)
-    flats = _random_flats(cfg, seed=3)
+    if dense:
+        assert all(s.cell8 is not None for s in eng.sp if s.deposit >= 0)
+    flats = _random_flats(cfg, seed=3, vscale=(18.0 if dense else 0.7))
     eng.upload(flats)
     rng = np.random.default_rng(11)
     for step in range(12):
@@ -159,15 +165,22 @@ def test_epilogue_matches_oracle_bitwise(cuda):
         assert bits_equal(eng.right.cpu().numpy(), right)
 
 
-def test_absorbing_walls_counts_and_survivors(cuda):
+@pytest.mark.parametrize("dense", [False, True])
+def test_absorbing_walls_counts_and_survivors(cuda, dense):
+    """dense: the compressed cell index is in use, so compaction must carry
+    it along with the particles it moves into the holes."""
     import torch
 
     from oracle import oracle
     from paper_2404_10270_b200 import Engine
 
-    cfg = _mk_config(particle_boundary="absorbing", boundary="dirichlet")
+    if dense:
+        cfg = _mk_config(nc=200, ppc0=48, particle_boundary="absorbing", boundary="dirichlet")
+    else:
+        cfg = _mk_config(particle_boundary="absorbing", boundary="dirichlet")
     eng = Engine(cfg, device=cuda, check_every=0)
-    flats = _random_flats(cfg, seed=7, vscale=2.5)
+    assert dense == any(s.cell8 is not None for s in eng.sp)
+    flats = _random_flats(cfg, seed=7, vscale=(9.0 if dense else 2.5))
     eng.upload(flats)
     live = [f for f in flats]
     total_abs = np.zeros((3, 2), dtype=np.int64)
