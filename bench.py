@@ -348,8 +348,10 @@ def run_ours(args, rank, world, local_rank):
     arr, nsp = eng._species()
     actual_bytes = 0.0
     for s in eng.sp:
-        actual_bytes += s.n * (36.0 if s.kind != 1 else (48.0 if s.has_yp else 24.0))
-    # (the probe streams the c2 byte mix: x, vx [, vy, yp] and cell per species)
+        cell_b = 1.0 if s.cell8 is not None else 4.0
+        actual_bytes += s.n * ((32.0 + cell_b) if s.kind != 1 else (48.0 if s.has_yp else 24.0))
+    # (the probe streams the c2 byte mix: x, vx [, vy, yp] and the cell index
+    # the mover reads -- cell8 where in use -- per species)
     torch.cuda.synchronize(dev)
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(2):
@@ -413,7 +415,8 @@ def run_ours(args, rank, world, local_rank):
                               "graphs_captured_in_timed_region": graphs_timed},
         "sol_probe": {"ms": sol_ms, "actual_bytes": actual_bytes, "gbs": actual_bytes / (sol_ms * 1e-3) / 1e9,
                       "mover_actual_gbs": actual_bytes / (push_ms * 1e-3) / 1e9,
-                      "note": "pb_stream_sol: same bytes (incl. cell index), trivial update, no deposit"},
+                      "note": "pb_stream_sol: the mover's bytes (incl. its cell index), trivial update, "
+                              "no deposit"},
     }
     return out, clk.summary()
 

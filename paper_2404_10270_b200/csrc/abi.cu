@@ -210,15 +210,18 @@ extern "C" int pb_density_step(uint64_t *bins, uint64_t *bins_next, uint64_t *co
 // achieved bandwidth is reported against the copy peak, not against this.
 namespace pb {
 __global__ void __launch_bounds__(256) k_stream_sol(double *x, double *vx, const double *vy,
-                                                    double *yp, const int32_t *cell, int64_t n,
-                                                    int write_v) {
+                                                    double *yp, const int32_t *cell,
+                                                    const int8_t *cell8, int64_t n, int write_v) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i + 3 < n; i += stride) {
     double a0, a1, a2, a3, b0, b1, b2, b3;
     asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a0), "=d"(a1), "=d"(a2), "=d"(a3) : "l"(x + i));
     asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(b0), "=d"(b1), "=d"(b2), "=d"(b3) : "l"(vx + i));
     int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
-    if (cell) {
+    if (cell8) {  // the mover's compressed cell index: 4 bytes per lane
+      const int p = __ldcs(reinterpret_cast<const int *>(cell8 + i));
+      c0 = p & 1; c1 = (p >> 8) & 1; c2 = (p >> 16) & 1; c3 = (p >> 24) & 1;
+    } else if (cell) {
       const int4 c = __ldcs(reinterpret_cast<const int4 *>(cell + i));
       c0 = c.x; c1 = c.y; c2 = c.z; c3 = c.w;
     }
@@ -245,7 +248,8 @@ extern "C" int pb_stream_sol(const pb_species *sp, int nsp, void *stream) {
     if (s.kind == PB_KIND_INACTIVE || s.n < 4) continue;
     const bool charged = s.kind != PB_KIND_DRIFT;
     pb::k_stream_sol<<<sms * 8, 256, 0, (cudaStream_t)stream>>>(
-        s.x, s.vx, s.vy, s.yp, charged ? s.cell : nullptr, s.n & ~(int64_t)3, charged ? 1 : 0);
+        s.x, s.vx, s.vy, s.yp, charged ? s.cell : nullptr, charged ? s.cell8 : nullptr,
+        s.n & ~(int64_t)3, charged ? 1 : 0);
   }
   PB_CHECK_LAUNCH("k_stream_sol");
   return PB_OK;
