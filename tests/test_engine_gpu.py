@@ -476,3 +476,35 @@ def test_run_pipelined_field_solve_absorbing(cuda):
     a.sync()
     b.sync()
     assert np.array_equal(a.absorbed, b.absorbed) and a.absorbed.sum() > 0
+
+
+@pytest.mark.parametrize("replay", [False, True])
+def test_field_split_matches_serial_cycle(cuda, replay):
+    """Field-solve steps with the neutral push overlapped with the field
+    pipeline (the multi-GPU default) give bitwise the serial cycle's
+    particles, rho and tallies, eager and graph-replayed."""
+    from oracle import oracle
+    from paper_2404_10270_b200 import Engine
+
+    cfg = _mk_config(nc=64, ppc0=24, field_solve=True, smoothing_passes=1)
+    flats = _random_flats(cfg, 21, vscale=0.4)
+    a = Engine(cfg, device=cuda, check_every=0)
+    b = Engine(cfg, device=cuda, check_every=0)
+    a.field_split, b.field_split = False, True
+    a.upload(flats)
+    b.upload(flats)
+    assert b._field_split()[0] and not a._field_split()[0]
+    for _ in range(9):
+        a.step()
+    if replay:
+        b.replay(9)
+    else:
+        for _ in range(9):
+            b.step()
+    a.sync()
+    b.sync()
+    assert bits_equal(a.rho.cpu().numpy(), b.rho.cpu().numpy())
+    assert bits_equal(a.e.cpu().numpy(), b.e.cpu().numpy())
+    assert np.array_equal(a.moved, b.moved)
+    for x, y in zip(a.download(), b.download()):
+        assert np.array_equal(oracle.canonical(x.cell, x.fields()), oracle.canonical(y.cell, y.fields()))
