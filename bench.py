@@ -246,7 +246,9 @@ def run_ours(args, rank, world, local_rank):
 
     from paper_2404_10270_b200 import Engine
 
-    dev = torch.device("cuda", local_rank)
+    # one GPU per rank; --dist-backend gloo lets several ranks share a GPU to
+    # exercise the multi-rank path where only one GPU is visible
+    dev = torch.device("cuda", local_rank % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     cfg, desc, scaling = workload_config(args.workload, world, args.sort_every)
     nc_total = cfg.grid.nc
@@ -433,6 +435,8 @@ def main():
     ap.add_argument("--sort-every", type=int, default=None,
                     help="base cell-sort period (default: 100 for c2, the TOML value otherwise)")
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: ranks may share one GPU (functional check of the N>1 path)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -460,7 +464,10 @@ def main():
     import torch.distributed as dist
 
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     if args.sort_every is None and args.workload == "c2":
         args.sort_every = 100
     out, clocks = run_ours(args, rank, world, local_rank)
