@@ -922,8 +922,21 @@ struct Quad {
   double x[4], vx[4], vy[4], vz[4], y[4];
   int32_t c[4];
   int32_t base;  // chunk_base of the quad's chunk (cell8 in use)
+  int packed;    // 4 cell8 bytes, not yet decoded when c[0] == kPackedCells
   int nv;
 };
+
+constexpr int32_t kPackedCells = -2;  // c[0] marker: cells still in q.packed
+
+template <int KIND, bool YP>
+__device__ __forceinline__ void quad_cells(const pb_species &s, int64_t i, Quad<KIND, YP> &q) {
+  if (q.c[0] != kPackedCells) return;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int8_t o = (int8_t)((q.packed >> (8 * k)) & 0xff);
+    q.c[k] = o == PB_CELL8_ESCAPE ? s.cell[i + k] : q.base + (int32_t)o;
+  }
+}
 
 __device__ __forceinline__ int8_t cell8_encode(int32_t cell, int32_t base) {
   const int32_t d = cell - base;
@@ -942,6 +955,7 @@ __device__ __forceinline__ void quad_load(const pb_species &s, int64_t i, int64_
     q.c[k] = -1;
   }
   q.base = 0;
+  q.packed = 0;
   if (q.nv == 4) {
     ld4(s.x + i, q.x[0], q.x[1], q.x[2], q.x[3]);
     ld4(s.vx + i, q.vx[0], q.vx[1], q.vx[2], q.vx[3]);
@@ -950,14 +964,11 @@ __device__ __forceinline__ void quad_load(const pb_species &s, int64_t i, int64_
     if (YP) ld4(s.yp + i, q.y[0], q.y[1], q.y[2], q.y[3]);
     if (kCell) {
       if (s.cell8) {
-        // 4 compressed cells in one 32-bit load; escapes read the full index
+        // 4 compressed cells in one 32-bit load, decoded at first use
+        // (quad_cells) so a prefetched slice does not stall here
         q.base = __ldg(s.chunk_base + i / PB_CELL8_CHUNK);
-        const int packed = __ldcs(reinterpret_cast<const int *>(s.cell8 + i));
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int8_t o = (int8_t)((packed >> (8 * k)) & 0xff);
-          q.c[k] = o == PB_CELL8_ESCAPE ? s.cell[i + k] : q.base + (int32_t)o;
-        }
+        q.packed = __ldcs(reinterpret_cast<const int *>(s.cell8 + i));
+        q.c[0] = kPackedCells;
       } else {
         const int4 cc = __ldcs(reinterpret_cast<const int4 *>(s.cell + i));
         q.c[0] = cc.x;
@@ -994,6 +1005,7 @@ __device__ __forceinline__ void quad_process(const LaunchArgs &a, int isp, int64
   constexpr bool kCell = KIND != PB_KIND_DRIFT;
   const int lane = (int)lane_id();
   const int nv = q.nv;
+  if (kCell) quad_cells<KIND, YP>(s, i, q);
   int32_t nn[4];
   int8_t wall[4];
   bool mv[4], cfl[4];
