@@ -508,3 +508,34 @@ def test_field_split_matches_serial_cycle(cuda, replay):
     assert np.array_equal(a.moved, b.moved)
     for x, y in zip(a.download(), b.download()):
         assert np.array_equal(oracle.canonical(x.cell, x.fields()), oracle.canonical(y.cell, y.fields()))
+
+
+def test_boris_exb_drift(cuda):
+    """Config-4 physics known answer: electrons starting at
+    rest in uniform E_x and B_z drift at v = E x B / B^2, i.e. vy averages to
+    -E_x/B_z (grid units: * dt/dx) over whole gyro-periods, with no net x
+    drift."""
+    import math
+
+    import torch
+
+    from paper_2404_10270_b200 import Engine, SpeciesDef
+    from paper_2404_10270_b200.core import ELECTRON_MASS, ELEMENTARY_CHARGE
+
+    bz, ex, dt, dx = 2.0, 1.0e4, 4e-14, 1e-5
+    cfg = _mk_config(nc=64, ppc0=8, species=[SpeciesDef("e", -ELEMENTARY_CHARGE, ELECTRON_MASS)],
+                     temperatures_ev=[0.0], densities_m3=[1e21], b_field_t=(0.0, 0.0, bz))
+    eng = Engine(cfg, device=cuda, check_every=0)
+    e = torch.full((eng.nc + 1,), ex, dtype=torch.float64, device=cuda)
+    period = 2.0 * math.pi * ELECTRON_MASS / (ELEMENTARY_CHARGE * bz) / dt  # steps per gyration
+    steps = int(round(10 * period))
+    vy_sum = torch.zeros(eng.sp[0].n, dtype=torch.float64, device=cuda)
+    for _ in range(steps):
+        eng.push(e)
+        vy_sum += eng.sp[0].arr["vy"][: eng.sp[0].n]
+    eng.sync()
+    vy_mean = float(vy_sum.mean()) / steps
+    want = -(ex / bz) * dt / dx
+    assert abs(vy_mean - want) <= 0.02 * abs(want), (vy_mean, want)
+    vx_mean = float(eng.sp[0].arr["vx"][: eng.sp[0].n].mean())
+    assert abs(vx_mean) <= 2.5 * abs(want)  # bounded gyration, no secular x motion
