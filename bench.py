@@ -375,8 +375,10 @@ def run_ours(args, rank, world, local_rank):
         launches_per_step += cfg.smoothing_passes + 2
     if eng.absorbing:
         launches_per_step += 1
-    # our kernels per sort: k_cell_count + k_cell_scatter (the scan is CUB's)
-    n_sorts = sum(args.steps // p for p in eng.sort_periods if p)
+    # our kernels per sort: k_cell_count + k_cell_scatter (+ k_cell8_build
+    # where the compressed cell index is kept); the scan is CUB's
+    n_sort_kernels = sum((args.steps // p) * (3 if s.cell8 is not None else 2)
+                         for p, s in zip(eng.sort_periods, eng.sp) if p)
     out = {
         "metric": METRIC,
         "value": value,
@@ -414,7 +416,7 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": nodes * 8,
                 "path": "Engine.run_pipelined(): per step E-field H2D from pinned memory + step + rho D2H "
                         "into pinned memory read by the host (one step late, overlapped); max(device, wall)"},
-        "gpu_launches": args.steps * launches_per_step + n_sorts * 2,
+        "gpu_launches": args.steps * launches_per_step + n_sort_kernels,
         "timing_windows_ms": {"steps_per_window": 200, "min": min(win_ms), "median": float(np.median(win_ms)),
                               "max": max(win_ms), "argmax": int(np.argmax(win_ms)),
                               "graphs_captured_in_timed_region": graphs_timed},
