@@ -205,3 +205,24 @@ def test_density_allreduce_world2_equals_single_rank(tmp_path):
             oracle.step_flat(1, 0, 40.0, 0.0, z, nc, f.x, f.vx, f.vy, f.vz, f.yp, f.cell)
         R, C = oracle.deposit_fixed(f.x, f.cell, nc)
         assert np.array_equal(got[d, 0], R) and np.array_equal(got[d, 1], C)
+
+
+def test_bench_reference_arm_json_line():
+    """`bench.py --impl reference` (the driver's reference arm) runs on the
+    host alone and prints one JSON line with the contract's keys."""
+    import json
+    import subprocess
+    import sys
+
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--steps", "5", "--warmup", "3", "--cpu-seconds", "1"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "particle-pushes/s"
+    for k in ("metric", "n_gpus", "steps", "warmup", "higher_is_better", "scaling", "dtype", "config"):
+        assert k in line
+    cb = line["cpu_baseline"]
+    assert cb["value"] == line["value"] and cb["cores"] >= 1 and cb["kind"] in ("reference", "port")
+    assert line["e2e"] == {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
