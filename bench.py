@@ -260,6 +260,11 @@ def run_ours(args, rank, world, local_rank):
 
     # Every CUDA graph the timed replay can need (bin parity x sort buffer
     # state) is captured before timing; periodic sorts run eagerly.
+    # one untimed sort of every species first: first-use costs (module
+    # loading, scratch allocation) stay out of the timed region; physics is
+    # order-free.  Then every graph the timed replay can need is captured.
+    eng.sort_by_cell()
+    eng.sync()
     eng.prepare_graphs(args.warmup + args.steps)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:

@@ -220,6 +220,16 @@ int pb_solve_poisson_scan(const double *rho, double *phi, int64_t nc,
 int pb_compute_efield(const double *phi, double *e, int64_t nc, double dx,
                       int field_bc, void *stream);
 
+/* smoothing (passes > 0: rho_s receives the smoothed density) + the scan
+ * Poisson solve + E in one cooperative launch with grid-wide syncs between
+ * the phases; bitwise pb_smooth_density + pb_solve_poisson_scan +
+ * pb_compute_efield (which it falls back to when the grid cannot be
+ * co-resident). */
+int pb_field_pipeline(const double *rho, double *rho_s, double *phi, double *e,
+                      int64_t nc, int passes, double dx, double eps0,
+                      int field_bc, double phi_left, double phi_right,
+                      void *scratch, void *stream);
+
 /* Roofline probe: streams the mover's exact read/write bytes per species with
  * a trivial update (no physics, no deposit).  Destroys particle state. */
 int pb_stream_sol(const pb_species *sp, int nsp, void *stream);

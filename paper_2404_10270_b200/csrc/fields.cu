@@ -7,28 +7,32 @@
 // reference's direct elimination (fields.py:138-202), restated operation for
 // operation -- including NumPy's pairwise summation inside np.mean -- on one
 // thread, so a given rho yields a bitwise-identical phi.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace pb {
 
 // ---- stencils ---------------------------------------------------------------
 // core = 0.25*roll(core,1) + 0.5*core + 0.25*roll(core,-1); out[nc] = out[0]
-__global__ void k_smooth_pass(const double *__restrict__ in,
-                              double *__restrict__ out, int64_t nc) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j > nc) return;
+__device__ __forceinline__ void smooth_node(const double *__restrict__ in, double *__restrict__ out,
+                                            int64_t nc, int64_t j) {
   const int64_t jj = j == nc ? 0 : j;
   const double a = in[jj == 0 ? nc - 1 : jj - 1];
   const double b = in[jj];
   const double c = in[jj == nc - 1 ? 0 : jj + 1];
-  out[j] = __dadd_rn(__dadd_rn(__dmul_rn(0.25, a), __dmul_rn(0.5, b)),
-                     __dmul_rn(0.25, c));
+  out[j] = __dadd_rn(__dadd_rn(__dmul_rn(0.25, a), __dmul_rn(0.5, b)), __dmul_rn(0.25, c));
 }
 
-__global__ void k_efield(const double *__restrict__ phi, double *__restrict__ e,
-                         int64_t nc, double two_dx, int field_bc) {
+__global__ void k_smooth_pass(const double *__restrict__ in,
+                              double *__restrict__ out, int64_t nc) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j > nc) return;
+  smooth_node(in, out, nc, j);
+}
+
+__device__ __forceinline__ void efield_node(const double *__restrict__ phi, double *__restrict__ e,
+                                            int64_t nc, double two_dx, int field_bc, int64_t j) {
   if (field_bc == PB_FIELD_PERIODIC) {
     const int64_t jj = j == nc ? 0 : j;  // e[nc] = e[0]
     const double l = phi[jj == 0 ? nc - 1 : jj - 1];
@@ -46,6 +50,13 @@ __global__ void k_efield(const double *__restrict__ phi, double *__restrict__ e,
   } else {
     e[j] = __ddiv_rn(__dsub_rn(phi[j - 1], phi[j + 1]), two_dx);
   }
+}
+
+__global__ void k_efield(const double *__restrict__ phi, double *__restrict__ e,
+                         int64_t nc, double two_dx, int field_bc) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > nc) return;
+  efield_node(phi, e, nc, two_dx, field_bc, j);
 }
 
 // ---- NumPy-exact reductions -------------------------------------------------
@@ -237,36 +248,35 @@ __device__ __forceinline__ double mb_rhs(const PoissonArgs &a, int64_t k, double
   return r;
 }
 
-// tile partial sums of src[0, len) -> part[blockIdx.x]
-__global__ void __launch_bounds__(kMbThreads) k_mb_tile_sum(const double *__restrict__ src,
-                                                            int64_t len, DD *part) {
-  __shared__ DD sm[kMbThreads];
-  const int64_t base = (int64_t)blockIdx.x * kMbTile + (int64_t)threadIdx.x * kMbPer;
+// ---- scan phases, one tile each (shared by the per-phase kernels and the
+// cooperative fused pipeline, so both give bitwise the same phi) ----------
+// tile partial sums of src[0, len) -> part[tile]
+__device__ void mb_tile_sum(const double *__restrict__ src, int64_t len, DD *part, int64_t tile,
+                            DD *sm) {
+  const int64_t base = tile * kMbTile + (int64_t)threadIdx.x * kMbPer;
   DD acc = dd_of(0.0);
   for (int j = 0; j < kMbPer; ++j)
     if (base + j < len) acc = dd_add(acc, dd_of(src[base + j]));
   const DD r = mb_block_reduce(acc, sm);
-  if (threadIdx.x == 0) part[blockIdx.x] = r;
+  if (threadIdx.x == 0) part[tile] = r;
 }
 
-__global__ void __launch_bounds__(kMbThreads) k_mb_fwd_part(const PoissonArgs a) {
-  __shared__ DD sm[kMbThreads];
+__device__ void mb_fwd_part(const PoissonArgs &a, int64_t tile, DD *sm) {
   const double mean = mb_mean(a, sm);
-  const int64_t base = (int64_t)blockIdx.x * kMbTile + (int64_t)threadIdx.x * kMbPer;
+  const int64_t base = tile * kMbTile + (int64_t)threadIdx.x * kMbPer;
   DD acc = dd_of(0.0);
   for (int j = 0; j < kMbPer; ++j) {
     const int64_t k = base + j;
     if (k < a.n) acc = dd_add(acc, dd_of(__dmul_rn((double)(k + 1), mb_rhs(a, k, mean))));
   }
   const DD r = mb_block_reduce(acc, sm);
-  if (threadIdx.x == 0) a.p1[blockIdx.x] = r;
+  if (threadIdx.x == 0) a.p1[tile] = r;
 }
 
-__global__ void __launch_bounds__(kMbThreads) k_mb_fwd_scan(const PoissonArgs a) {
-  __shared__ DD sm[kMbThreads];
+__device__ void mb_fwd_scan(const PoissonArgs &a, int64_t tile, DD *sm) {
   const double mean = mb_mean(a, sm);
-  const DD before = mb_sum_parts(a.p1, 0, blockIdx.x, sm);
-  const int64_t base = (int64_t)blockIdx.x * kMbTile + (int64_t)threadIdx.x * kMbPer;
+  const DD before = mb_sum_parts(a.p1, 0, tile, sm);
+  const int64_t base = tile * kMbTile + (int64_t)threadIdx.x * kMbPer;
   double v[kMbPer];
   DD loc = dd_of(0.0);
   for (int j = 0; j < kMbPer; ++j) {
@@ -285,13 +295,12 @@ __global__ void __launch_bounds__(kMbThreads) k_mb_fwd_scan(const PoissonArgs a)
     bsum = dd_add(bsum, dd_of(-__ddiv_rn(y, (double)(k + 2))));
   }
   const DD r = mb_block_reduce(bsum, sm);
-  if (threadIdx.x == 0) a.p2[blockIdx.x] = r;
+  if (threadIdx.x == 0) a.p2[tile] = r;
 }
 
-__global__ void __launch_bounds__(kMbThreads) k_mb_bwd_scan(const PoissonArgs a) {
-  __shared__ DD sm[kMbThreads];
-  const DD after = mb_sum_parts(a.p2, blockIdx.x + 1, a.nt, sm);
-  const int64_t base = (int64_t)blockIdx.x * kMbTile + (int64_t)threadIdx.x * kMbPer;
+__device__ void mb_bwd_scan(const PoissonArgs &a, int64_t tile, DD *sm) {
+  const DD after = mb_sum_parts(a.p2, tile + 1, a.nt, sm);
+  const int64_t base = tile * kMbTile + (int64_t)threadIdx.x * kMbPer;
   double u[kMbPer];
   DD loc = dd_of(0.0);
   for (int j = kMbPer - 1; j >= 0; --j) {
@@ -306,7 +315,7 @@ __global__ void __launch_bounds__(kMbThreads) k_mb_bwd_scan(const PoissonArgs a)
     off = dd_add(off, dd_of(u[j]));
     a.phi[k + 1] = __dmul_rn((double)(k + 1), __dadd_rn(off.hi, off.lo));
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (tile == 0 && threadIdx.x == 0) {
     if (a.field_bc == PB_FIELD_PERIODIC) {
       a.phi[0] = 0.0;
     } else {
@@ -316,27 +325,125 @@ __global__ void __launch_bounds__(kMbThreads) k_mb_bwd_scan(const PoissonArgs a)
   }
 }
 
-// periodic: phi[0..nc] -= mean(phi[:nc]); phi[nc] = phi[0]
-__global__ void __launch_bounds__(kMbThreads) k_mb_shift(const PoissonArgs a) {
-  __shared__ DD sm[kMbThreads];
+// periodic: phi[0..nc) -= mean(phi[:nc]) over nodes j = first, first+stride, ...
+__device__ void mb_shift(const PoissonArgs &a, int64_t first, int64_t stride, DD *sm) {
   const DD s = mb_sum_parts(a.p3, 0, a.ntc, sm);
   const double shift = __ddiv_rn(__dadd_rn(s.hi, s.lo), (double)a.nc);
-  for (int64_t j = (int64_t)blockIdx.x * kMbThreads + threadIdx.x; j <= a.nc;
-       j += (int64_t)gridDim.x * kMbThreads) {
-    if (j < a.nc) a.phi[j] = __dsub_rn(a.phi[j], shift);
-  }
+  for (int64_t j = first; j < a.nc; j += stride) a.phi[j] = __dsub_rn(a.phi[j], shift);
+}
+
+__global__ void __launch_bounds__(kMbThreads) k_mb_tile_sum(const double *__restrict__ src,
+                                                            int64_t len, DD *part) {
+  __shared__ DD sm[kMbThreads];
+  mb_tile_sum(src, len, part, blockIdx.x, sm);
+}
+
+__global__ void __launch_bounds__(kMbThreads) k_mb_fwd_part(const PoissonArgs a) {
+  __shared__ DD sm[kMbThreads];
+  mb_fwd_part(a, blockIdx.x, sm);
+}
+
+__global__ void __launch_bounds__(kMbThreads) k_mb_fwd_scan(const PoissonArgs a) {
+  __shared__ DD sm[kMbThreads];
+  mb_fwd_scan(a, blockIdx.x, sm);
+}
+
+__global__ void __launch_bounds__(kMbThreads) k_mb_bwd_scan(const PoissonArgs a) {
+  __shared__ DD sm[kMbThreads];
+  mb_bwd_scan(a, blockIdx.x, sm);
+}
+
+__global__ void __launch_bounds__(kMbThreads) k_mb_shift(const PoissonArgs a) {
+  __shared__ DD sm[kMbThreads];
+  mb_shift(a, (int64_t)blockIdx.x * kMbThreads + threadIdx.x, (int64_t)gridDim.x * kMbThreads, sm);
 }
 
 __global__ void k_mb_wrap(double *phi, int64_t nc) { phi[nc] = phi[0]; }
 
+// ---- cooperative fused field pipeline ----------------------------------------
+// smoothing passes -> scan Poisson -> E in ONE launch, grid-wide syncs between
+// the phases (same tile functions as the per-phase kernels: bitwise the same
+// rho_s / phi / E).  Replaces 5-9 tiny launches per field-solve step.
+struct CoopArgs {
+  PoissonArgs pa;
+  const double *rho;
+  double *out;  // smoothed density (passes > 0)
+  double *tmp;  // smoothing ping-pong
+  int passes;
+  double *e;
+  double two_dx;
+};
+
+__global__ void __launch_bounds__(kMbThreads) k_field_coop(const CoopArgs c) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ DD sm[kMbThreads];
+  const int64_t nc = c.pa.nc;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
+  const double *src = c.rho;
+  for (int p = 0; p < c.passes; ++p) {
+    double *dst = ((c.passes - 1 - p) % 2 == 0) ? c.out : c.tmp;
+    for (int64_t j = gtid; j <= nc; j += gsz) smooth_node(src, dst, nc, j);
+    grid.sync();
+    src = dst;
+  }
+  PoissonArgs a = c.pa;
+  a.rho = src;
+  const bool periodic = a.field_bc == PB_FIELD_PERIODIC;
+  if (periodic) {
+    for (int64_t t = blockIdx.x; t < a.ntc; t += gridDim.x) mb_tile_sum(src, nc, a.p0, t, sm);
+    grid.sync();
+  }
+  for (int64_t t = blockIdx.x; t < a.nt; t += gridDim.x) mb_fwd_part(a, t, sm);
+  grid.sync();
+  for (int64_t t = blockIdx.x; t < a.nt; t += gridDim.x) mb_fwd_scan(a, t, sm);
+  grid.sync();
+  for (int64_t t = blockIdx.x; t < a.nt; t += gridDim.x) mb_bwd_scan(a, t, sm);
+  grid.sync();
+  if (periodic) {
+    for (int64_t t = blockIdx.x; t < a.ntc; t += gridDim.x) mb_tile_sum(a.phi, nc, a.p3, t, sm);
+    grid.sync();
+    mb_shift(a, gtid, gsz, sm);
+    grid.sync();
+    if (gtid == 0) a.phi[nc] = a.phi[0];
+    grid.sync();
+  }
+  for (int64_t j = gtid; j <= nc; j += gsz) efield_node(a.phi, c.e, nc, c.two_dx, a.field_bc, j);
+}
+
 static unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+static PoissonArgs poisson_args(const double *rho, double *phi, int64_t nc, double dx, double eps0,
+                                int field_bc, double phi_left, double phi_right, void *scratch) {
+  PoissonArgs a;
+  a.rho = rho;
+  a.phi = phi;
+  a.nc = nc;
+  a.n = nc - 1;
+  a.nt = (int)((a.n + kMbTile - 1) / kMbTile);
+  a.ntc = (int)((nc + kMbTile - 1) / kMbTile);
+  a.scale = (dx * dx) / eps0;
+  a.phi_left = phi_left;
+  a.phi_right = phi_right;
+  a.field_bc = field_bc;
+  a.y = (double *)scratch;
+  const size_t off = ((size_t)(nc + 1) * sizeof(double) + 255) & ~(size_t)255;
+  DD *parts = (DD *)((char *)scratch + off);
+  const int ptile = a.ntc + 1;
+  a.p0 = parts;
+  a.p1 = parts + ptile;
+  a.p2 = parts + 2 * ptile;
+  a.p3 = parts + 3 * ptile;
+  return a;
+}
 
 }  // namespace pb
 
 extern "C" size_t pb_field_scratch_bytes(int64_t nc) {
   // smoothing ping-pong + the scan solve's y and DD tile partials
   const size_t tiles = (size_t)((nc + 1 + pb::kMbTile - 1) / pb::kMbTile) + 1;
-  return 3 * (size_t)(nc + 1) * sizeof(double) + 4 * tiles * sizeof(pb::DD) + 256;
+  return 4 * (size_t)(nc + 1) * sizeof(double) + 4 * tiles * sizeof(pb::DD) + 512;
 }
 
 extern "C" int pb_smooth_density(const double *rho, double *out, int64_t nc,
@@ -405,27 +512,8 @@ extern "C" int pb_solve_poisson_scan(const double *rho, double *phi, int64_t nc,
     pb::set_error("unknown boundary condition %d", field_bc);
     return PB_ERR_INVALID;
   }
-  const double scale = (dx * dx) / eps0;
   cudaStream_t st = (cudaStream_t)stream;
-  pb::PoissonArgs a;
-  a.rho = rho;
-  a.phi = phi;
-  a.nc = nc;
-  a.n = nc - 1;
-  a.nt = (int)((a.n + pb::kMbTile - 1) / pb::kMbTile);
-  a.ntc = (int)((nc + pb::kMbTile - 1) / pb::kMbTile);
-  a.scale = scale;
-  a.phi_left = phi_left;
-  a.phi_right = phi_right;
-  a.field_bc = field_bc;
-  a.y = (double *)scratch;
-  size_t off = ((size_t)(nc + 1) * sizeof(double) + 255) & ~(size_t)255;
-  pb::DD *parts = (pb::DD *)((char *)scratch + off);
-  const int ptile = a.ntc + 1;
-  a.p0 = parts;
-  a.p1 = parts + ptile;
-  a.p2 = parts + 2 * ptile;
-  a.p3 = parts + 3 * ptile;
+  pb::PoissonArgs a = pb::poisson_args(rho, phi, nc, dx, eps0, field_bc, phi_left, phi_right, scratch);
   if (field_bc == PB_FIELD_PERIODIC) {
     pb::k_mb_tile_sum<<<a.ntc, pb::kMbThreads, 0, st>>>(rho, nc, a.p0);
   }
@@ -451,4 +539,71 @@ extern "C" int pb_compute_efield(const double *phi, double *e, int64_t nc,
       phi, e, nc, 2.0 * dx, field_bc);
   PB_CHECK_LAUNCH("k_efield");
   return PB_OK;
+}
+
+// smoothing + scan Poisson + E in one cooperative launch (falls back to the
+// per-phase kernels when the grid cannot be co-resident).  rho_s receives the
+// smoothed density when passes > 0.  Same results as pb_smooth_density +
+// pb_solve_poisson_scan + pb_compute_efield, bit for bit.
+extern "C" int pb_field_pipeline(const double *rho, double *rho_s, double *phi, double *e,
+                                 int64_t nc, int passes, double dx, double eps0, int field_bc,
+                                 double phi_left, double phi_right, void *scratch, void *stream) {
+  if (nc < 3 || passes < 0 || !rho || !phi || !e || !scratch || (passes > 0 && !rho_s) ||
+      (field_bc != PB_FIELD_PERIODIC && field_bc != PB_FIELD_DIRICHLET)) {
+    pb::set_error("pb_field_pipeline: bad arguments (nc=%lld)", (long long)nc);
+    return PB_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  pb::CoopArgs c;
+  c.pa = pb::poisson_args(rho, phi, nc, dx, eps0, field_bc, phi_left, phi_right, scratch);
+  // smoothing ping-pong lives after the scan's scratch (y, then 4 partial sets)
+  const char *parts_end = (const char *)(c.pa.p3 + (c.pa.ntc + 1));
+  const size_t used = (size_t)(parts_end - (const char *)scratch);
+  double *tmp = (double *)((char *)scratch + ((used + 255) & ~(size_t)255));
+  c.rho = rho;
+  c.out = rho_s;
+  c.tmp = tmp;
+  c.passes = passes;
+  c.e = e;
+  c.two_dx = 2.0 * dx;
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
+    int dev = 0, sms = 0, bps = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pb::k_field_coop, pb::kMbThreads, 0);
+    max_blocks = sms * bps;
+  }
+  // at least one block per SM for the node-parallel stencil phases; idle
+  // blocks just pass the scan phases' grid syncs
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int grid = c.pa.ntc > c.pa.nt ? c.pa.ntc : c.pa.nt;
+  const int64_t node_blocks = (nc + 1 + pb::kMbThreads - 1) / pb::kMbThreads;
+  const int want = (int)(node_blocks < sms ? node_blocks : sms);
+  if (grid < want) grid = want;
+  if (grid > max_blocks) grid = max_blocks > 0 ? max_blocks : 1;
+  if (grid < 1) grid = 1;
+  const int tiles = c.pa.ntc > c.pa.nt ? c.pa.ntc : c.pa.nt;
+  if (tiles <= max_blocks) {
+    void *args[] = {&c};
+    const cudaError_t err = cudaLaunchCooperativeKernel((const void *)pb::k_field_coop, grid,
+                                                        pb::kMbThreads, args, 0, st);
+    if (err != cudaSuccess) return pb::cuda_status(err, "cudaLaunchCooperativeKernel");
+    return PB_OK;
+  }
+  int rc = PB_OK;
+  const double *src = rho;
+  if (passes > 0) {
+    rc = pb_smooth_density(rho, rho_s, nc, passes, tmp, stream);
+    if (rc) return rc;
+    src = rho_s;
+  }
+  rc = pb_solve_poisson_scan(src, phi, nc, dx, eps0, field_bc, phi_left, phi_right, scratch, stream);
+  if (rc) return rc;
+  return pb_compute_efield(phi, e, nc, dx, field_bc, stream);
 }

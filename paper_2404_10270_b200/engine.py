@@ -99,6 +99,10 @@ class Engine:
     # than the ~30 us field pipeline it hides); with N > 1 it also hides the
     # density allreduce.  PB_FIELD_SPLIT=1/0 forces it either way.
     field_split = None
+    # pb_field_pipeline (one cooperative launch for smoothing + Poisson + E)
+    # measured 0.8-6% slower than the per-phase kernels inside graphs
+    # (configs 4 and 3), so it is opt-in: PB_FUSED_FIELD=1
+    fused_field = os.environ.get("PB_FUSED_FIELD", "0") == "1"
 
     def __init__(self, config, device=None, *, rank: int = 0, world: int = 1,
                  group=None, init: str = "host", check_every: int = 1):
@@ -149,7 +153,11 @@ class Engine:
             # The mover reads a 1-byte cell offset instead of the 4-byte index
             # for charged species dense enough that a 2048-particle chunk spans
             # well under 127 cells (pb_species.cell8).
-            cell8 = (self.use_cell8 and kind in (_lib.PB_KIND_KICK, _lib.PB_KIND_BORIS)
+            # Measured: a win (-1.7% step) when neutral slices share the launch,
+            # a loss (+2-5%) in charged-only runs, whose latency-bound slices
+            # pay for the extra dependent base load + decode.
+            has_neutral = any(species_kind(x, self.b_field) == _lib.PB_KIND_DRIFT for x in config.species)
+            cell8 = (self.use_cell8 and has_neutral and kind in (_lib.PB_KIND_KICK, _lib.PB_KIND_BORIS)
                      and int(config.ppc0) >= 32)
             with torch.cuda.stream(self.stream):
                 self.sp.append(DeviceSpecies(spd, nloc, self.device, kind=kind, deposit=dep,
@@ -306,6 +314,13 @@ class Engine:
         sh = ctypes.c_void_p(st.cuda_stream)
         scr = self.field_scratch.data_ptr()
         with torch.cuda.stream(st):
+            if self.poisson == "scan" and self.fused_field:
+                # one cooperative launch: smoothing + scan Poisson + E
+                _lib.check(self.lib.pb_field_pipeline(
+                    rho.data_ptr(), self.rho_s.data_ptr(), self.phi.data_ptr(), self.e.data_ptr(),
+                    self.nc, int(cfg.smoothing_passes), self.grid.dx_m, cfg.consts.epsilon0,
+                    self.field_bc, cfg.phi_left, cfg.phi_right, scr, sh), "pb_field_pipeline")
+                return self.e
             src = rho
             if cfg.smoothing_passes > 0:
                 _lib.check(self.lib.pb_smooth_density(rho.data_ptr(), self.rho_s.data_ptr(), self.nc,
