@@ -1197,6 +1197,131 @@ __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
 }
 
 // ---------------------------------------------------------------------------
+// Charged-only launches (e.g. config 3: no neutral slices to interleave
+// with): a per-warp TMA ring.  Each warp streams its 128-particle slices
+// (x, vx, cell = 2.5 KB) through kRing shared-memory stages with
+// cp.async.bulk issued by one lane (mbarrier completion), claiming the next
+// chunk before the current one runs out, so kRing-1 slices stay in flight per
+// warp without holding registers.  In mixed launches the shared-memory
+// carve-out cost the neutral slices more than it gained, so k_push_quad
+// stays the default there.
+// ---------------------------------------------------------------------------
+#ifndef PB_RING_STAGES
+#define PB_RING_STAGES 3
+#endif
+constexpr int kRing = PB_RING_STAGES;
+constexpr int kSlice = 128;
+constexpr int kSliceBytes = kSlice * 8 * 2 + kSlice * 4;  // x, vx, cell
+
+struct SliceMeta {
+  int64_t base;
+  int32_t isp;
+  int32_t cnt;  // kSlice: staged by TMA; fewer: loaded directly
+};
+
+struct WarpRing {
+  unsigned char *buf;
+  uint64_t *bar;
+  SliceMeta *meta;
+};
+
+static constexpr int ring_smem_bytes() {
+  return kWarpsPerBlock * kRing * (kSliceBytes + (int)sizeof(uint64_t) + (int)sizeof(SliceMeta));
+}
+
+template <int BC>
+__global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
+    k_push_ring(const __grid_constant__ LaunchArgs a) {
+  extern __shared__ __align__(128) unsigned char r_smem[];
+  const int lane = (int)lane_id();
+  const int w = threadIdx.x >> 5;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(r_smem + (size_t)kWarpsPerBlock * kRing * kSliceBytes);
+  SliceMeta *metas = reinterpret_cast<SliceMeta *>(bars + kWarpsPerBlock * kRing);
+  const WarpRing r{r_smem + (size_t)w * kRing * kSliceBytes, bars + w * kRing, metas + w * kRing};
+  if (lane == 0) {
+    for (int k = 0; k < kRing; ++k) mbar_init(&r.bar[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int64_t total = a.tile_start[a.nsp];
+  Window win{nullptr, nullptr, 0, 0, nullptr, nullptr};
+  Tally t;
+  int cur = -1;
+  int64_t ibeg = 0, iend = 0;
+  int iisp = 0;
+  bool issuing = true;
+  uint32_t head = 0, tail = 0;
+  auto issue = [&]() {
+    while (ibeg >= iend) {  // current chunk exhausted (or empty): claim the next
+      const int64_t c = claim_chunk(a);
+      if (c >= total) {
+        issuing = false;
+        return;
+      }
+      iisp = chunk_species(a, c, ibeg, iend);
+    }
+    const int cnt = (int)(iend - ibeg < kSlice ? iend - ibeg : kSlice);
+    const uint32_t st = head % kRing;
+    if (lane == 0) {
+      r.meta[st].base = ibeg;
+      r.meta[st].isp = iisp;
+      r.meta[st].cnt = cnt;
+      if (cnt == kSlice) {
+        const pb_species &s = a.sp[iisp];
+        unsigned char *b = r.buf + st * kSliceBytes;
+        mbar_expect_tx(&r.bar[st], (uint32_t)kSliceBytes);
+        tma_load_1d(b, s.x + ibeg, kSlice * 8, &r.bar[st]);
+        tma_load_1d(b + kSlice * 8, s.vx + ibeg, kSlice * 8, &r.bar[st]);
+        tma_load_1d(b + kSlice * 16, s.cell + ibeg, kSlice * 4, &r.bar[st]);
+      } else {
+        mbar_arrive(&r.bar[st]);  // partial slice: loaded directly, phase still completes
+      }
+    }
+    ibeg += cnt;
+    ++head;
+  };
+  while (issuing && head - tail < (uint32_t)kRing) issue();
+  while (tail != head) {
+    const uint32_t st = tail % kRing;
+    mbar_wait(&r.bar[st], (tail / kRing) & 1u);
+    const SliceMeta m = r.meta[st];
+    const pb_species &s = a.sp[m.isp];
+    if (m.isp != cur) {
+      if (cur >= 0) flush_tally(a, a.id[cur], t, nullptr);
+      t = Tally();
+      cur = m.isp;
+      win.gR = a.bins + (size_t)s.deposit * 2 * (size_t)a.nc;
+      win.gC = win.gR + a.nc;
+    }
+    Quad<PB_KIND_KICK, false> q;
+    const int64_t i = m.base + 4 * lane;
+    if (m.cnt == kSlice) {
+      const unsigned char *b = r.buf + st * kSliceBytes;
+      const double2 *px = reinterpret_cast<const double2 *>(b) + 2 * lane;
+      const double2 *pv = reinterpret_cast<const double2 *>(b + kSlice * 8) + 2 * lane;
+      const int4 cc = reinterpret_cast<const int4 *>(b + kSlice * 16)[lane];
+      const double2 x01 = px[0], x23 = px[1], v01 = pv[0], v23 = pv[1];
+      q.x[0] = x01.x; q.x[1] = x01.y; q.x[2] = x23.x; q.x[3] = x23.y;
+      q.vx[0] = v01.x; q.vx[1] = v01.y; q.vx[2] = v23.x; q.vx[3] = v23.y;
+      q.c[0] = cc.x; q.c[1] = cc.y; q.c[2] = cc.z; q.c[3] = cc.w;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) q.vy[k] = q.vz[k] = q.y[k] = 0.0;
+      q.base = 0;
+      q.packed = 0;
+      q.nv = 4;
+    } else {
+      quad_load<PB_KIND_KICK, false>(s, i, m.base + m.cnt, q);
+    }
+    __syncwarp();  // every lane holds its slice in registers: the stage may be refilled
+    ++tail;
+    if (issuing) issue();
+    quad_process<PB_KIND_KICK, false, BC, true>(a, m.isp, i, q, win, t);
+  }
+  if (cur >= 0) flush_tally(a, a.id[cur], t, nullptr);
+  if (lane == 0) release_work_counter(a.st, (unsigned long long)gridDim.x * kWarpsPerBlock);
+}
+
+// ---------------------------------------------------------------------------
 // Host side.
 // ---------------------------------------------------------------------------
 static int g_sm_count = 0;
@@ -1204,6 +1329,7 @@ static int g_use_tma = -1;  // 0 ldg, 1 tma, 2 quad
 
 typedef void (*LdgFn)(LaunchArgs);
 static int g_interleave = -1;
+static const bool g_ring = !(getenv("PB_RING") && atoi(getenv("PB_RING")) == 0);
 typedef void (*TmaFn)(LaunchArgs, int, int, int);
 static int g_stages = 0;
 static int g_ahead = -1;
@@ -1358,6 +1484,21 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
     LdgFn fn = bc == PB_BC_PERIODIC
                    ? (boris ? k_push_quad<PB_BC_PERIODIC, true> : k_push_quad<PB_BC_PERIODIC, false>)
                    : (boris ? k_push_quad<PB_BC_ABSORBING, true> : k_push_quad<PB_BC_ABSORBING, false>);
+    // charged-only launches (every species KICK without yp, depositing, on
+    // the full int32 cell index): the per-warp TMA ring kernel
+    bool ring = g_ring;
+    for (int k = 0; k < a.nsp && ring; ++k)
+      ring = a.sp[k].kind == PB_KIND_KICK && !a.sp[k].yp && a.sp[k].deposit >= 0 && bins &&
+             !a.sp[k].cell8;
+    if (ring) {
+      LdgFn rfn = bc == PB_BC_PERIODIC ? k_push_ring<PB_BC_PERIODIC> : k_push_ring<PB_BC_ABSORBING>;
+      int bps = 0;
+      int rc = occupancy((const void *)rfn, kThreads, ring_smem_bytes(), &bps);
+      if (rc) return rc;
+      rfn<<<sms * bps, kThreads, ring_smem_bytes(), stream>>>(a);
+      PB_CHECK_LAUNCH("k_push_ring");
+      return PB_OK;
+    }
     int bps = 0;
     int rc = occupancy((const void *)fn, kThreads, 0, &bps);
     if (rc) return rc;
