@@ -304,6 +304,7 @@ def run_ours(args, rank, world, local_rank):
         eng.step(timed=True)
     eng.sync()
     push_ms = float(np.mean(eng.mover_ms()))
+    mover_kernel = eng.lib.pb_last_mover_kernel().decode()
     if world > 1:
         t = torch.tensor([ms, push_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -410,7 +411,7 @@ def run_ours(args, rank, world, local_rank):
         },
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "peak_source": peak_kind, "kernel": "k_push_quad",
+            "peak_source": peak_kind, "kernel": mover_kernel,
             "alg_bytes_per_launch": alg_bytes, "push_ms": push_ms,
             # committed ncu capture of the c2 bench launch (profiles/)
             "traffic": (None if traffic is None or args.workload != "c2"

@@ -103,8 +103,9 @@ typedef struct pb_status {
   int64_t overflow;                     /* deposit bins over capacity   */
   uint64_t tile_next;                   /* mover work counter (chunks claimed) */
   uint64_t tile_done;                   /* claimers finished; the last one
-                                           resets both words, so the counter
-                                           is zero again after every launch */
+                                           resets the counters, so they are
+                                           zero again after every launch */
+  uint64_t tile_next2;                  /* second work list (split mover)   */
 } pb_status;
 /* The caller resets *status before each pb_push_deposit: all zero except
  * cfl_index = UINT64_MAX (the engine copies a template). */
@@ -160,6 +161,10 @@ int pb_push_deposit(const pb_species *sp, int nsp, const double *e_nodes,
 /* Rebuild cell8 / chunk_base of a species from its cell array (slots
  * [0, sp->n)). */
 int pb_cell8_build(const pb_species *sp, void *stream);
+
+/* Name of the mover kernel the last pb_push_deposit / pb_deposit_only call
+ * launched (k_push_split, k_push_quad, k_push_ring, ...). */
+const char *pb_last_mover_kernel(void);
 
 /* Standalone fixed-point deposit of current positions (step-0 deposit and
  * inactive charged species). */

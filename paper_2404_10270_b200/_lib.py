@@ -60,6 +60,7 @@ class PbStatus(ctypes.Structure):
         ("n_holes", _i64 * PB_MAX_SPECIES),
         ("overflow", _i64),
         ("tile_next", ctypes.c_uint64), ("tile_done", ctypes.c_uint64),
+        ("tile_next2", ctypes.c_uint64),
     ]
 
 
@@ -93,6 +94,7 @@ _SIGS = {
     "pb_push_deposit": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int, _p,
                                        _i64, ctypes.c_int, _p, _p, _p]),
     "pb_cell8_build": (ctypes.c_int, [ctypes.POINTER(PbSpecies), _p]),
+    "pb_last_mover_kernel": (ctypes.c_char_p, []),
     "pb_deposit_only": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int,
                                        _i64, _p, _p, _p]),
     "pb_rho_epilogue": (ctypes.c_int, [_p, ctypes.POINTER(_f64), ctypes.c_int, _i64,
