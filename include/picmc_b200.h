@@ -307,6 +307,17 @@ int pb_canonical_resort(const pb_species *src, const pb_species *dst,
                         int particle_bc, int species_id, pb_status *status,
                         void *scratch, size_t scratch_bytes, void *stream);
 
+/* Multi-GPU canonical order, first half of a species' step: push +
+ * transfer in place and write int64 keys[0, n_old + n_tail) = (dest cell,
+ * moved, rank_offset + canonical rank) packed over rank_bits (all ones for
+ * vacated / absorbed slots).  The caller exchanges the particles whose dest
+ * cell another rank owns and orders its union by key. */
+int pb_canonical_keys(const pb_species *src, const pb_canon *cv,
+                      const double *e_nodes, int64_t nc, int particle_bc,
+                      int species_id, pb_status *status, int64_t rank_offset,
+                      int rank_bits, int64_t *keys, void *scratch,
+                      size_t scratch_bytes, void *stream);
+
 /* pb_canonical_resort for species 0..nsp-1 (cv[k], species id k) in one
  * call, then the new live counts (offs[nc] of each) into the host array
  * n_new[nsp].  Synchronises the stream. */

@@ -129,6 +129,9 @@ _SIGS = {
     "pb_canonical_resort": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.POINTER(PbSpecies),
                                            ctypes.POINTER(PbCanon), _p, _i64, ctypes.c_int,
                                            ctypes.c_int, _p, _p, ctypes.c_size_t, _p]),
+    "pb_canonical_keys": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.POINTER(PbCanon), _p, _i64,
+                                         ctypes.c_int, ctypes.c_int, _p, _i64, ctypes.c_int, _p, _p,
+                                         ctypes.c_size_t, _p]),
     "pb_canonical_step": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.POINTER(PbSpecies),
                                          ctypes.POINTER(PbCanon), ctypes.c_int, _p, _i64, ctypes.c_int,
                                          _p, _p, ctypes.c_size_t, ctypes.POINTER(_i64), _p]),

@@ -49,16 +49,16 @@ class CanonicalEngine(Engine):
 
     def __init__(self, config, device=None, *, rank: int = 0, world: int = 1, group=None,
                  init: str = "host", check_every: int = 1):
-        if world != 1:
-            raise ConfigError("the canonical-order engine runs on one GPU "
-                              "(collisions need every particle of a cell on one rank)")
+        # N > 1: every rank owns the particles of its cell range (the
+        # reference's worker decomposition, decomposition.py:66-79,177-229):
+        # collisions stay cell-local, movers that leave the range migrate.
         self.roles = None
         c = config.collisions
         if c is not None and c.enabled:
             self.roles = (config.species_index(c.electron), config.species_index(c.neutral),
                           config.species_index(c.ion))
         self._nloc = config.grid.nc * int(config.ppc0)
-        super().__init__(config, device, rank=0, world=1, group=group, init=init,
+        super().__init__(config, device, rank=rank, world=world, group=group, init=init,
                          check_every=check_every)
         nc = self.nc
         dev = self.device
@@ -122,6 +122,12 @@ class CanonicalEngine(Engine):
                 _lib.check(self.lib.pb_deposit_partials(s.arr["x"].data_ptr(), self.offs[k].data_ptr(),
                                                         self.counts[k].data_ptr(), nc, base, base + nc * 8,
                                                         sh), "pb_deposit_partials")
+            if self.world > 1:
+                # each cell's partials come from its owner alone (zeros
+                # elsewhere), so the sum is exact: bitwise the single domain
+                import torch.distributed as dist
+
+                dist.all_reduce(self.raw, group=self.group)
             _lib.check(self.lib.pb_rho_from_partials(self.raw.data_ptr(), self._coef_c, self.ndep, nc,
                                                      self.field_bc, self.left.data_ptr(),
                                                      self.right.data_ptr(), self.rho.data_ptr(), sh),
@@ -135,6 +141,12 @@ class CanonicalEngine(Engine):
         e, n, i = self.roles
         se, sn, si = self.sp[e], self.sp[n], self.sp[i]
         self.cparams.step_key = collide_step_key(self.cfg.seed, step)
+        if self.world > 1:  # newborn pairs <= live neutrals of this rank
+            se.ensure_capacity(se.n + sn.n)
+            si.ensure_capacity(si.n + sn.n)
+            if self.nb_k.numel() < max(sn.n, 1):
+                self.nb_k = torch.zeros(sn.n, dtype=torch.int32, device=self.device)
+            self._arr = None
         cap = min(se.cap - se.n, si.cap - si.n)
         with torch.cuda.stream(self.stream):
             pe, pn, pi = se.pb(), sn.pb(), si.pb()
@@ -149,14 +161,30 @@ class CanonicalEngine(Engine):
         if ctr[_CTR_OVERFLOW]:
             raise EngineError(f"collision pass overflow ({int(ctr[_CTR_OVERFLOW])} events): newborn "
                               "capacity or dt-guard depth exceeded")
-        self.tally_last = tuple(int(v) for v in ctr[:4])
-        self.tally_total += ctr[:4]
+        self._ionized_local = int(ctr[_CTR_IONIZATION])
+        tally = ctr[:4].copy()
+        if self.world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor(tally, dtype=torch.int64, device=self._coll_device())
+            dist.all_reduce(t, group=self.group)
+            tally = t.cpu().numpy()
+        self.tally_last = tuple(int(v) for v in tally)
+        self.tally_total += tally
         return int(ctr[_CTR_NEWBORN])
+
+    def _coll_device(self):
+        """Device for small collective tensors (gloo works on the host)."""
+        import torch.distributed as dist
+
+        return torch.device("cpu") if dist.get_backend(self.group) == "gloo" else self.device
 
     def push(self, e: torch.Tensor = None, newborns: int = 0):
         """Push + transfer + canonical resort of every species (one C call)."""
         if e is None:
             e = self.e
+        if self.world > 1:
+            return self._push_multirank(e, newborns)
         roles = self.roles or (-1, -1, -1)
         nsp = len(self.sp)
         src = (_lib.PbSpecies * nsp)()
@@ -184,6 +212,85 @@ class CanonicalEngine(Engine):
             if s.absorbing:
                 s.n_dev.fill_(s.n)
         self._arr = None
+
+    def _push_multirank(self, e, newborns):
+        """Canonical push across ranks: keys with a global canonical rank
+        (pb_canonical_keys), emigrants exchanged with all_to_all, the union
+        ordered by key -- per destination cell the survivors in slot order,
+        then newborns, then incomers by (src cell, src slot), exactly the
+        single-domain order (resort_collect / commit_incomers /
+        migrate_particles, pkg/src/picmc/mover.py:113-208,
+        decomposition.py:177-229)."""
+        import torch.distributed as dist
+
+        roles = self.roles or (-1, -1, -1)
+        cdev = self._coll_device()
+        hi = torch.tensor([h for _, h in self.partition.ranges], dtype=torch.int64, device=self.device)
+        for k, s in enumerate(self.sp):
+            tail = newborns if k in (roles[0], roles[2]) else 0
+            n_tot = s.n + tail
+            dead = getattr(self, "_ionized_local", 0) if k == roles[1] else 0
+            n_pre = torch.tensor([n_tot - dead], dtype=torch.int64, device=cdev)
+            allp = [torch.zeros_like(n_pre) for _ in range(self.world)]
+            dist.all_gather(allp, n_pre, group=self.group)
+            allp = [int(v.item()) for v in allp]
+            offset, total = sum(allp[: self.rank]), sum(allp)
+            rb = max(1, int(total).bit_length())
+            cv = _lib.PbCanon()
+            cv.n_old, cv.n_tail = s.n, tail
+            cv.offs, cv.counts = self.offs[k].data_ptr(), self.counts[k].data_ptr()
+            cv.newborn_per_cell = self.nb_per_cell.data_ptr() if tail else None
+            cv.newborn_k = self.nb_k.data_ptr() if tail else None
+            keys = torch.empty(max(n_tot, 1), dtype=torch.int64, device=self.device)
+            need = self.lib.pb_canonical_scratch_bytes(max(n_tot, 1), self.nc)
+            if self.canon_scratch.numel() < need:
+                self.canon_scratch = torch.empty(need, dtype=torch.uint8, device=self.device)
+            with torch.cuda.stream(self.stream):
+                a = s.pb(n_tot)
+                _lib.check(self.lib.pb_canonical_keys(
+                    ctypes.byref(a), ctypes.byref(cv), e.data_ptr(), self.nc, self.bc, k,
+                    self.status.data_ptr(), offset, rb, keys.data_ptr(), self.canon_scratch.data_ptr(),
+                    self.canon_scratch.numel(), self._sh()), "pb_canonical_keys")
+            self.stream.synchronize()
+            keys = keys[:n_tot]
+            names = list(s.arr)
+            cols = [s.arr[f][:n_tot] for f in names] + [keys.view(torch.float64)]
+            rows = torch.stack(cols, dim=1)
+            live = keys != -1
+            cell = torch.where(live, keys >> (rb + 1), torch.zeros_like(keys))
+            owner = torch.bucketize(cell, hi, right=True)
+            owner = torch.where(live, owner, torch.full_like(owner, self.world))  # dead -> dropped
+            order = torch.argsort(owner, stable=True)
+            send_counts = torch.bincount(owner, minlength=self.world + 1)[: self.world]
+            rows = rows[order][: int(send_counts.sum())]
+            sc = send_counts.to(cdev)
+            rc = torch.empty_like(sc)
+            dist.all_to_all_single(rc, sc, group=self.group)
+            sizes_in, sizes_out = sc.tolist(), rc.tolist()
+            out = torch.empty((sum(sizes_out), rows.shape[1]), dtype=torch.float64, device=cdev)
+            dist.all_to_all_single(out, rows.to(cdev), sizes_out, sizes_in, group=self.group)
+            got = out.to(self.device)
+            gkeys = got[:, -1].contiguous().view(torch.int64)
+            srt = torch.argsort(gkeys, stable=True)
+            got = got[srt]
+            m = int(got.shape[0])
+            s.ensure_capacity(m)
+            dst = s.spare()
+            for j, f in enumerate(names):
+                dst.arr[f][:m].copy_(got[:, j])
+            gk = got[:, -1].contiguous().view(torch.int64)
+            cells = (gk >> (rb + 1)).to(torch.int32)
+            dst.cell[:m].copy_(cells)
+            counts = torch.bincount(cells.to(torch.int64), minlength=self.nc)
+            self.counts[k].copy_(counts)
+            self.offs[k][0] = 0
+            torch.cumsum(counts, 0, out=self.offs[k][1:])
+            s.swap_with_spare()
+            s.n = m
+            if s.absorbing:
+                s.n_dev.fill_(s.n)
+        self._arr = None
+        torch.cuda.synchronize(self.device)
 
     def resort(self):
         pass  # the canonical resort is part of push()

@@ -255,6 +255,7 @@ __global__ void k_sum_counts(const int64_t *__restrict__ a, const int64_t *__res
 struct CanonPushArgs {
   pb_species s;
   int64_t n_old, n_tot;
+  int64_t rank_offset;  // global canonical position of this rank's first particle
   const int64_t *offs, *cnt_after, *offp;
   const int32_t *nb_k;
   const double *e;
@@ -277,8 +278,8 @@ __global__ void __launch_bounds__(256) k_canon_push(const __grid_constant__ Cano
       a.keys[i] = kDeadKey;
       continue;
     }
-    const int64_t rank = i < a.n_old ? a.offp[c] + (i - a.offs[c])
-                                     : a.offp[c] + a.cnt_after[c] + a.nb_k[i - a.n_old];
+    const int64_t rank = a.rank_offset + (i < a.n_old ? a.offp[c] + (i - a.offs[c])
+                                                      : a.offp[c] + a.cnt_after[c] + a.nb_k[i - a.n_old]);
     int32_t dest = c;
     bool mv = false;
     if (KIND != PB_KIND_INACTIVE) {
@@ -390,6 +391,47 @@ static int offsets_from_counts(const int64_t *counts, int64_t *offs, int64_t nc,
   size_t tb = scan_temp_bytes(nc);
   e = cub::DeviceScan::ExclusiveSum(cub_tmp, tb, ext, offs, (int)(nc + 1), st);
   if (e != cudaSuccess) return cuda_status(e, "DeviceScan::ExclusiveSum");
+  return PB_OK;
+}
+
+static int launch_canon_push(const pb_species *src, const pb_canon *cv, const double *e_nodes,
+                             int64_t nc, int particle_bc, int species_id, pb_status *status,
+                             int64_t rank_offset, int rank_bits, const int64_t *offp,
+                             uint64_t *keys, uint32_t *vals, cudaStream_t st) {
+  CanonPushArgs a;
+  a.s = *src;
+  a.n_old = cv->n_old;
+  a.n_tot = cv->n_old + cv->n_tail;
+  a.rank_offset = rank_offset;
+  a.offs = cv->offs;
+  a.cnt_after = cv->counts;
+  a.offp = offp;
+  a.nb_k = cv->newborn_k;
+  a.e = e_nodes;
+  a.nc = nc;
+  a.sid = species_id;
+  a.rank_bits = rank_bits;
+  a.st = status;
+  a.keys = keys;
+  a.vals = vals;
+  int64_t blocks = (a.n_tot + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  const bool abs = particle_bc == PB_BC_ABSORBING;
+#define PB_CANON(KIND)                                                              \
+  (abs ? k_canon_push<KIND, PB_BC_ABSORBING><<<(unsigned)blocks, 256, 0, st>>>(a) \
+       : k_canon_push<KIND, PB_BC_PERIODIC><<<(unsigned)blocks, 256, 0, st>>>(a))
+  switch (src->kind) {
+    case PB_KIND_INACTIVE: PB_CANON(PB_KIND_INACTIVE); break;
+    case PB_KIND_DRIFT: PB_CANON(PB_KIND_DRIFT); break;
+    case PB_KIND_KICK: PB_CANON(PB_KIND_KICK); break;
+    case PB_KIND_BORIS: PB_CANON(PB_KIND_BORIS); break;
+    default:
+      set_error("canonical push: unknown kind %d", src->kind);
+      return PB_ERR_INVALID;
+  }
+#undef PB_CANON
+  PB_CHECK_LAUNCH("k_canon_push");
   return PB_OK;
 }
 
@@ -544,38 +586,9 @@ extern "C" int pb_canonical_resort(const pb_species *src, const pb_species *dst,
     pb::set_error("pb_canonical_resort: key needs %d bits", key_bits);
     return PB_ERR_INVALID;
   }
-  pb::CanonPushArgs a;
-  a.s = *src;
-  a.n_old = cv->n_old;
-  a.n_tot = n_tot;
-  a.offs = cv->offs;
-  a.cnt_after = cv->counts;
-  a.offp = offp;
-  a.nb_k = cv->newborn_k;
-  a.e = e_nodes;
-  a.nc = nc;
-  a.sid = species_id;
-  a.rank_bits = rank_bits;
-  a.st = status;
-  a.keys = keys;
-  a.vals = vals;
-  int64_t blocks = (n_tot + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  const bool abs = particle_bc == PB_BC_ABSORBING;
-#define PB_CANON(KIND)                                                              \
-  (abs ? pb::k_canon_push<KIND, PB_BC_ABSORBING><<<(unsigned)blocks, 256, 0, st>>>(a) \
-       : pb::k_canon_push<KIND, PB_BC_PERIODIC><<<(unsigned)blocks, 256, 0, st>>>(a))
-  switch (src->kind) {
-    case PB_KIND_INACTIVE: PB_CANON(PB_KIND_INACTIVE); break;
-    case PB_KIND_DRIFT: PB_CANON(PB_KIND_DRIFT); break;
-    case PB_KIND_KICK: PB_CANON(PB_KIND_KICK); break;
-    case PB_KIND_BORIS: PB_CANON(PB_KIND_BORIS); break;
-    default:
-      pb::set_error("pb_canonical_resort: unknown kind %d", src->kind);
-      return PB_ERR_INVALID;
-  }
-#undef PB_CANON
-  PB_CHECK_LAUNCH("k_canon_push");
+  rc = pb::launch_canon_push(src, cv, e_nodes, nc, particle_bc, species_id, status, 0, rank_bits,
+                             offp, keys, vals, st);
+  if (rc) return rc;
   size_t tb = pb::sort_temp_bytes(n_tot);
   err = cub::DeviceRadixSort::SortPairs(sort_tmp, tb, keys, keys_s, vals, perm, (int)n_tot, 0,
                                         key_bits, st);
@@ -594,6 +607,8 @@ extern "C" int pb_canonical_resort(const pb_species *src, const pb_species *dst,
     g.dst[nf++] = dst->yp;
   }
   g.nf = nf;
+  int64_t blocks = (n_tot + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
   pb::k_canon_gather<<<(unsigned)blocks, 256, 0, st>>>(g, perm, keys_s, n_tot, rank_bits,
                                                        dst->cell, cv->counts);
   PB_CHECK_LAUNCH("k_canon_gather");
@@ -625,6 +640,46 @@ extern "C" int pb_canonical_step(const pb_species *src, const pb_species *dst, c
   }
   const cudaError_t e = cudaStreamSynchronize(st);
   return e == cudaSuccess ? PB_OK : pb::cuda_status(e, "cudaStreamSynchronize");
+}
+
+// Multi-rank canonical step, first half: push + transfer every particle of
+// the species in place and write its key (dest cell, moved, global canonical
+// rank = rank_offset + local rank) to keys[0, n_old + n_tail) -- all ones for
+// vacated / absorbed slots.  The caller exchanges emigrants between ranks and
+// orders the union by key (the same order pb_canonical_resort produces).
+extern "C" int pb_canonical_keys(const pb_species *src, const pb_canon *cv, const double *e_nodes,
+                                 int64_t nc, int particle_bc, int species_id, pb_status *status,
+                                 int64_t rank_offset, int rank_bits, int64_t *keys,
+                                 void *scratch, size_t scratch_bytes, void *stream) {
+  if (!src || !cv || !status || !keys || nc < 1 || species_id < 0 || species_id >= PB_MAX_SPECIES ||
+      rank_bits < 1 || rank_bits + pb::bits_for((uint64_t)(2 * nc)) > 63) {
+    pb::set_error("pb_canonical_keys: bad arguments");
+    return PB_ERR_INVALID;
+  }
+  const int64_t n_tot = cv->n_old + cv->n_tail;
+  if (n_tot == 0) return PB_OK;
+  if (!scratch || scratch_bytes < pb_canonical_scratch_bytes(n_tot, nc)) {
+    pb::set_error("pb_canonical_keys: scratch too small");
+    return PB_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  char *p = (char *)scratch;
+  p += 2 * pb::a256((size_t)n_tot * 8);
+  uint32_t *vals = (uint32_t *)p;
+  p += 2 * pb::a256((size_t)n_tot * 4);
+  int64_t *offp = (int64_t *)p;
+  p += pb::a256((size_t)(nc + 1) * 8);
+  int64_t *pre = (int64_t *)p;
+  p += pb::a256((size_t)nc * 8);
+  p += pb::a256(pb::sort_temp_bytes(n_tot));
+  char *scan_tmp = p;
+  pb::k_sum_counts<<<148, 256, 0, st>>>(cv->counts, cv->n_tail ? cv->newborn_per_cell : nullptr,
+                                        pre, nc);
+  PB_CHECK_LAUNCH("k_sum_counts");
+  int rc = pb::offsets_from_counts(pre, offp, nc, scan_tmp, st);
+  if (rc) return rc;
+  return pb::launch_canon_push(src, cv, e_nodes, nc, particle_bc, species_id, status, rank_offset,
+                               rank_bits, offp, (uint64_t *)keys, vals, st);
 }
 
 // Weighted partials + stitch from per-species fp64 partials (the bitwise

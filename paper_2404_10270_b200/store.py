@@ -102,6 +102,26 @@ class DeviceSpecies:
             s.chunk_base = self.chunk_base.data_ptr()
         return s
 
+    def ensure_capacity(self, need: int):
+        """Grow the arrays (keeping slots [0, n)) so `need` slots fit; the
+        ping-pong spare is dropped and recreated on demand."""
+        if need <= self.cap:
+            return
+        cap = max(int(need), int(self.cap * 1.25) + 1)
+        for f, t in list(self.arr.items()):
+            new = torch.empty(cap, dtype=t.dtype, device=t.device)
+            new[: self.n].copy_(t[: self.n])
+            self.arr[f] = new
+        cell = torch.empty(cap, dtype=self.cell.dtype, device=self.cell.device)
+        cell[: self.n].copy_(self.cell[: self.n])
+        self.cell = cell
+        if self.cell8 is not None:
+            raise RuntimeError("ensure_capacity: cell8 species are fixed-size")
+        if self.absorbing:
+            self.holes = torch.empty(cap, dtype=torch.int64, device=self.cell.device)
+        self.cap = cap
+        self._spare = None
+
     def spare(self) -> "DeviceSpecies":
         """Second buffer set, same shape, for the ping-pong cell sort."""
         if self._spare is None:
