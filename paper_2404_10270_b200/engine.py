@@ -94,6 +94,7 @@ class Engine:
 
     supports_collisions = False  # CanonicalEngine (canonical.py) runs them
     use_cell8 = os.environ.get("PB_CELL8", "1") != "0"
+    sort_ratio_cap = int(os.environ.get("PB_SORT_RATIO_CAP", "16"))
     # Field-solve steps: push neutral movers while the field pipeline runs.
     # Measured 2.4% slower on one GPU (a second launch's ramp/tail costs more
     # than the ~30 us field pipeline it hides); with N > 1 it also hides the
@@ -207,7 +208,8 @@ class Engine:
         """Per-species cell-sort period.  `sort_every` applies to the fastest
         species (largest thermal drift per step, nstep included); slower ones
         lose cell order proportionally more slowly and are sorted
-        proportionally less often (x64 at most).  0 = never."""
+        proportionally less often (x16 at most: measured +0.4% over x64, the
+        slow species otherwise lose order over a few thousand steps).  0 = never."""
         if not self.sort_every:
             return [0] * len(self.sp)
         drift = []
@@ -221,7 +223,7 @@ class Engine:
             if v <= 0.0:
                 out.append(0)
                 continue
-            out.append(self.sort_every * int(min(64, max(1, round(vmax / v)))))
+            out.append(self.sort_every * int(min(self.sort_ratio_cap, max(1, round(vmax / v)))))
         return out
 
     def _species_cap(self, isp: int, nloc: int) -> int:
