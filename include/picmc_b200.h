@@ -200,7 +200,8 @@ int pb_compact(const pb_species *sp, int nsp, pb_status *status,
 /* Periodic sort by cell: counting sort (cell histogram, exclusive scan,
  * scatter of every field) into the `dst` species buffers (ping-pong).  Order
  * within a cell is arbitrary (the engine's physics is order independent).
- * `scratch` needs pb_sort_scratch_bytes(n, nc) bytes. */
+ * With src->n_dev set (absorbing species) the live count is read on device
+ * and src->n is only its upper bound.  `scratch` needs pb_sort_scratch_bytes(n, nc) bytes. */
 size_t pb_sort_scratch_bytes(int64_t n, int64_t nc);
 int pb_sort_by_cell(const pb_species *src, const pb_species *dst, int64_t nc,
                     void *scratch, size_t scratch_bytes, void *stream);

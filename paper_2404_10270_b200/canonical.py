@@ -343,6 +343,21 @@ class CanonicalEngine(Engine):
         for _ in range(steps):
             self.step()
 
+    def prepare_pipe_graphs(self, with_input: bool, horizon: int = None, group: int = None):
+        pass  # no graphs: every step syncs for the newborn / migration counts
+
+    def run_pipelined(self, steps: int, e_source=None, on_result=None, group: int = None):
+        """Host-driven loop of the canonical engine: eager steps (each one
+        syncs anyway), every step's rho copied to the host and handed to
+        on_result(k, rho_host).  E is always computed on device here."""
+        if e_source is not None:
+            raise EngineError("the canonical-order engine takes no external E input")
+        for k in range(steps):
+            rho, _ = self.step()
+            if on_result is not None:
+                on_result(k, rho.cpu())
+        return steps
+
     def totals(self) -> list:
         return [s.n for s in self.sp]
 

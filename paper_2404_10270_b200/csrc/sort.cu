@@ -29,7 +29,17 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 
 // Per-cell counts; lanes holding the same cell add once per warp.
-__global__ void k_cell_count(const int32_t *__restrict__ cell, int64_t n, uint32_t *counts) {
+// n_dev (absorbing species): the live count on device, bounded by n, so the
+// sort needs no host read of it.
+__device__ __forceinline__ int64_t live_n(int64_t n, const int64_t *n_dev) {
+  if (!n_dev) return n;
+  const int64_t m = *n_dev;
+  return m < n ? m : n;
+}
+
+__global__ void k_cell_count(const int32_t *__restrict__ cell, int64_t n, const int64_t *n_dev,
+                             uint32_t *counts) {
+  n = live_n(n, n_dev);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x; b < n; b += stride) {
     const int64_t i = b + threadIdx.x;
@@ -48,14 +58,16 @@ struct ScatterArgs {
   int32_t *cell_out;
   uint32_t *cursor;
   int64_t n;
+  const int64_t *n_dev;
 };
 
 __global__ void k_cell_scatter(const __grid_constant__ ScatterArgs a) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const unsigned lane = threadIdx.x & 31;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x; b < a.n; b += stride) {
+  const int64_t n = live_n(a.n, a.n_dev);
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x; b < n; b += stride) {
     const int64_t i = b + threadIdx.x;
-    const int32_t c = i < a.n ? __ldg(a.cell + i) : -1;
+    const int32_t c = i < n ? __ldg(a.cell + i) : -1;
     const unsigned grp = __match_any_sync(0xffffffffu, c);
     const unsigned leader = (unsigned)(__ffs(grp) - 1);
     uint32_t base = 0;
@@ -195,7 +207,7 @@ extern "C" int pb_sort_by_cell(const pb_species *src, const pb_species *dst, int
   p += pb::align256((size_t)nc * sizeof(uint32_t));
   cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)nc * sizeof(uint32_t), st);
   if (e != cudaSuccess) return pb::cuda_status(e, "cudaMemsetAsync");
-  pb::k_cell_count<<<148 * 8, 256, 0, st>>>(src->cell, n, counts);
+  pb::k_cell_count<<<148 * 8, 256, 0, st>>>(src->cell, n, src->n_dev, counts);
   PB_CHECK_LAUNCH("k_cell_count");
   size_t tb = pb::scan_temp_bytes(nc);
   e = cub::DeviceScan::ExclusiveSum(p, tb, counts, cursor, (int)nc, st);
@@ -215,6 +227,7 @@ extern "C" int pb_sort_by_cell(const pb_species *src, const pb_species *dst, int
   a.cell_out = dst->cell;
   a.cursor = cursor;
   a.n = n;
+  a.n_dev = src->n_dev;
   pb::k_cell_scatter<<<148 * 8, 256, 0, st>>>(a);
   PB_CHECK_LAUNCH("k_cell_scatter");
   return PB_OK;

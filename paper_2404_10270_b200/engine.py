@@ -432,7 +432,7 @@ class Engine:
             for k, s in enumerate(self.sp):
                 if which is not None and k not in which:
                     continue
-                n = s.live_count()
+                n = s.n  # absorbing species: the kernels bound this by n_dev on device
                 if n <= 1:
                     continue
                 need = self.lib.pb_sort_scratch_bytes(n, self.nc)
@@ -504,123 +504,159 @@ class Engine:
             self.sync()
         return rho, e
 
-    def run_pipelined(self, steps: int, e_source=None, on_result=None):
-        """`steps` cycles driven from the host with the I/O overlapped.
+    PIPE_GROUP = int(os.environ.get("PB_PIPE_GROUP", "4"))
 
-        Per step k: the step's input E (a pinned host tensor from
-        e_source(k), field-free runs) is copied H2D on an input stream into
-        one of two device slots; the step runs on the engine stream (a
-        captured single-step graph when no sort is due); its rho is
-        snapshotted on device and copied D2H into one of two pinned host
-        buffers on a result stream.  The host launches step k+1 before it
-        waits for rho_k, then calls on_result(k, rho_host) -- every step's
-        result is read, one step late, while the GPU works on the next.
-        Returns the number of results delivered (== steps)."""
+    def _pipe_group(self, group):
+        g = self.PIPE_GROUP if group is None else int(group)
+        if g < 1:
+            raise EngineError(f"pipe group must be >= 1, got {g}")
+        return g
+
+    def _pipe_buffers(self, group: int):
+        """Two parities x `group` slots of device E inputs, device rho
+        snapshots and pinned host results."""
         dev, nodes = self.device, self.nc + 1
-        if not hasattr(self, "_pipe"):
+        P = getattr(self, "_pipe", None)
+        if P is None or P["e"].shape[1] < group:
             self._pipe = {
                 "h2d": torch.cuda.Stream(dev),  # inputs never queue behind results
                 "d2h": torch.cuda.Stream(dev),
-                "e": [torch.zeros(nodes, dtype=torch.float64, device=dev) for _ in range(2)],
-                "snap": [torch.zeros(nodes, dtype=torch.float64, device=dev) for _ in range(2)],
-                "host": [torch.zeros(nodes, dtype=torch.float64).pin_memory() for _ in range(2)],
+                "e": torch.zeros(2, group, nodes, dtype=torch.float64, device=dev),
+                "snap": torch.zeros(2, group, nodes, dtype=torch.float64, device=dev),
+                "host": torch.zeros(2, group, nodes, dtype=torch.float64).pin_memory(),
             }
+            # captured pipe graphs point at the old slots
+            self.graphs = {k: g for k, g in self.graphs.items() if k[0] != "pipe"}
+
+    def run_pipelined(self, steps: int, e_source=None, on_result=None, group: int = None):
+        """`steps` cycles driven from the host with the I/O overlapped.
+
+        Steps run in blocks of `group` (default PB_PIPE_GROUP, 4; single
+        steps around sorts).  Per block: each step's input E (a pinned host
+        tensor from e_source(k), field-free runs) is copied H2D on an input
+        stream into the block's device slots; the block runs on the engine
+        stream (one captured graph when no sort falls inside it); each step's
+        rho is snapshotted on device and the block's results are copied D2H
+        into pinned host memory on a result stream.  The host launches block
+        b+1 before it waits for block b's results, then calls
+        on_result(k, rho_host) for each of its steps -- every step's result
+        is read, one block late, while the GPU works on the next block.
+        Returns the number of results delivered (== steps)."""
+        G = self._pipe_group(group)
+        self._pipe_buffers(G)
         P = self._pipe
         h2d, d2h = P["h2d"], P["d2h"]
-        step_done = [None, None]
+        block_done = [None, None]
         d2h_done = [None, None]
+        pending = None  # (parity, first step, length) of the block not yet delivered
         delivered = 0
 
-        def deliver(k):
+        def deliver(blk):
             nonlocal delivered
-            slot = k % 2
-            d2h_done[slot].synchronize()
+            gp, k0, n = blk
+            d2h_done[gp].synchronize()
             if on_result is not None:
-                on_result(k, P["host"][slot])
-            delivered += 1
+                for j in range(n):
+                    on_result(k0 + j, P["host"][gp, j])
+            delivered += n
 
-        use_graphs = self.world == 1 and (e_source is None or not self.cfg.field_solve)
-        for k in range(steps):
-            slot = k % 2
-            e_dev = None
-            if e_source is not None:
-                if step_done[slot] is not None:
-                    h2d.wait_event(step_done[slot])  # step k-2 finished reading this slot
+        with_input = e_source is not None
+        use_graphs = self.world == 1 and (not with_input or not self.cfg.field_solve)
+        k, b = 0, 0
+        while k < steps:
+            gp = b % 2
+            n = 1
+            if use_graphs and G > 1 and k + G <= steps and not any(self._sort_due(j) for j in range(1, G + 1)):
+                n = G
+            if with_input:
+                if block_done[gp] is not None:
+                    h2d.wait_event(block_done[gp])  # block b-2 finished reading these slots
                 with torch.cuda.stream(h2d):
-                    P["e"][slot].copy_(e_source(k), non_blocking=True)
+                    for j in range(n):
+                        P["e"][gp, j].copy_(e_source(k + j), non_blocking=True)
                     ev_in = torch.cuda.Event()
                     ev_in.record(h2d)
                 self.stream.wait_event(ev_in)
-                e_dev = P["e"][slot]
-            if use_graphs and not self._sort_due(1):
-                # one captured step per (buffer state, input slot): density on a
-                # side stream overlapped with the push, then the rho snapshot
-                key = ("pipe", slot, e_dev is not None) + self._graph_key()
+            if use_graphs and not self._sort_due(n):
+                key = ("pipe", gp, n, with_input) + self._graph_key()
                 g = self.graphs.get(key)
                 if g is None:
                     self.sync()
                     self.stream.synchronize()
-                    g = self._capture_pipe_step(slot, e_dev)
+                    g = self._capture_pipe_steps(gp, n, with_input)
                     self.graphs[key] = g
                 if self._epi_prev is not None:
                     self.stream.wait_event(self._epi_prev)
                 with torch.cuda.stream(self.stream):
                     g.replay()
                 self._epi_prev = None
-                self.cur = 1 - self.cur  # the replayed push deposited into the other set
+                self.cur ^= n & 1  # each replayed push deposited into the other set
                 self._next_clear = False
-                self.step_index += 1
+                self.step_index += n
             else:
-                rho, _ = self.step(e_ext=e_dev)
+                rho, _ = self.step(e_ext=P["e"][gp, 0] if with_input else None)
                 self.stream.wait_stream(self._side)  # rho may come from the side stream
                 with torch.cuda.stream(self.stream):
-                    P["snap"][slot].copy_(rho, non_blocking=True)
+                    P["snap"][gp, 0].copy_(rho, non_blocking=True)
             with torch.cuda.stream(self.stream):
                 ev = torch.cuda.Event()
                 ev.record(self.stream)
-            step_done[slot] = ev
-            if k >= 1:
-                deliver(k - 1)  # host buffer (k-1)%2 is free again after this
+            block_done[gp] = ev
+            if pending is not None:
+                deliver(pending)  # host slots of block b-1's parity are free again after this
             d2h.wait_event(ev)
             with torch.cuda.stream(d2h):
-                P["host"][slot].copy_(P["snap"][slot], non_blocking=True)
+                P["host"][gp, :n].copy_(P["snap"][gp, :n], non_blocking=True)
                 d = torch.cuda.Event()
                 d.record(d2h)
-            d2h_done[slot] = d
-        if steps >= 1:
-            deliver(steps - 1)
+            d2h_done[gp] = d
+            pending = (gp, k, n)
+            k += n
+            b += 1
+        if pending is not None:
+            deliver(pending)
         return delivered
 
-    def _capture_pipe_step(self, slot, e_dev):
-        """One step as a graph: field-free runs put the density epilogue on
-        the side stream concurrent with the push; field-solve runs are serial
-        (density -> smooth -> Poisson -> E -> push).  Then rho is snapshotted
-        into the pipe slot."""
+    def _capture_pipe_steps(self, gp, n, with_input):
+        """`n` steps as one graph: field-free runs put each density epilogue
+        on the side stream concurrent with the push; field-solve runs are
+        serial (density -> smooth -> Poisson -> E -> push).  Step j's rho is
+        snapshotted into pipe slot (gp, j)."""
         g = torch.cuda.CUDAGraph()
         start = self.cur
         overlap = not self.cfg.field_solve
+        P = self._pipe
         with torch.cuda.graph(g, stream=self.stream):
-            if overlap:
-                self._side.wait_stream(self.stream)
-                rho = self.density(self._side, clear_next=False)
-                done = torch.cuda.Event()
-                done.record(self._side)
-                e = e_dev if e_dev is not None else self.e
-                self.push(e)
-            else:
-                rho, e = self._field_cycle()
-            if self.absorbing:
-                arr, n = self._species()
-                _lib.check(self.lib.pb_compact(arr, n, self.status.data_ptr(),
-                                               self.compact_scratch.data_ptr(),
-                                               self.compact_scratch.numel(), self._sh()), "pb_compact")
-            if overlap:
-                self.stream.wait_event(done)
-            elif self._field_split()[0]:
-                self.stream.wait_stream(self._side)
-            self._pipe["snap"][slot].copy_(rho, non_blocking=True)
+            prev = None
+            for j in range(n):
+                if overlap:
+                    self._side.wait_stream(self.stream)
+                    rho = self.density(self._side, clear_next=False)
+                    done = torch.cuda.Event()
+                    done.record(self._side)
+                    if prev is not None:
+                        self.stream.wait_event(prev)  # epilogue j-1 cleared this push's bin set
+                    prev = done
+                    self.push(P["e"][gp, j] if with_input else self.e)
+                else:
+                    rho, e = self._field_cycle()
+                if self.absorbing:
+                    arr, m = self._species()
+                    _lib.check(self.lib.pb_compact(arr, m, self.status.data_ptr(),
+                                                   self.compact_scratch.data_ptr(),
+                                                   self.compact_scratch.numel(), self._sh()), "pb_compact")
+                if overlap:
+                    snap_stream = self._side  # rho_j is final once epilogue j is done
+                else:
+                    if self._field_split()[0]:
+                        self.stream.wait_stream(self._side)
+                    snap_stream = self.stream
+                with torch.cuda.stream(snap_stream):
+                    P["snap"][gp, j].copy_(rho, non_blocking=True)
+            if overlap or self._field_split()[0]:
+                self.stream.wait_stream(self._side)  # join the forked side stream
         # capture advanced the host-side parity; replay() of this graph does
-        # the same, so restore it and let the caller account the step
+        # the same, so restore it and let the caller account the steps
         self.cur = start
         return g
 
@@ -675,6 +711,29 @@ class Engine:
         here are pointer bookkeeping only; timed replays then never capture."""
         if self.world > 1:
             return  # multi-GPU steps replay eagerly: no NCCL collectives inside graphs
+        self._each_buffer_state(horizon, lambda: None if self._graph_key() in self.graphs
+                                else self._capture())
+
+    def prepare_pipe_graphs(self, with_input: bool, horizon: int = None, group: int = None):
+        """The same for run_pipelined's graphs (single steps and `group`-step
+        blocks, both pipe parities; with_input: E comes from the pipe's device
+        slots)."""
+        if self.world > 1 or (with_input and self.cfg.field_solve):
+            return
+        group = self._pipe_group(group)
+        self._pipe_buffers(group)
+
+        def cap():
+            for gp in (0, 1):
+                for n in sorted({1, group}):
+                    key = ("pipe", gp, n, with_input) + self._graph_key()
+                    if key not in self.graphs:
+                        self.graphs[key] = self._capture_pipe_steps(gp, n, with_input)
+        self._each_buffer_state(horizon, cap)
+
+    def _each_buffer_state(self, horizon, fn):
+        """Call fn() once per (bin parity, ping-pong buffer of every species
+        sorted within `horizon` steps), restoring the current state after."""
         self.sync()
         self.stream.synchronize()
         clear0 = self._next_clear
@@ -689,8 +748,7 @@ class Engine:
             self._arr = None
             for cur in (0, 1):
                 self.cur = cur
-                if self._graph_key() not in self.graphs:
-                    self._capture()
+                fn()
             for k in flip:
                 self.sp[k].swap_with_spare()
             self._arr = None

@@ -226,3 +226,20 @@ def test_collision_statistics_binomial(cuda):
         assert tally.suppressed == 0
     assert abs(observed - expected) <= 4.0 * math.sqrt(variance)
     assert sp[0].n == nc * ne0 + observed and sp[1].n == observed and sp[2].n == nc * nn0 - observed
+
+
+def test_canonical_run_pipelined_matches_reference(cuda):
+    """CanonicalEngine.run_pipelined (the host-driven loop of the public
+    engine API) hands every step's rho to the host, bitwise the reference's."""
+    from paper_2404_10270_b200.canonical import CanonicalEngine
+
+    g = load_golden("run_collide_desk.npz")
+    cfg = cfg_from(g)
+    eng = CanonicalEngine(cfg, device=cuda, init="host")
+    got = {}
+    n = eng.run_pipelined(cfg.n_steps, on_result=lambda k, r: got.__setitem__(k, r.numpy().copy()))
+    assert n == cfg.n_steps
+    for k in range(cfg.n_steps):
+        assert bits_equal(got[k], g["rho"][k]), k
+    with pytest.raises(Exception):
+        eng.run_pipelined(1, e_source=lambda k: None)

@@ -420,11 +420,12 @@ def test_graph_replay_matches_eager_steps(cuda, case):
     assert len(b.graphs) >= 2
 
 
-@pytest.mark.parametrize("sort_every", [0, 3])
-def test_run_pipelined_matches_eager_steps(cuda, sort_every):
+@pytest.mark.parametrize("group", [1, 4])
+@pytest.mark.parametrize("sort_every", [0, 3, 7])
+def test_run_pipelined_matches_eager_steps(cuda, sort_every, group):
     """The overlapped host loop (H2D of each step's E, D2H of each step's rho
-    one step late) delivers exactly the eager steps' rho sequence and leaves
-    the same particles."""
+    one block late, blocks of `group` steps as one graph) delivers exactly
+    the eager steps' rho sequence and leaves the same particles."""
     import torch
 
     from paper_2404_10270_b200 import Engine
@@ -432,19 +433,21 @@ def test_run_pipelined_matches_eager_steps(cuda, sort_every):
     cfg = _mk_config(nc=48, ppc0=16, sort_every=sort_every)
     flats = _random_flats(cfg, 11, vscale=0.3)
     rng = np.random.default_rng(3)
-    es = [torch.from_numpy(2e4 * rng.standard_normal(cfg.grid.nc + 1)).pin_memory() for _ in range(7)]
+    steps = 19
+    es = [torch.from_numpy(2e4 * rng.standard_normal(cfg.grid.nc + 1)).pin_memory() for _ in range(steps)]
     a = Engine(cfg, device=cuda, check_every=0)
     b = Engine(cfg, device=cuda, check_every=0)
     a.upload(flats)
     b.upload(flats)
     want = []
-    for k in range(7):
+    for k in range(steps):
         rho, _ = a.step(e_ext=es[k].to(cuda))
         want.append(rho.cpu().numpy().copy())
     got = {}
-    n = b.run_pipelined(7, e_source=lambda k: es[k], on_result=lambda k, r: got.__setitem__(k, r.numpy().copy()))
-    assert n == 7 and sorted(got) == list(range(7))
-    for k in range(7):
+    n = b.run_pipelined(steps, e_source=lambda k: es[k], group=group,
+                        on_result=lambda k, r: got.__setitem__(k, r.numpy().copy()))
+    assert n == steps and sorted(got) == list(range(steps))
+    for k in range(steps):
         assert bits_equal(got[k], want[k]), k
     from oracle import oracle
     for x, y in zip(a.download(), b.download()):
@@ -452,30 +455,63 @@ def test_run_pipelined_matches_eager_steps(cuda, sort_every):
     assert any(isinstance(k, tuple) and k[0] == "pipe" for k in b.graphs)
 
 
-def test_run_pipelined_field_solve_absorbing(cuda):
-    """Field-solve + absorbing walls through the pipelined loop (single-step
-    graphs, serial density -> Poisson -> E -> push -> compaction) deliver the
-    eager steps' rho sequence bit for bit."""
+@pytest.mark.parametrize("with_input", [False, True])
+def test_prepare_pipe_graphs_covers_run(cuda, with_input):
+    """prepare_pipe_graphs captures every graph run_pipelined needs across
+    sorts (so a timed loop never captures), and the run still matches eager."""
+    import torch
+
+    from paper_2404_10270_b200 import Engine
+
+    cfg = _mk_config(nc=40, ppc0=12, sort_every=4)
+    flats = _random_flats(cfg, 5, vscale=0.3)
+    e_host = torch.zeros(cfg.grid.nc + 1, dtype=torch.float64).pin_memory()
+    src = (lambda k: e_host) if with_input else None
+    a = Engine(cfg, device=cuda, check_every=0)
+    b = Engine(cfg, device=cuda, check_every=0)
+    a.upload(flats)
+    b.upload(flats)
+    b.prepare_pipe_graphs(with_input, group=3)
+    n0 = len(b.graphs)
+    assert n0 > 0
+    got = {}
+    b.run_pipelined(30, e_source=src, group=3, on_result=lambda k, r: got.__setitem__(k, r.numpy().copy()))
+    assert len(b.graphs) == n0
+    for k in range(30):
+        rho, _ = a.step(e_ext=e_host.to(cuda) if with_input else None)
+        assert bits_equal(got[k], rho.cpu().numpy()), k
+
+
+@pytest.mark.parametrize("group", [1, 3])
+def test_run_pipelined_field_solve_absorbing(cuda, group):
+    """Field-solve + absorbing walls + cell sorts through the pipelined loop
+    (graphs of `group` steps, serial density -> Poisson -> E -> push ->
+    compaction; sorts bounded by the device live count) deliver the eager
+    steps' rho sequence bit for bit."""
     from paper_2404_10270_b200 import Engine
 
     cfg = _mk_config(nc=64, ppc0=16, field_solve=True, smoothing_passes=1, boundary="dirichlet",
-                     particle_boundary="absorbing", phi_left=2.0, phi_right=-1.0)
+                     particle_boundary="absorbing", phi_left=2.0, phi_right=-1.0, sort_every=5)
     flats = _random_flats(cfg, 13, vscale=0.4)
     a = Engine(cfg, device=cuda, check_every=0)
     b = Engine(cfg, device=cuda, check_every=0)
     a.upload(flats)
     b.upload(flats)
+    steps = 14
     want = []
-    for _ in range(6):
+    for _ in range(steps):
         rho, _ = a.step()
         want.append(rho.cpu().numpy().copy())
     got = {}
-    b.run_pipelined(6, on_result=lambda k, r: got.__setitem__(k, r.numpy().copy()))
-    for k in range(6):
+    b.run_pipelined(steps, group=group, on_result=lambda k, r: got.__setitem__(k, r.numpy().copy()))
+    for k in range(steps):
         assert bits_equal(got[k], want[k]), k
     a.sync()
     b.sync()
     assert np.array_equal(a.absorbed, b.absorbed) and a.absorbed.sum() > 0
+    from oracle import oracle
+    for x, y in zip(a.download(), b.download()):
+        assert np.array_equal(oracle.canonical(x.cell, x.fields()), oracle.canonical(y.cell, y.fields()))
 
 
 @pytest.mark.parametrize("replay", [False, True])
