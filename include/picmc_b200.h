@@ -335,6 +335,70 @@ int pb_rho_from_partials(const double *raw, const double *coef, int ndep,
                          int64_t nc, int field_bc, double *left,
                          double *right, double *rho, void *stream);
 
+/* ---- Mover API on the reference's cell-segmented store ------------------
+ * CellSortedStore (pkg/src/picmc/core.py:100-264): per cell j, live slots
+ * [offs[j], offs[j]+counts[j]) of packed float64 field arrays, free space
+ * zeroed.  Field 0 is x; the others (vx, vy, vz[, yp]) in the store's order.
+ * These back the twin of pkg/src/picmc/mover.py (paper_2404_10270_b200.mover). */
+#define PB_CS_MAX_FIELDS 5
+
+typedef struct pb_cell_fields {
+  double *field[PB_CS_MAX_FIELDS];
+  int nf;
+  const int64_t *offs;
+  int64_t *counts;
+  int64_t nc;
+} pb_cell_fields;
+
+/* Movers (mover.py:74-110): dest, src_cell, src_slot and the fields, x
+ * already normalised to the destination cell. */
+typedef struct pb_movers {
+  double *field[PB_CS_MAX_FIELDS];
+  int64_t *dest;
+  int64_t *src_cell;
+  int64_t *src_slot;
+} pb_movers;
+
+/* Scratch for pb_push_velocity / pb_resort_count. */
+size_t pb_cs_scratch_bytes(int64_t nc);
+
+/* push_velocity (mover.py:43-54): vx[live k] += coef * e_p[k], e_p in live
+ * (cell-major) order. */
+int pb_push_velocity(const double *e_p, double coef, double *vx,
+                     const int64_t *offs, const int64_t *counts, int64_t nc,
+                     void *scratch, size_t scratch_bytes, void *stream);
+
+/* resort_collect, pass 1 (mover.py:136-148): movers per cell into
+ * mover_counts[nc+1] (last entry 0), their exclusive scan into
+ * mover_base[nc+1] (mover_base[nc] = total), and the slot of the first
+ * particle whose displacement reaches across nc_global cells into *cfl_slot
+ * (UINT64_MAX when none). */
+int pb_resort_count(const double *x, const int64_t *offs, const int64_t *counts,
+                    int64_t nc, int64_t nc_global, int64_t *mover_counts,
+                    int64_t *mover_base, uint64_t *cfl_slot, void *scratch,
+                    size_t scratch_bytes, void *stream);
+
+/* resort_collect, pass 2 (mover.py:149-181): movers written in (src_cell,
+ * src_slot) order at mover_base, dest wrapped into [0, nc_global) with the
+ * carry rule, survivors compacted in slot order, vacated slots zeroed,
+ * counts updated.  `lo` is the store's global cell offset. */
+int pb_resort_collect(const pb_cell_fields *s, const pb_movers *m, int64_t lo,
+                      int64_t nc_global, const int64_t *mover_base, void *stream);
+
+/* commit_incomers (mover.py:185-195): mover order[t] goes to slot
+ * offs[j] + counts[j] + rank[t] of its destination cell j = dest - lo;
+ * `order` is lexsort(dest, src_cell, src_slot).  Capacity is the caller's
+ * (grow first); counts are not updated here. */
+int pb_commit_place(const pb_cell_fields *s, const pb_movers *m,
+                    const int64_t *order, const int64_t *rank, int64_t n,
+                    int64_t lo, void *stream);
+
+/* Copy live segments to new per-cell offsets (capacity growth,
+ * core.py:220-240); dst must be zeroed. */
+int pb_repack(const double *src, double *dst, const int64_t *offs_old,
+              const int64_t *offs_new, const int64_t *counts, int64_t nc,
+              void *stream);
+
 #ifdef __cplusplus
 }
 #endif

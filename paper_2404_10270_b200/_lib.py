@@ -80,6 +80,18 @@ class PbCanon(ctypes.Structure):
     ]
 
 
+PB_CS_MAX_FIELDS = 5
+
+
+class PbCellFields(ctypes.Structure):
+    _fields_ = [("field", _p * PB_CS_MAX_FIELDS), ("nf", ctypes.c_int), ("offs", _p),
+                ("counts", _p), ("nc", _i64)]
+
+
+class PbMovers(ctypes.Structure):
+    _fields_ = [("field", _p * PB_CS_MAX_FIELDS), ("dest", _p), ("src_cell", _p), ("src_slot", _p)]
+
+
 STATUS_BYTES = ctypes.sizeof(PbStatus)
 
 # name -> (restype, argtypes); mirrors include/picmc_b200.h one to one.
@@ -137,6 +149,14 @@ _SIGS = {
                                          _p, _p, ctypes.c_size_t, ctypes.POINTER(_i64), _p]),
     "pb_rho_from_partials": (ctypes.c_int, [_p, ctypes.POINTER(_f64), ctypes.c_int, _i64,
                                             ctypes.c_int, _p, _p, _p, _p]),
+    "pb_cs_scratch_bytes": (ctypes.c_size_t, [_i64]),
+    "pb_push_velocity": (ctypes.c_int, [_p, _f64, _p, _p, _p, _i64, _p, ctypes.c_size_t, _p]),
+    "pb_resort_count": (ctypes.c_int, [_p, _p, _p, _i64, _i64, _p, _p, _p, _p, ctypes.c_size_t, _p]),
+    "pb_resort_collect": (ctypes.c_int, [ctypes.POINTER(PbCellFields), ctypes.POINTER(PbMovers),
+                                         _i64, _i64, _p, _p]),
+    "pb_commit_place": (ctypes.c_int, [ctypes.POINTER(PbCellFields), ctypes.POINTER(PbMovers),
+                                       _p, _p, _i64, _i64, _p]),
+    "pb_repack": (ctypes.c_int, [_p, _p, _p, _p, _p, _i64, _p]),
 }
 
 _lock = threading.Lock()

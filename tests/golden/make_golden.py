@@ -408,6 +408,91 @@ def gen_desk_criterion01(picmc):
     print("desk criterion 01:", steps, "steps", m.diagnostics[-1])
 
 
+def raw_store(store, prefix):
+    """Every array of a store, free space included (slot layout pinned)."""
+    out = {}
+    for isp in range(store.nsp):
+        out[f"{prefix}sp{isp}_counts"] = store.counts(isp).copy()
+        out[f"{prefix}sp{isp}_caps"] = store.caps(isp).copy()
+        out[f"{prefix}sp{isp}_offs"] = store.offsets(isp).copy()
+        for name, arr in store.data(isp).items():
+            out[f"{prefix}sp{isp}_{name}"] = arr.copy()
+    return out
+
+
+def gen_mover_api(picmc):
+    """The store-level mover API (pkg/src/picmc/mover.py) on a store with
+    slack and tight capacities: mover_phase + resort per step (capacity
+    doubling included), resort_collect's Movers, and the separable
+    gather + push_velocity + push_position composition."""
+    from picmc.core import CellSortedStore, Grid1D, PhysicalConstants, SpeciesDef
+    from picmc.fields import gather_field
+    from picmc.mover import mover_phase, push_position, push_velocity, resort, resort_collect
+    from picmc.scheduler import Scheduler
+
+    nc, ppc = 23, 6
+    species = [SpeciesDef("q", -1.602176634e-19, 9.1093837015e-31),
+               SpeciesDef("n", 0.0, 3.3e-27, nstep=3, track_transverse=True)]
+    consts = PhysicalConstants(dt_s=4e-14)
+
+    def fresh(seed):
+        store = CellSortedStore(Grid1D.from_cells(nc, nc * 1e-5), species, initial_cap=ppc)
+        rng = np.random.default_rng(seed)
+        for isp in range(2):
+            store.counts(isp)[:] = rng.integers(0, ppc + 1, size=nc)
+            idx = store.live_indices(isp)
+            d = store.data(isp)
+            d["x"][idx] = rng.random(idx.size)
+            for f in ("vx", "vy", "vz"):
+                d[f][idx] = 1.3 * rng.standard_normal(idx.size)
+            d["vx"][idx[::11]] = -0.0
+            if "yp" in d:
+                d["yp"][idx] = rng.standard_normal(idx.size)
+        return store, rng
+
+    store, rng = fresh(77)
+    out = raw_store(store, "init_")
+    steps = 6
+    e_hist = []
+    with Scheduler(workers=2, trace=False) as sched:
+        for k in range(steps):
+            e = 2e3 * rng.standard_normal(nc + 1)
+            e_hist.append(e)
+            mover_phase(store, e, consts, sched, grainsize=5)
+            out[f"moved{k}"] = np.array(resort(store))
+            out.update(raw_store(store, f"step{k}_"))
+    out["e_hist"] = np.array(e_hist)
+    out["steps"] = np.array(steps)
+
+    # resort_collect alone: the Movers and the compacted store
+    store, rng = fresh(78)
+    out.update(raw_store(store, "cinit_"))
+    for isp in range(2):
+        push_position(store, isp)
+    out.update(raw_store(store, "cpushed_"))
+    for m in resort_collect(store):
+        out[f"cmov{m.isp}_dest"] = m.dest_cell
+        out[f"cmov{m.isp}_src_cell"] = m.src_cell
+        out[f"cmov{m.isp}_src_slot"] = m.src_slot
+        for name, v in m.fields.items():
+            out[f"cmov{m.isp}_{name}"] = v
+    out.update(raw_store(store, "collected_"))
+
+    # separable composition on the charged species
+    store, rng = fresh(79)
+    out.update(raw_store(store, "vinit_"))
+    e = 300.0 * rng.standard_normal(nc + 1)
+    e_p = gather_field(e, store, store.grid)
+    push_velocity(store, 0, e_p[0], consts)
+    push_position(store, 0)
+    out["v_e"] = e
+    out["v_e_p0"] = e_p[0]
+    out.update(raw_store(store, "vdone_"))
+    out["dt_s"] = np.array(4e-14)
+    out["nc"] = np.array(nc)
+    np.savez_compressed(os.path.join(HERE, "mover_api.npz"), **out)
+
+
 if __name__ == "__main__":
     ref = import_reference()
     gen_backend(ref)
@@ -417,6 +502,7 @@ if __name__ == "__main__":
     gen_runs(ref)
     gen_fields(ref)
     gen_mover_multistep(ref)
+    gen_mover_api(ref)
     gen_collision_runs(ref)
     gen_collision_kats(ref)
     gen_desk_criterion01(ref)
