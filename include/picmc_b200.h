@@ -193,6 +193,13 @@ int pb_density_step(uint64_t *bins, uint64_t *bins_next,
 /* Fill the holes left by absorbed particles from the tail (warp-ballot
  * stream compaction); updates *n_dev.  `scratch` needs
  * pb_compact_scratch_bytes(n) bytes. */
+/* stitch_rho (fields.py:81-92): rho[g] = R[g-1] + L[g]; periodic ends
+ * rho[0] = rho[nc] = R[nc-1] + L[0], else rho[0] = L[0], rho[nc] = R[nc-1]
+ * (no wall doubling: that is deposit_charge's, done by pb_density_step /
+ * pb_rho_from_partials). */
+int pb_stitch_rho(const double *left, const double *right, int64_t nc,
+                  int periodic, double *rho, void *stream);
+
 size_t pb_compact_scratch_bytes(int64_t n);
 int pb_compact(const pb_species *sp, int nsp, pb_status *status,
                void *scratch, size_t scratch_bytes, void *stream);

@@ -16,7 +16,7 @@ from .engine import PHASE_KEYS, Engine, Partition, partition_cells, reduce_bins
 from .errors import CflViolation, ConfigError, ContractViolation, EngineError, InitError
 from .harness import CollisionTally, RunMetrics, run_simulation
 from .canonical import CanonicalEngine
-from . import cellstore, collisions, mover
+from . import cellstore, collisions, fields, mover
 
 __version__ = "0.1.0"
 

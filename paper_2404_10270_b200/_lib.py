@@ -149,6 +149,7 @@ _SIGS = {
                                          _p, _p, ctypes.c_size_t, ctypes.POINTER(_i64), _p]),
     "pb_rho_from_partials": (ctypes.c_int, [_p, ctypes.POINTER(_f64), ctypes.c_int, _i64,
                                             ctypes.c_int, _p, _p, _p, _p]),
+    "pb_stitch_rho": (ctypes.c_int, [_p, _p, _i64, ctypes.c_int, _p, _p]),
     "pb_cs_scratch_bytes": (ctypes.c_size_t, [_i64]),
     "pb_push_velocity": (ctypes.c_int, [_p, _f64, _p, _p, _p, _i64, _p, ctypes.c_size_t, _p]),
     "pb_resort_count": (ctypes.c_int, [_p, _p, _p, _i64, _i64, _p, _p, _p, _p, ctypes.c_size_t, _p]),

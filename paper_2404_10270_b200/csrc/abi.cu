@@ -111,8 +111,10 @@ __global__ void k_partials_clear(uint64_t *__restrict__ bins, CoefArgs ca, int n
   }
 }
 
+// wall = 2.0: deposit_charge's doubled wall nodes (fields.py:115-117);
+// wall = 1.0: plain stitch_rho (fields.py:89-91, x*1.0 == x exactly).
 __global__ void k_stitch(const double *__restrict__ left, const double *__restrict__ right,
-                         int64_t nc, int field_bc, double *__restrict__ rho) {
+                         int64_t nc, int field_bc, double *__restrict__ rho, double wall = 2.0) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g > nc) return;
   double v;
@@ -121,9 +123,9 @@ __global__ void k_stitch(const double *__restrict__ left, const double *__restri
   } else if (field_bc == PB_FIELD_PERIODIC) {
     v = __dadd_rn(right[nc - 1], left[0]);
   } else if (g == 0) {
-    v = __dmul_rn(left[0], 2.0);  // fields.py:115-117
+    v = __dmul_rn(left[0], wall);
   } else {
-    v = __dmul_rn(right[nc - 1], 2.0);
+    v = __dmul_rn(right[nc - 1], wall);
   }
   rho[g] = v;
 }
@@ -252,5 +254,19 @@ extern "C" int pb_stream_sol(const pb_species *sp, int nsp, void *stream) {
         s.n & ~(int64_t)3, charged ? 1 : 0);
   }
   PB_CHECK_LAUNCH("k_stream_sol");
+  return PB_OK;
+}
+
+extern "C" int pb_stitch_rho(const double *left, const double *right, int64_t nc, int periodic,
+                             double *rho, void *stream) {
+  if (nc < 1 || !left || !right || !rho) {
+    pb::set_error("pb_stitch_rho: bad arguments (nc=%lld)", (long long)nc);
+    return PB_ERR_INVALID;
+  }
+  const int threads = 256;
+  const int64_t blocks = (nc + 1 + threads - 1) / threads;
+  pb::k_stitch<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
+      left, right, nc, periodic ? PB_FIELD_PERIODIC : PB_FIELD_DIRICHLET, rho, 1.0);
+  PB_CHECK_LAUNCH("k_stitch");
   return PB_OK;
 }

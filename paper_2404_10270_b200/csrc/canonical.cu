@@ -731,7 +731,7 @@ __global__ void k_rho_raw(const double *__restrict__ raw, RawCoef ca, int ndep, 
 extern "C" int pb_rho_from_partials(const double *raw, const double *coef, int ndep, int64_t nc,
                                     int field_bc, double *left, double *right, double *rho,
                                     void *stream) {
-  if (ndep < 0 || ndep > PB_MAX_SPECIES || nc < 2 || !rho || (ndep > 0 && (!raw || !coef)) ||
+  if (ndep < 0 || ndep > PB_MAX_SPECIES || nc < 1 || !rho || (ndep > 0 && (!raw || !coef)) ||
       (field_bc != PB_FIELD_PERIODIC && field_bc != PB_FIELD_DIRICHLET)) {
     pb::set_error("pb_rho_from_partials: bad arguments");
     return PB_ERR_INVALID;

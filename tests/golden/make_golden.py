@@ -493,6 +493,48 @@ def gen_mover_api(picmc):
     np.savez_compressed(os.path.join(HERE, "mover_api.npz"), **out)
 
 
+def gen_fields_api(picmc):
+    """Store-level field functions (pkg/src/picmc/fields.py:55-236) on a
+    store with slack: weighted partials over sub-ranges, stitch_rho, the
+    wall-doubled deposit_charge and gather_field."""
+    from picmc.core import CellSortedStore, Grid1D, PhysicalConstants, SpeciesDef
+    from picmc.fields import deposit_charge, deposit_partials_range, gather_field, stitch_rho
+
+    nc, ppc = 29, 7
+    species = [SpeciesDef("e", -1.602176634e-19, 9.1093837015e-31),
+               SpeciesDef("D+", 1.602176634e-19, 3.3435837483066354e-27),
+               SpeciesDef("D", 0.0, 3.344494686676785e-27, track_transverse=True)]
+    store = CellSortedStore(Grid1D.from_cells(nc, nc * 1e-5), species, initial_cap=ppc + 2)
+    store.weights = [3.7e14, 2.9e14, 1.1e14]
+    rng = np.random.default_rng(91)
+    for isp in range(3):
+        store.counts(isp)[:] = rng.integers(0, ppc + 1, size=nc)
+        idx = store.live_indices(isp)
+        d = store.data(isp)
+        d["x"][idx] = rng.random(idx.size)
+        d["x"][idx[::13]] = 0.0
+        for f in ("vx", "vy", "vz"):
+            d[f][idx] = rng.standard_normal(idx.size)
+        if "yp" in d:
+            d["yp"][idx] = rng.standard_normal(idx.size)
+    consts = PhysicalConstants(dt_s=4e-14)
+    out = raw_store(store, "store_")
+    out["weights"] = np.array(store.weights)
+    for lo, hi in ((0, nc), (5, 17), (28, 29)):
+        left, right = deposit_partials_range(store, consts, lo, hi)
+        out[f"dpr_{lo}_{hi}_left"], out[f"dpr_{lo}_{hi}_right"] = left, right
+    left, right = deposit_partials_range(store, consts, 0, nc)
+    out["stitch_periodic"] = stitch_rho(left, right, True)
+    out["stitch_walls"] = stitch_rho(left, right, False)
+    out["charge_periodic"] = deposit_charge(store, store.grid, consts, "periodic")
+    out["charge_dirichlet"] = deposit_charge(store, store.grid, consts, "dirichlet")
+    e = 1e3 * rng.standard_normal(nc + 1)
+    out["gather_e"] = e
+    for isp, v in gather_field(e, store, store.grid).items():
+        out[f"gather_sp{isp}"] = v
+    np.savez_compressed(os.path.join(HERE, "fields_api.npz"), **out)
+
+
 if __name__ == "__main__":
     ref = import_reference()
     gen_backend(ref)
@@ -503,6 +545,7 @@ if __name__ == "__main__":
     gen_fields(ref)
     gen_mover_multistep(ref)
     gen_mover_api(ref)
+    gen_fields_api(ref)
     gen_collision_runs(ref)
     gen_collision_kats(ref)
     gen_desk_criterion01(ref)
