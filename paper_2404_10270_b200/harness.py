@@ -152,3 +152,8 @@ def write_metrics_csv(phase_seconds, path):
         w.writerow(["phase", "seconds"])
         for key in PHASE_KEYS + ("total",):
             w.writerow([key, f"{phase_seconds.get(key, 0.0):.9f}"])
+
+
+# the reference keeps its scaling driver in harness.py (:278-383)
+from .scaling import (ScalingReport, compute_parallel_efficiency, compute_speedup,  # noqa: E402,F401
+                      strong_scaling_sweep, weak_scaling_sweep, write_scaling_csv)
