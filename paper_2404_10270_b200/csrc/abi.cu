@@ -17,6 +17,14 @@ void set_error(const char *fmt, ...) {
   va_end(ap);
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *v = getenv("PB_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 int cuda_status(cudaError_t err, const char *what) {
   set_error("%s: %s (%s)", what, cudaGetErrorString(err), cudaGetErrorName(err));
   return PB_ERR_CUDA;
@@ -94,6 +102,7 @@ __global__ void k_rho_epilogue(const uint64_t *__restrict__ bins, CoefArgs ca,
 __global__ void k_partials_clear(uint64_t *__restrict__ bins, CoefArgs ca, int ndep, int64_t nc,
                                  double *__restrict__ left, double *__restrict__ right,
                                  uint64_t *__restrict__ clear, uint64_t *__restrict__ counter) {
+  pdl_enter();
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (counter && g == 0) *counter = 0;
   if (g >= nc) return;
@@ -114,7 +123,8 @@ __global__ void k_partials_clear(uint64_t *__restrict__ bins, CoefArgs ca, int n
 // wall = 2.0: deposit_charge's doubled wall nodes (fields.py:115-117);
 // wall = 1.0: plain stitch_rho (fields.py:89-91, x*1.0 == x exactly).
 __global__ void k_stitch(const double *__restrict__ left, const double *__restrict__ right,
-                         int64_t nc, int field_bc, double *__restrict__ rho, double wall = 2.0) {
+                         int64_t nc, int field_bc, double *__restrict__ rho, double wall) {
+  pdl_enter();
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g > nc) return;
   double v;
@@ -196,11 +206,12 @@ extern "C" int pb_density_step(uint64_t *bins, uint64_t *bins_next, uint64_t *co
   cudaStream_t st = (cudaStream_t)stream;
   const int threads = 256;
   const int64_t b1 = (nc + threads - 1) / threads, b2 = (nc + 1 + threads - 1) / threads;
-  pb::k_partials_clear<<<(unsigned)b1, threads, 0, st>>>(bins, ca, ndep, nc, left, right, bins_next,
-                                                         counter);
-  PB_CHECK_LAUNCH("k_partials_clear");
-  pb::k_stitch<<<(unsigned)b2, threads, 0, st>>>(left, right, nc, field_bc, rho);
-  PB_CHECK_LAUNCH("k_stitch");
+  cudaError_t e = pb::launch_pdl(pb::k_partials_clear, dim3((unsigned)b1), dim3(threads), 0, st, bins,
+                                  ca, ndep, nc, left, right, bins_next, counter);
+  if (e != cudaSuccess) return pb::cuda_status(e, "k_partials_clear");
+  e = pb::launch_pdl(pb::k_stitch, dim3((unsigned)b2), dim3(threads), 0, st, (const double *)left,
+                     (const double *)right, nc, field_bc, rho, 2.0);
+  if (e != cudaSuccess) return pb::cuda_status(e, "k_stitch");
   return PB_OK;
 }
 

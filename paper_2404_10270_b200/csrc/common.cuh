@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/picmc_b200.h"
 
 namespace pb {
@@ -51,6 +53,41 @@ __device__ __forceinline__ unsigned lane_id() {
 __device__ __forceinline__ int64_t floor_mod(int64_t a, int64_t m) {
   int64_t r = a % m;
   return r < 0 ? r + m : r;
+}
+
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// The per-step chain (density epilogue -> smoothing -> Poisson tiles -> E ->
+// mover -> compaction) is a string of dependent kernels, most of them a few
+// microseconds long.  Launched with programmatic stream serialisation, a
+// kernel's successor is scheduled while it still runs: every CTA waits until
+// the predecessor grid has completed and its writes are visible
+// (griddepcontrol.wait) before touching memory, then lets its own dependent
+// launch (launch_dependents) -- the same ordering as plain stream order,
+// minus the launch gap, with at most one kernel queued ahead.  Both are
+// no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled();  // PB_PDL (default 1)
+
+// Launch `kern` with programmatic stream serialisation (when enabled); the
+// kernel must call pdl_enter() before its first global memory access.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 }  // namespace pb

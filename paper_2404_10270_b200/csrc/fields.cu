@@ -26,6 +26,7 @@ __device__ __forceinline__ void smooth_node(const double *__restrict__ in, doubl
 
 __global__ void k_smooth_pass(const double *__restrict__ in,
                               double *__restrict__ out, int64_t nc) {
+  pdl_enter();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j > nc) return;
   smooth_node(in, out, nc, j);
@@ -54,6 +55,7 @@ __device__ __forceinline__ void efield_node(const double *__restrict__ phi, doub
 
 __global__ void k_efield(const double *__restrict__ phi, double *__restrict__ e,
                          int64_t nc, double two_dx, int field_bc) {
+  pdl_enter();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j > nc) return;
   efield_node(phi, e, nc, two_dx, field_bc, j);
@@ -334,31 +336,39 @@ __device__ void mb_shift(const PoissonArgs &a, int64_t first, int64_t stride, DD
 
 __global__ void __launch_bounds__(kMbThreads) k_mb_tile_sum(const double *__restrict__ src,
                                                             int64_t len, DD *part) {
+  pdl_enter();
   __shared__ DD sm[kMbThreads];
   mb_tile_sum(src, len, part, blockIdx.x, sm);
 }
 
 __global__ void __launch_bounds__(kMbThreads) k_mb_fwd_part(const PoissonArgs a) {
+  pdl_enter();
   __shared__ DD sm[kMbThreads];
   mb_fwd_part(a, blockIdx.x, sm);
 }
 
 __global__ void __launch_bounds__(kMbThreads) k_mb_fwd_scan(const PoissonArgs a) {
+  pdl_enter();
   __shared__ DD sm[kMbThreads];
   mb_fwd_scan(a, blockIdx.x, sm);
 }
 
 __global__ void __launch_bounds__(kMbThreads) k_mb_bwd_scan(const PoissonArgs a) {
+  pdl_enter();
   __shared__ DD sm[kMbThreads];
   mb_bwd_scan(a, blockIdx.x, sm);
 }
 
 __global__ void __launch_bounds__(kMbThreads) k_mb_shift(const PoissonArgs a) {
+  pdl_enter();
   __shared__ DD sm[kMbThreads];
   mb_shift(a, (int64_t)blockIdx.x * kMbThreads + threadIdx.x, (int64_t)gridDim.x * kMbThreads, sm);
 }
 
-__global__ void k_mb_wrap(double *phi, int64_t nc) { phi[nc] = phi[0]; }
+__global__ void k_mb_wrap(double *phi, int64_t nc) {
+  pdl_enter();
+  phi[nc] = phi[0];
+}
 
 // ---- cooperative fused field pipeline ----------------------------------------
 // smoothing passes -> scan Poisson -> E in ONE launch, grid-wide syncs between
@@ -467,8 +477,9 @@ extern "C" int pb_smooth_density(const double *rho, double *out, int64_t nc,
   const double *src = rho;
   for (int p = 0; p < passes; ++p) {
     double *dst = ((passes - 1 - p) % 2 == 0) ? out : tmp;
-    pb::k_smooth_pass<<<pb::blocks_for(nc + 1, 256), 256, 0, st>>>(src, dst, nc);
-    PB_CHECK_LAUNCH("k_smooth_pass");
+    cudaError_t e = pb::launch_pdl(pb::k_smooth_pass, dim3(pb::blocks_for(nc + 1, 256)), dim3(256), 0,
+                                   st, src, dst, nc);
+    if (e != cudaSuccess) return pb::cuda_status(e, "k_smooth_pass");
     src = dst;
   }
   return PB_OK;
@@ -514,17 +525,20 @@ extern "C" int pb_solve_poisson_scan(const double *rho, double *phi, int64_t nc,
   }
   cudaStream_t st = (cudaStream_t)stream;
   pb::PoissonArgs a = pb::poisson_args(rho, phi, nc, dx, eps0, field_bc, phi_left, phi_right, scratch);
+  const dim3 tb(pb::kMbThreads);
+  cudaError_t e = cudaSuccess;
+  if (field_bc == PB_FIELD_PERIODIC && e == cudaSuccess)
+    e = pb::launch_pdl(pb::k_mb_tile_sum, dim3(a.ntc), tb, 0, st, rho, nc, a.p0);
+  if (e == cudaSuccess) e = pb::launch_pdl(pb::k_mb_fwd_part, dim3(a.nt), tb, 0, st, a);
+  if (e == cudaSuccess) e = pb::launch_pdl(pb::k_mb_fwd_scan, dim3(a.nt), tb, 0, st, a);
+  if (e == cudaSuccess) e = pb::launch_pdl(pb::k_mb_bwd_scan, dim3(a.nt), tb, 0, st, a);
   if (field_bc == PB_FIELD_PERIODIC) {
-    pb::k_mb_tile_sum<<<a.ntc, pb::kMbThreads, 0, st>>>(rho, nc, a.p0);
+    if (e == cudaSuccess)
+      e = pb::launch_pdl(pb::k_mb_tile_sum, dim3(a.ntc), tb, 0, st, (const double *)phi, nc, a.p3);
+    if (e == cudaSuccess) e = pb::launch_pdl(pb::k_mb_shift, dim3(a.ntc), tb, 0, st, a);
+    if (e == cudaSuccess) e = pb::launch_pdl(pb::k_mb_wrap, dim3(1), dim3(1), 0, st, phi, nc);
   }
-  pb::k_mb_fwd_part<<<a.nt, pb::kMbThreads, 0, st>>>(a);
-  pb::k_mb_fwd_scan<<<a.nt, pb::kMbThreads, 0, st>>>(a);
-  pb::k_mb_bwd_scan<<<a.nt, pb::kMbThreads, 0, st>>>(a);
-  if (field_bc == PB_FIELD_PERIODIC) {
-    pb::k_mb_tile_sum<<<a.ntc, pb::kMbThreads, 0, st>>>(phi, nc, a.p3);
-    pb::k_mb_shift<<<a.ntc, pb::kMbThreads, 0, st>>>(a);
-    pb::k_mb_wrap<<<1, 1, 0, st>>>(phi, nc);
-  }
+  if (e != cudaSuccess) return pb::cuda_status(e, "poisson scan");
   PB_CHECK_LAUNCH("poisson scan");
   return PB_OK;
 }
@@ -535,9 +549,9 @@ extern "C" int pb_compute_efield(const double *phi, double *e, int64_t nc,
     pb::set_error("pb_compute_efield: bad arguments");
     return PB_ERR_INVALID;
   }
-  pb::k_efield<<<pb::blocks_for(nc + 1, 256), 256, 0, (cudaStream_t)stream>>>(
-      phi, e, nc, 2.0 * dx, field_bc);
-  PB_CHECK_LAUNCH("k_efield");
+  cudaError_t err = pb::launch_pdl(pb::k_efield, dim3(pb::blocks_for(nc + 1, 256)), dim3(256), 0,
+                                   (cudaStream_t)stream, phi, e, nc, 2.0 * dx, field_bc);
+  if (err != cudaSuccess) return pb::cuda_status(err, "k_efield");
   return PB_OK;
 }
 

@@ -1186,6 +1186,7 @@ constexpr int kWarpsPerBlock = kThreads / 32;
 template <int BC, bool BORIS>
 __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
     k_push_quad(const __grid_constant__ LaunchArgs a) {
+  pdl_enter();
   const int64_t total = a.tile_start[a.nsp];
   Window win{nullptr, nullptr, 0, 0, nullptr, nullptr};
   Tally t;
@@ -1245,6 +1246,7 @@ static constexpr int ring_smem_bytes() {
 template <int BC>
 __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
     k_push_ring(const __grid_constant__ LaunchArgs a) {
+  pdl_enter();
   extern __shared__ __align__(128) unsigned char r_smem[];
   const int lane = (int)lane_id();
   const int w = threadIdx.x >> 5;
@@ -1407,6 +1409,7 @@ __device__ __forceinline__ void split_register_list(const LaunchArgs &a, int g, 
 template <int BC>
 __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
     k_push_split(const __grid_constant__ LaunchArgs a) {
+  pdl_enter();
   extern __shared__ __align__(128) unsigned char s_smem[];
   const int lane = (int)lane_id();
   const int w = threadIdx.x >> 5;
@@ -1727,8 +1730,8 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
         int sbps = 0;
         int src = occupancy((const void *)sfn, kThreads, split_smem_bytes(), &sbps);
         if (src) return src;
-        sfn<<<sms * sbps, kThreads, split_smem_bytes(), stream>>>(a);
-        PB_CHECK_LAUNCH("k_push_split");
+        cudaError_t le = launch_pdl(sfn, dim3(sms * sbps), dim3(kThreads), split_smem_bytes(), stream, a);
+        if (le != cudaSuccess) return cuda_status(le, "k_push_split");
         g_last_kernel = "k_push_split";
         return PB_OK;
       }
@@ -1744,16 +1747,16 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
       int bps = 0;
       int rc = occupancy((const void *)rfn, kThreads, ring_smem_bytes(), &bps);
       if (rc) return rc;
-      rfn<<<sms * bps, kThreads, ring_smem_bytes(), stream>>>(a);
-      PB_CHECK_LAUNCH("k_push_ring");
+      cudaError_t le = launch_pdl(rfn, dim3(sms * bps), dim3(kThreads), ring_smem_bytes(), stream, a);
+      if (le != cudaSuccess) return cuda_status(le, "k_push_ring");
       g_last_kernel = "k_push_ring";
       return PB_OK;
     }
     int bps = 0;
     int rc = occupancy((const void *)fn, kThreads, 0, &bps);
     if (rc) return rc;
-    fn<<<sms * bps, kThreads, 0, stream>>>(a);
-    PB_CHECK_LAUNCH("k_push_quad");
+    cudaError_t le = launch_pdl(fn, dim3(sms * bps), dim3(kThreads), 0, stream, a);
+    if (le != cudaSuccess) return cuda_status(le, "k_push_quad");
     g_last_kernel = "k_push_quad";
     return PB_OK;
   }

@@ -126,6 +126,7 @@ struct CompactArgs {
 // over warp ballots; holes are consumed through a cursor.
 __global__ void __launch_bounds__(kCompactThreads)
     k_compact(const __grid_constant__ CompactArgs a) {
+  pdl_enter();
   using Scan = cub::BlockScan<int, kCompactThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int64_t s_cnt;
@@ -266,7 +267,9 @@ extern "C" int pb_compact(const pb_species *sp, int nsp, pb_status *status,
   a.tail = (int64_t *)scratch;
   a.tail_stride = nmax;
   a.st = status;
-  pb::k_compact<<<a.nsp, pb::kCompactThreads, 0, (cudaStream_t)stream>>>(a);
+  cudaError_t le = pb::launch_pdl(pb::k_compact, dim3(a.nsp), dim3(pb::kCompactThreads), 0,
+                                  (cudaStream_t)stream, a);
+  if (le != cudaSuccess) return pb::cuda_status(le, "k_compact");
   PB_CHECK_LAUNCH("k_compact");
   return PB_OK;
 }
