@@ -53,6 +53,7 @@ struct LaunchArgs {
   // over the species (rr_each per species), the rest species by species
   int64_t rr_chunks, rr_each;
   int64_t tail_start[PB_MAX_SPECIES + 1];
+  int64_t chunk;  // particles per claimed chunk (power of two dividing PB_CELL8_CHUNK)
   // split mover: list 0 = ring-staged charged species, list 1 = the rest
   ChunkList lists[2];
   const double *e;
@@ -1145,8 +1146,8 @@ __device__ __forceinline__ int chunk_species(const LaunchArgs &a, int64_t c, int
   const int isp = a.order[kk];
   const pb_species &s = a.sp[isp];
   const int64_t n = s.n_dev ? *s.n_dev : s.n;
-  beg = local * kChunk;
-  end = beg + kChunk < n ? beg + kChunk : n;
+  beg = local * a.chunk;
+  end = beg + a.chunk < n ? beg + a.chunk : n;
   return isp;
 }
 
@@ -1372,8 +1373,8 @@ __device__ __forceinline__ int list_chunk(const LaunchArgs &a, const ChunkList &
   const int isp = L.order[kk];
   const pb_species &s = a.sp[isp];
   const int64_t n = s.n_dev ? *s.n_dev : s.n;
-  beg = local * kChunk;
-  end = beg + kChunk < n ? beg + kChunk : n;
+  beg = local * a.chunk;
+  end = beg + a.chunk < n ? beg + a.chunk : n;
   return isp;
 }
 
@@ -1530,6 +1531,9 @@ static int g_interleave = -1;
 static const char *g_last_kernel = "";
 static const bool g_ring = !(getenv("PB_RING") && atoi(getenv("PB_RING")) == 0);
 static const bool g_split = !(getenv("PB_SPLIT") && atoi(getenv("PB_SPLIT")) == 0);
+// PB_SPLIT_SOLO=1: the split kernel also for charged-only launches (its
+// register warps then steal charged chunks); default: k_push_ring there.
+static const bool g_split_solo = getenv("PB_SPLIT_SOLO") && atoi(getenv("PB_SPLIT_SOLO")) != 0;
 typedef void (*TmaFn)(LaunchArgs, int, int, int);
 static int g_stages = 0;
 static int g_ahead = -1;
@@ -1601,6 +1605,7 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
   }
   LaunchArgs a;
   memset(&a, 0, sizeof(a));
+  a.chunk = kChunk;
   a.push = push ? 1 : 0;
   a.e = e;
   a.nc = nc;
@@ -1672,11 +1677,28 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
         order[j] = order[j - 1];
         order[j - 1] = tmp;
       }
+    // Claim granularity: 1024-particle chunks (a shorter tail) unless the
+    // launch is large enough that 2048 still gives every warp >= 64 chunks.
+    // Measured (profiles/r01h_claim_chunk_ab.jsonl): 1024 is -1.4% push on
+    // config 2, -1.4% config 3 (ring), -1.4% config 4; config 5 (1B
+    // particles, ~140 chunks per warp at 2048) is +5% slower at 1024.
+    // PB_CLAIM_CHUNK overrides (a power of two from 256 to 2048: chunks never
+    // straddle a cell8 chunk).
+    {
+      int64_t work = 0;
+      for (int k = 0; k < a.nsp; ++k) work += a.sp[k].n;
+      const int64_t warps = (int64_t)sms * 3 * kWarpsPerBlock;
+      static const int claim = getenv("PB_CLAIM_CHUNK") ? atoi(getenv("PB_CLAIM_CHUNK")) : 0;
+      if (claim >= 256 && claim <= kChunk && (claim & (claim - 1)) == 0)
+        a.chunk = claim;
+      else
+        a.chunk = work < warps * 64 * (int64_t)kChunk ? kChunk / 2 : kChunk;
+    }
     a.tile_start[0] = 0;
     int64_t min_chunks = -1;
     for (int k = 0; k < a.nsp; ++k) {
       a.order[k] = order[k];
-      const int64_t nk = (a.sp[order[k]].n + kChunk - 1) / kChunk;
+      const int64_t nk = (a.sp[order[k]].n + a.chunk - 1) / a.chunk;
       a.tile_start[k + 1] = a.tile_start[k] + nk;
       if (min_chunks < 0 || nk < min_chunks) min_chunks = nk;
     }
@@ -1706,7 +1728,7 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
         const bool elig = sp2.kind == PB_KIND_KICK && !sp2.yp && sp2.deposit >= 0 && bins;
         if (elig) g0[n0++] = sk; else g1[n1++] = sk;
       }
-      if (n0 > 0 && n1 > 0) {
+      if (n0 > 0 && (n1 > 0 || g_split_solo)) {
         const int *gs[2] = {g0, g1};
         const int gn[2] = {n0, n1};
         for (int g = 0; g < 2; ++g) {
@@ -1716,7 +1738,7 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
           int64_t mn = -1;
           for (int k = 0; k < L.nsp; ++k) {
             L.order[k] = gs[g][k];
-            const int64_t nk = (a.sp[L.order[k]].n + kChunk - 1) / kChunk;
+            const int64_t nk = (a.sp[L.order[k]].n + a.chunk - 1) / a.chunk;
             L.tile_start[k + 1] = L.tile_start[k] + nk;
             if (mn < 0 || nk < mn) mn = nk;
           }

@@ -94,6 +94,7 @@ class Engine:
 
     supports_collisions = False  # CanonicalEngine (canonical.py) runs them
     use_cell8 = os.environ.get("PB_CELL8", "1") != "0"
+    force_cell8 = os.environ.get("PB_CELL8", "1") == "2"  # also in charged-only runs (A/B)
     sort_ratio_cap = int(os.environ.get("PB_SORT_RATIO_CAP", "16"))
     # Field-solve steps: push neutral movers while the field pipeline runs.
     # Measured 2.4% slower on one GPU (a second launch's ramp/tail costs more
@@ -158,7 +159,7 @@ class Engine:
             # a loss (+2-5%) in charged-only runs, whose latency-bound slices
             # pay for the extra dependent base load + decode.
             has_neutral = any(species_kind(x, self.b_field) == _lib.PB_KIND_DRIFT for x in config.species)
-            cell8 = (self.use_cell8 and has_neutral and kind in (_lib.PB_KIND_KICK, _lib.PB_KIND_BORIS)
+            cell8 = (self.use_cell8 and (has_neutral or self.force_cell8) and kind in (_lib.PB_KIND_KICK, _lib.PB_KIND_BORIS)
                      and int(config.ppc0) >= 32)
             with torch.cuda.stream(self.stream):
                 self.sp.append(DeviceSpecies(spd, nloc, self.device, kind=kind, deposit=dep,

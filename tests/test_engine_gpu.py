@@ -411,7 +411,10 @@ def test_graph_replay_matches_eager_steps(cuda, case):
     from oracle import oracle
     for x, y in zip(fa, fb):
         assert np.array_equal(oracle.canonical(x.cell, x.fields()), oracle.canonical(y.cell, y.fields()))
-    if case != "sorted":  # without sorting the slot order is the same too
+    # without sorting the slot order is the same too -- except after
+    # absorbing-wall compaction, whose hole list is filled in the (arbitrary)
+    # order the mover's warps recorded the holes
+    if case not in ("sorted", "absorbing"):
         for x, y in zip(fa, fb):
             for k, v in x.fields().items():
                 assert bits_equal(v, y.fields()[k])
