@@ -429,6 +429,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": args.steps * launches_per_step + n_sort_kernels,
         "timing_windows_ms": {"steps_per_window": 200, "min": min(win_ms), "median": float(np.median(win_ms)),
                               "max": max(win_ms), "argmax": int(np.argmax(win_ms)),
+                              "all": [round(w, 5) for w in win_ms],
                               "graphs_captured_in_timed_region": graphs_timed},
         "sol_probe": {"ms": sol_ms, "actual_bytes": actual_bytes, "gbs": actual_bytes / (sol_ms * 1e-3) / 1e9,
                       "mover_actual_gbs": actual_bytes / (push_ms * 1e-3) / 1e9,

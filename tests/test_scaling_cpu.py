@@ -27,3 +27,32 @@ def test_scaling_csv_bytes(tmp_path):
     assert p.read_bytes() == (b"workers,t_total,t_mover,speedup,pe\n"
                               b"1,2.000000000,1.250000000,1.000000,100.0000\n"
                               b"4,0.625000000,0.312500000,3.200000,80.0000\n")
+
+
+def test_module_twins_have_no_cpu_fallback():
+    """mover / fields / cellstore run on the GPU only: without a device they
+    raise instead of computing on the host."""
+    import numpy as np
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_2404_10270_b200 import Grid1D, SpeciesDef, fields, mover
+    from paper_2404_10270_b200.cellstore import CellSortedStore
+
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        fields.smooth_density(np.zeros(9))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        CellSortedStore(Grid1D.from_cells(4, 4.0), [SpeciesDef("s", 0.0, 1.0)])
+
+    class Store:  # the reference store interface, numpy arrays
+        species = [SpeciesDef("s", 0.0, 1.0)]
+        grid = Grid1D.from_cells(4, 4.0)
+        data = lambda self, i: {"x": np.zeros(16), "vx": np.zeros(16), "vy": np.zeros(16),  # noqa: E731
+                                "vz": np.zeros(16)}
+        offsets = lambda self, i: np.arange(0, 16, 4)  # noqa: E731
+        counts = lambda self, i: np.zeros(4, dtype=np.int64)  # noqa: E731
+        field_names = lambda self, i: ("x", "vx", "vy", "vz")  # noqa: E731
+
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        mover.resort_collect(Store())
