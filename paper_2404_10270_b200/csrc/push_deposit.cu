@@ -1216,13 +1216,15 @@ __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
 // with): a per-warp TMA ring.  Each warp streams its 128-particle slices
 // (x, vx, cell = 2.5 KB) through kRing shared-memory stages with
 // cp.async.bulk issued by one lane (mbarrier completion), claiming the next
-// chunk before the current one runs out, so kRing-1 slices stay in flight per
-// warp without holding registers.  In mixed launches the shared-memory
-// carve-out cost the neutral slices more than it gained, so k_push_quad
-// stays the default there.
+// chunk before the current one runs out.  A stage is released as soon as the
+// warp has copied its slice to registers, so the next slice streams in while
+// the current one is computed and stored.  One stage is the fastest
+// (config 3 push: 1 stage 93.9 us, 2 stages 94.7, 3 stages 96.2, 4 stages
+// 115 -- two blocks per SM; a smaller carve-out leaves more L1 for the E
+// gather).  Mixed launches use k_push_split.
 // ---------------------------------------------------------------------------
 #ifndef PB_RING_STAGES
-#define PB_RING_STAGES 3
+#define PB_RING_STAGES 1
 #endif
 constexpr int kRing = PB_RING_STAGES;
 constexpr int kSlice = 128;
