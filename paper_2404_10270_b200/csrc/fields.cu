@@ -183,10 +183,15 @@ __device__ __forceinline__ DD dd_of(double v) { return {v, 0.0}; }
 //   z_k = sum_{i<=k} (i+1) rhs_i,  y_k = z_k/(k+1)          (forward)
 //   w_k = sum_{i>=k} -y_i/(i+2),   x_k = (k+1) w_k          (backward)
 // Both are prefix sums, done with double-double accumulation over a grid of
-// 2048-element tiles: per-tile DD partials, then every block adds the
+// 512-element tiles (256 threads x 2; the phases are latency-bound, so more,
+// smaller blocks win: config 3 step -3% against 2048-element tiles, 1 per
+// thread no better): per-tile DD partials, then every block adds the
 // partials before it (deterministic order) and scans its own tile.
+#ifndef PB_MB_PER
+#define PB_MB_PER 2
+#endif
 constexpr int kMbThreads = 256;
-constexpr int kMbPer = 8;
+constexpr int kMbPer = PB_MB_PER;
 constexpr int kMbTile = kMbThreads * kMbPer;
 
 __device__ DD mb_block_reduce(DD v, DD *sm) {
