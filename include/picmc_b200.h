@@ -40,6 +40,7 @@ extern "C" {
 #define PB_ERR_CFL 3
 #define PB_ERR_CONTRACT 4
 #define PB_ERR_OVERFLOW 5
+#define PB_ERR_PEER 6 /* a peer GPU did not reach a density barrier */
 
 /* Species kinds: which arithmetic the mover applies (SpeciesDef flags,
  * pkg/src/picmc/core.py:53-81, and accel_nodes_for_species,
@@ -405,6 +406,41 @@ int pb_commit_place(const pb_cell_fields *s, const pb_movers *m,
 int pb_repack(const double *src, double *dst, const int64_t *offs_old,
               const int64_t *offs_new, const int64_t *counts, int64_t nc,
               void *stream);
+
+/* ---- Multi-GPU density exchange over peer memory --------------------------
+ * The per-step density allreduce fused with the epilogue: one kernel per
+ * rank sums its slice of the fixed-point bins out of every rank's memory
+ * (CUDA IPC mappings over NVLink; exact integer sums), computes
+ * left/right/rho there and stores the slice into every rank's buffers, with
+ * flag barriers in peer memory.  Replaces reduce_bins (the NCCL allreduce)
+ * + pb_density_step; bitwise the same result.  All ranks call it with the
+ * same epoch sequence (1, 2, ...), grid and nc. */
+#define PB_MAX_RANKS 8
+#define PB_PEER_HANDLE_BYTES 64 /* sizeof(cudaIpcMemHandle_t) */
+
+typedef struct pb_peer_density {
+  uint64_t *bins[PB_MAX_RANKS];  /* every rank's current bin set (this rank's: its own) */
+  double *left[PB_MAX_RANKS];
+  double *right[PB_MAX_RANKS];
+  double *rho[PB_MAX_RANKS];
+  uint64_t *flags[PB_MAX_RANKS]; /* 2 * world zeroed words per rank */
+  int rank;
+  int world;
+  uint64_t epoch;                /* 1, 2, ... one per call */
+} pb_peer_density;
+
+/* cudaMalloc + zero + IPC handle (PB_PEER_HANDLE_BYTES) for a buffer peers map. */
+int pb_peer_alloc(size_t bytes, void **ptr, void *handle_out);
+/* Map a peer's buffer from its handle. */
+int pb_peer_open(const void *handle, void **ptr);
+/* Unmap (owned = 0) or free (owned = 1). */
+int pb_peer_close(void *ptr, int owned);
+/* One density exchange + epilogue (see above); bins_next (optional) is
+ * zeroed as well, like pb_density_step's. Timeouts set PB_ERR_PEER in
+ * *status. */
+int pb_peer_density_step(const pb_peer_density *p, uint64_t *bins_next,
+                         const double *coef, int ndep, int64_t nc,
+                         int field_bc, pb_status *status, void *stream);
 
 #ifdef __cplusplus
 }

@@ -20,6 +20,7 @@ PB_ERR_CUDA = 2
 PB_ERR_CFL = 3
 PB_ERR_CONTRACT = 4
 PB_ERR_OVERFLOW = 5
+PB_ERR_PEER = 6
 
 PB_KIND_INACTIVE = 0
 PB_KIND_DRIFT = 1
@@ -81,6 +82,14 @@ class PbCanon(ctypes.Structure):
 
 
 PB_CS_MAX_FIELDS = 5
+PB_MAX_RANKS = 8
+PB_PEER_HANDLE_BYTES = 64
+
+
+class PbPeerDensity(ctypes.Structure):
+    _fields_ = [("bins", _p * PB_MAX_RANKS), ("left", _p * PB_MAX_RANKS), ("right", _p * PB_MAX_RANKS),
+                ("rho", _p * PB_MAX_RANKS), ("flags", _p * PB_MAX_RANKS), ("rank", ctypes.c_int),
+                ("world", ctypes.c_int), ("epoch", ctypes.c_uint64)]
 
 
 class PbCellFields(ctypes.Structure):
@@ -151,6 +160,11 @@ _SIGS = {
                                             ctypes.c_int, _p, _p, _p, _p]),
     "pb_stitch_rho": (ctypes.c_int, [_p, _p, _i64, ctypes.c_int, _p, _p]),
     "pb_cs_scratch_bytes": (ctypes.c_size_t, [_i64]),
+    "pb_peer_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(_p), _p]),
+    "pb_peer_open": (ctypes.c_int, [_p, ctypes.POINTER(_p)]),
+    "pb_peer_close": (ctypes.c_int, [_p, ctypes.c_int]),
+    "pb_peer_density_step": (ctypes.c_int, [ctypes.POINTER(PbPeerDensity), _p, ctypes.POINTER(_f64),
+                                            ctypes.c_int, _i64, ctypes.c_int, _p, _p]),
     "pb_push_velocity": (ctypes.c_int, [_p, _f64, _p, _p, _p, _i64, _p, ctypes.c_size_t, _p]),
     "pb_resort_count": (ctypes.c_int, [_p, _p, _p, _i64, _i64, _p, _p, _p, _p, ctypes.c_size_t, _p]),
     "pb_resort_collect": (ctypes.c_int, [ctypes.POINTER(PbCellFields), ctypes.POINTER(PbMovers),
@@ -202,6 +216,6 @@ def check(rc: int, what: str = ""):
         raise CflViolation(msg)
     if rc == PB_ERR_CONTRACT:
         raise ContractViolation(msg)
-    if rc == PB_ERR_OVERFLOW:
+    if rc in (PB_ERR_OVERFLOW, PB_ERR_PEER):
         raise EngineError(msg)
     raise RuntimeError(msg)

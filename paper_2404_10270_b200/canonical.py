@@ -45,6 +45,7 @@ class CanonicalEngine(Engine):
     """Single-GPU engine in the reference's canonical slot order."""
 
     supports_collisions = True
+    supports_peer = False  # its density allreduces fp64 partials (exact, rank order)
     use_cell8 = False  # the canonical kernels read the full cell index
 
     def __init__(self, config, device=None, *, rank: int = 0, world: int = 1, group=None,

@@ -105,9 +105,10 @@ class Engine:
     # measured 0.8-6% slower than the per-phase kernels inside graphs
     # (configs 4 and 3), so it is opt-in: PB_FUSED_FIELD=1
     fused_field = os.environ.get("PB_FUSED_FIELD", "0") == "1"
+    supports_peer = True  # the fused peer-memory density exchange (N > 1)
 
     def __init__(self, config, device=None, *, rank: int = 0, world: int = 1,
-                 group=None, init: str = "host", check_every: int = 1):
+                 group=None, init: str = "host", check_every: int = 1, peer: bool = None):
         config.validate()
         if config.collisions is not None and config.collisions.enabled and not self.supports_collisions:
             raise ConfigError(
@@ -178,6 +179,15 @@ class Engine:
             self.rho = torch.zeros(nc + 1, dtype=torch.float64, device=self.device)
             self.left = torch.zeros(nc, dtype=torch.float64, device=self.device)
             self.right = torch.zeros(nc, dtype=torch.float64, device=self.device)
+        # N > 1: the density exchange through peer memory (pb_peer_density_step:
+        # the allreduce fused with the epilogue over NVLink) unless PB_PEER=0;
+        # the bins and the outputs then live in IPC-shared buffers
+        self.peer = None
+        if peer is None:
+            peer = os.environ.get("PB_PEER", "1") != "0"
+        if world > 1 and peer and self.supports_peer:
+            self._setup_peer(max(ndep, 1) * 2 * nc, nc)
+        with torch.cuda.stream(self.stream):
             self.rho_s = torch.zeros(nc + 1, dtype=torch.float64, device=self.device)
             self.phi = torch.zeros(nc + 1, dtype=torch.float64, device=self.device)
             self.e = torch.zeros(nc + 1, dtype=torch.float64, device=self.device)
@@ -299,6 +309,10 @@ class Engine:
         must not touch the set that push deposits into)."""
         st = stream if stream is not None else self.stream
         with torch.cuda.stream(st):
+            if self.peer is not None:
+                self._peer_density(st, clear_next)
+                self._next_clear = True
+                return self.rho
             if self.world > 1:
                 reduce_bins(self.bins, self.group)
             nxt = self.bins_pp[1 - self.cur].data_ptr() if clear_next else None
@@ -308,6 +322,42 @@ class Engine:
                 ctypes.c_void_p(st.cuda_stream)), "pb_density_step")
         self._next_clear = True
         return self.rho
+
+    def _setup_peer(self, nbins: int, nc: int):
+        from .peer import PeerBuffers
+
+        pb = PeerBuffers({"bins0": nbins * 8, "bins1": nbins * 8, "rho": (nc + 1) * 8, "left": nc * 8,
+                          "right": nc * 8, "flags": 2 * _lib.PB_MAX_RANKS * 8},
+                         self.rank, self.world, self.group, self.device)
+        if not pb.available:  # no P2P path on some pair: every rank keeps the NCCL allreduce
+            pb.close()
+            return
+        torch.cuda.synchronize(self.device)  # the buffers were zeroed on the legacy stream
+        self.peer = pb
+        self._peer_epoch = 0
+        self.bins_pp = [pb.tensor("bins0", nbins, torch.int64), pb.tensor("bins1", nbins, torch.int64)]
+        self.rho = pb.tensor("rho", nc + 1, torch.float64)
+        self.left = pb.tensor("left", nc, torch.float64)
+        self.right = pb.tensor("right", nc, torch.float64)
+
+    def _peer_density(self, st, clear_next: bool):
+        """pb_peer_density_step: every rank's bins summed over NVLink and the
+        epilogue, one kernel (replaces reduce_bins + pb_density_step)."""
+        pb = self.peer
+        self._peer_epoch += 1
+        d = _lib.PbPeerDensity()
+        key = "bins%d" % self.cur
+        for r in range(self.world):
+            d.bins[r] = pb.ptrs[key][r]
+            d.left[r] = pb.ptrs["left"][r]
+            d.right[r] = pb.ptrs["right"][r]
+            d.rho[r] = pb.ptrs["rho"][r]
+            d.flags[r] = pb.ptrs["flags"][r]
+        d.rank, d.world, d.epoch = self.rank, self.world, self._peer_epoch
+        nxt = self.bins_pp[1 - self.cur].data_ptr() if clear_next else None
+        _lib.check(self.lib.pb_peer_density_step(ctypes.byref(d), nxt, self._coef_c, self.ndep, self.nc,
+                                                 self.field_bc, self.status.data_ptr(),
+                                                 ctypes.c_void_p(st.cuda_stream)), "pb_peer_density_step")
 
     def field(self, rho: torch.Tensor, stream=None) -> torch.Tensor:
         cfg = self.cfg

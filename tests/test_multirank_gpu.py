@@ -27,7 +27,7 @@ def _cfg(field):
                      sort_every=4)
 
 
-def _worker(rank, world, port, field, out):
+def _worker(rank, world, port, field, out, peer=False):
     import torch
     import torch.distributed as dist
 
@@ -36,7 +36,9 @@ def _worker(rank, world, port, field, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2404_10270_b200 import Engine
 
-    eng = Engine(_cfg(field), device=torch.device("cuda", 0), rank=rank, world=world, check_every=0)
+    eng = Engine(_cfg(field), device=torch.device("cuda", 0), rank=rank, world=world, check_every=0,
+                 peer=peer)
+    assert (eng.peer is not None) == peer  # the peer-memory exchange mapped every rank's buffers
     assert eng._field_split()[0] if field else True  # the N>1 default overlaps the neutral push
     rhos = []
     for _ in range(9):
@@ -52,8 +54,12 @@ def _worker(rank, world, port, field, out):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("peer", [False, True])
 @pytest.mark.parametrize("field", [False, True])
-def test_two_ranks_match_one_rank_bitwise(cuda, tmp_path, field):
+def test_two_ranks_match_one_rank_bitwise(cuda, tmp_path, field, peer):
+    """peer False: reduce_bins (process-group allreduce) + pb_density_step;
+    peer True: pb_peer_density_step over CUDA IPC mappings (the NVLink path;
+    here two processes on one GPU)."""
     import torch
     import torch.multiprocessing as mp
 
@@ -63,7 +69,7 @@ def test_two_ranks_match_one_rank_bitwise(cuda, tmp_path, field):
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     out = str(tmp_path / "rho.npy")
-    mp.spawn(_worker, args=(2, port, field, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, port, field, out, peer), nprocs=2, join=True)
     got = np.load(out)
     eng = Engine(_cfg(field), device=cuda, check_every=0)
     want = []
