@@ -408,6 +408,10 @@ def run_ours(args, rank, world, local_rank):
             "particles_per_gpu": pushes_rank, "particles_total": pushes_total,
             "sort_every": cfg.sort_every, "sort_periods": eng.sort_periods,
             "parallelism": f"particle shards x{world}, replicated grid",
+            "density_exchange": ("none (one GPU)" if world == 1 else
+                                 "peer memory: pb_peer_density_step (bins summed over NVLink/IPC + epilogue, "
+                                 "one kernel)" if eng.peer is not None else
+                                 f"{args.dist_backend} all_reduce of the fixed-point bins + pb_density_step"),
             "l2": (f"inputs {alg_bytes / 1e9:.2f} GB/GPU vs 126 MB L2" +
                    ("; each step streams past L2, no flush needed" if alg_bytes > 2 * 126e6
                     else "; L2-resident, roofline not meaningful")),
