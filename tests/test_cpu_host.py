@@ -226,3 +226,19 @@ def test_bench_reference_arm_json_line():
     assert cb["value"] == line["value"] and cb["cores"] >= 1 and cb["kind"] in ("reference", "port")
     assert line["e2e"] == {"value": line["value"], "unit": line["unit"], "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
+
+
+def test_peer_status_maps_to_engine_error():
+    """PB_ERR_PEER (a GPU missed a density barrier) surfaces as EngineError."""
+    import pytest
+
+    from paper_2404_10270_b200 import _lib
+    from paper_2404_10270_b200.errors import EngineError
+
+    assert _lib.PB_ERR_PEER == 6
+    try:
+        _lib.load()
+    except ImportError:
+        pytest.skip("library not built")
+    with pytest.raises(EngineError):
+        _lib.check(_lib.PB_ERR_PEER, "peer")
