@@ -628,3 +628,78 @@ def test_charged_only_ring_bitwise_vs_oracle(cuda, bc):
             assert np.array_equal(bins[k, 0], R) and np.array_equal(bins[k, 1], C)
     if bc == "absorbing":
         assert eng.absorbed.sum() > 0
+
+
+def test_full_c2_sampled_particles_bitwise_vs_oracle(cuda):
+    """Config 2 at full size (30M particles, device init, the production
+    graph-replayed split mover): with E = 0 every particle evolves on its own,
+    so a random sample of 50K slots per species, pushed by the oracle from the
+    same initial state, must match the GPU bit for bit after 12 steps
+    (no sorting, so slots keep their particle); every particle is deposited
+    exactly once."""
+    import torch
+
+    from oracle import oracle
+    from paper_2404_10270_b200 import Engine
+
+    cfg = _mk_config(nc=100_000, ppc0=100, max_store_mb=65536, sort_every=0)
+    eng = Engine(cfg, device=cuda, init="device", check_every=0)
+    rng = np.random.default_rng(2024)
+    samples = []
+    for s in eng.sp:
+        idx = torch.from_numpy(np.sort(rng.choice(s.n, 50_000, replace=False))).to(cuda)
+        init = {f: t.index_select(0, idx).cpu().numpy() for f, t in s.arr.items()}
+        init["cell"] = s.cell.index_select(0, idx).cpu().numpy()
+        samples.append((idx, init))
+    eng.prepare_graphs(40)
+    eng.replay(12)
+    eng.sync()
+    e = np.zeros(eng.nc + 1)
+    for s, (idx, st) in zip(eng.sp, samples):
+        yp = st.get("yp")
+        for _ in range(12):
+            _, _, cfl = oracle.step_flat(s.kind, 0, s.fnstep, s.kick_coef, e, eng.nc, st["x"], st["vx"],
+                                         st["vy"], st["vz"], yp, st["cell"])
+            assert cfl == -1
+        for f, t in s.arr.items():
+            assert bits_equal(t.index_select(0, idx).cpu().numpy(), st[f]), (s.name, f)
+        assert np.array_equal(s.cell.index_select(0, idx).cpu().numpy(), st["cell"]), s.name
+    bins = eng.bins.cpu().numpy().view(np.uint64).reshape(eng.ndep, 2, eng.nc)
+    assert int(bins[:, 1].sum()) == 2 * 10_000_000
+
+
+def test_full_c4_sampled_particles_bitwise_vs_oracle(cuda):
+    """Config 4 at full size (100M particles, Boris push with the oblique B,
+    field solve): each step's E is taken from the engine and a 30K-slot
+    sample per species is pushed by the oracle with it; the GPU's particles
+    must match bit for bit after every step."""
+    import os
+
+    import torch
+
+    from oracle import oracle
+    from paper_2404_10270_b200 import Engine, load_config
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cfg = load_config(os.path.join(root, "configs", "c4_sol_boris.toml"))
+    eng = Engine(cfg, device=cuda, init="device", check_every=0)
+    assert any(s.boris is not None for s in eng.sp)
+    rng = np.random.default_rng(4)
+    samples = []
+    for s in eng.sp:
+        idx = torch.from_numpy(np.sort(rng.choice(s.n, 30_000, replace=False))).to(cuda)
+        st = {f: t.index_select(0, idx).cpu().numpy() for f, t in s.arr.items()}
+        st["cell"] = s.cell.index_select(0, idx).cpu().numpy()
+        samples.append((idx, st))
+    for _ in range(4):
+        eng.step()
+        e = eng.e.cpu().numpy()
+        for s, (idx, st) in zip(eng.sp, samples):
+            bt, bs = s.boris if s.boris is not None else (None, None)
+            _, _, cfl = oracle.step_flat(s.kind, 0, s.fnstep, s.kick_coef, e, eng.nc, st["x"], st["vx"],
+                                         st["vy"], st["vz"], st.get("yp"), st["cell"], bt, bs)
+            assert cfl == -1
+            for f, t in s.arr.items():
+                assert bits_equal(t.index_select(0, idx).cpu().numpy(), st[f]), (s.name, f)
+            assert np.array_equal(s.cell.index_select(0, idx).cpu().numpy(), st["cell"]), s.name
+    eng.sync()
