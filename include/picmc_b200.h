@@ -414,7 +414,7 @@ int pb_repack(const double *src, double *dst, const int64_t *offs_old,
  * left/right/rho there and stores the slice into every rank's buffers, with
  * flag barriers in peer memory.  Replaces reduce_bins (the NCCL allreduce)
  * + pb_density_step; bitwise the same result.  All ranks call it with the
- * same epoch sequence (1, 2, ...), grid and nc. */
+ * same epoch sequence (1, 2, ... or a device counter), grid and nc. */
 #define PB_MAX_RANKS 8
 #define PB_PEER_HANDLE_BYTES 64 /* sizeof(cudaIpcMemHandle_t) */
 
@@ -426,7 +426,10 @@ typedef struct pb_peer_density {
   uint64_t *flags[PB_MAX_RANKS]; /* 2 * world zeroed words per rank */
   int rank;
   int world;
-  uint64_t epoch;                /* 1, 2, ... one per call */
+  uint64_t epoch;                /* 1, 2, ... one per call (when epoch_dev is NULL) */
+  uint64_t *epoch_dev;           /* or: a zeroed device counter of this rank, read as
+                                    epoch - 1 and advanced after the exchange, so the
+                                    call can be captured in a CUDA graph */
 } pb_peer_density;
 
 /* cudaMalloc + zero + IPC handle (PB_PEER_HANDLE_BYTES) for a buffer peers map. */

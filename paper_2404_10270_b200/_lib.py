@@ -89,7 +89,7 @@ PB_PEER_HANDLE_BYTES = 64
 class PbPeerDensity(ctypes.Structure):
     _fields_ = [("bins", _p * PB_MAX_RANKS), ("left", _p * PB_MAX_RANKS), ("right", _p * PB_MAX_RANKS),
                 ("rho", _p * PB_MAX_RANKS), ("flags", _p * PB_MAX_RANKS), ("rank", ctypes.c_int),
-                ("world", ctypes.c_int), ("epoch", ctypes.c_uint64)]
+                ("world", ctypes.c_int), ("epoch", ctypes.c_uint64), ("epoch_dev", _p)]
 
 
 class PbCellFields(ctypes.Structure):

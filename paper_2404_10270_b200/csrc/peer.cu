@@ -41,6 +41,7 @@ struct PeerArgs {
   int ndep, rank, world, field_bc;
   int64_t nc;
   unsigned long long epoch;
+  const unsigned long long *epoch_dev;  // device epoch counter (graph replay), or null
   pb_status *st;
 };
 
@@ -93,14 +94,16 @@ __device__ __forceinline__ void reduced_partials(const PeerArgs &a, int64_t c, d
 
 __global__ void __launch_bounds__(kPeerThreads) k_peer_density(const __grid_constant__ PeerArgs a) {
   pdl_enter();
+  // bumped by k_peer_epoch after this grid
+  const unsigned long long epoch = a.epoch_dev ? *a.epoch_dev + 1 : a.epoch;
   const int64_t nc = a.nc;
   // A: announce that this rank's bins are final, wait for every rank
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     __threadfence_system();
-    for (int r = 0; r < a.world; ++r) st_release_sys(a.flags[r] + a.rank, a.epoch);
+    for (int r = 0; r < a.world; ++r) st_release_sys(a.flags[r] + a.rank, epoch);
   }
   __shared__ int ok;
-  if (threadIdx.x == 0) ok = peer_wait(a, 0, a.epoch);
+  if (threadIdx.x == 0) ok = peer_wait(a, 0, epoch);
   __syncthreads();
   // this rank's cells [c0, c1) and nodes [c0, c1) (the last rank also node nc)
   const int64_t c0 = nc * a.rank / a.world, c1 = nc * (a.rank + 1) / a.world;
@@ -140,7 +143,7 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_density(const __grid_cons
     __threadfence_system();
     for (int r = 0; r < a.world; ++r)
       atomicAdd_system(a.flags[r] + a.world + a.rank, 1ull);
-    ok = ok && peer_wait(a, a.world, a.epoch * (unsigned long long)gridDim.x);
+    ok = ok && peer_wait(a, a.world, epoch * (unsigned long long)gridDim.x);
   }
   __syncthreads();
   // every rank is past its reads: clear this rank's bins (and, if asked, the
@@ -152,6 +155,13 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_density(const __grid_cons
     mine[w] = 0;
     if (a.clear_next) a.clear_next[w] = 0;
   }
+}
+
+// The device epoch advances once per exchange, stream-ordered after the
+// exchange kernel (so a captured step replays with a fresh epoch each time).
+__global__ void k_peer_epoch(unsigned long long *epoch) {
+  pdl_enter();
+  *epoch += 1;
 }
 
 }  // namespace pb
@@ -194,7 +204,7 @@ extern "C" int pb_peer_density_step(const pb_peer_density *p, uint64_t *bins_nex
                                     const double *coef, int ndep, int64_t nc, int field_bc,
                                     pb_status *status, void *stream) {
   if (!p || p->world < 1 || p->world > PB_MAX_RANKS || p->rank < 0 || p->rank >= p->world ||
-      ndep < 0 || ndep > PB_MAX_SPECIES || nc < 2 || !status || p->epoch == 0 ||
+      ndep < 0 || ndep > PB_MAX_SPECIES || nc < 2 || !status || (p->epoch == 0 && !p->epoch_dev) ||
       (ndep > 0 && !coef) ||
       (field_bc != PB_FIELD_PERIODIC && field_bc != PB_FIELD_DIRICHLET)) {
     pb::set_error("pb_peer_density_step: bad arguments");
@@ -220,6 +230,7 @@ extern "C" int pb_peer_density_step(const pb_peer_density *p, uint64_t *bins_nex
   a.field_bc = field_bc;
   a.nc = nc;
   a.epoch = p->epoch;
+  a.epoch_dev = (const unsigned long long *)p->epoch_dev;
   a.clear_next = bins_next;
   a.st = status;
   // persistent grid: every block must be resident to reach the barriers
@@ -234,5 +245,10 @@ extern "C" int pb_peer_density_step(const pb_peer_density *p, uint64_t *bins_nex
   cudaError_t e = pb::launch_pdl(pb::k_peer_density, dim3((unsigned)blocks), dim3(pb::kPeerThreads),
                                  0, (cudaStream_t)stream, a);
   if (e != cudaSuccess) return pb::cuda_status(e, "k_peer_density");
+  if (p->epoch_dev) {
+    e = pb::launch_pdl(pb::k_peer_epoch, dim3(1), dim3(1), 0, (cudaStream_t)stream,
+                       (unsigned long long *)p->epoch_dev);
+    if (e != cudaSuccess) return pb::cuda_status(e, "k_peer_epoch");
+  }
   return PB_OK;
 }

@@ -334,7 +334,9 @@ class Engine:
             return
         torch.cuda.synchronize(self.device)  # the buffers were zeroed on the legacy stream
         self.peer = pb
-        self._peer_epoch = 0
+        # exchange epochs live on the device (advanced by the exchange itself),
+        # so steps with the exchange can be captured in CUDA graphs
+        self._peer_epoch_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.bins_pp = [pb.tensor("bins0", nbins, torch.int64), pb.tensor("bins1", nbins, torch.int64)]
         self.rho = pb.tensor("rho", nc + 1, torch.float64)
         self.left = pb.tensor("left", nc, torch.float64)
@@ -344,7 +346,6 @@ class Engine:
         """pb_peer_density_step: every rank's bins summed over NVLink and the
         epilogue, one kernel (replaces reduce_bins + pb_density_step)."""
         pb = self.peer
-        self._peer_epoch += 1
         d = _lib.PbPeerDensity()
         key = "bins%d" % self.cur
         for r in range(self.world):
@@ -353,7 +354,8 @@ class Engine:
             d.right[r] = pb.ptrs["right"][r]
             d.rho[r] = pb.ptrs["rho"][r]
             d.flags[r] = pb.ptrs["flags"][r]
-        d.rank, d.world, d.epoch = self.rank, self.world, self._peer_epoch
+        d.rank, d.world, d.epoch = self.rank, self.world, 0
+        d.epoch_dev = self._peer_epoch_dev.data_ptr()
         nxt = self.bins_pp[1 - self.cur].data_ptr() if clear_next else None
         _lib.check(self.lib.pb_peer_density_step(ctypes.byref(d), nxt, self._coef_c, self.ndep, self.nc,
                                                  self.field_bc, self.status.data_ptr(),
@@ -612,7 +614,7 @@ class Engine:
             delivered += n
 
         with_input = e_source is not None
-        use_graphs = self.world == 1 and (not with_input or not self.cfg.field_solve)
+        use_graphs = self._graphs_ok() and (not with_input or not self.cfg.field_solve)
         k, b = 0, 0
         while k < steps:
             gp = b % 2
@@ -760,16 +762,22 @@ class Engine:
         steps: both bin parities x both buffers of every species whose sort
         falls in that window.  Capturing launches nothing, so the buffer swaps
         here are pointer bookkeeping only; timed replays then never capture."""
-        if self.world > 1:
-            return  # multi-GPU steps replay eagerly: no NCCL collectives inside graphs
+        if not self._graphs_ok():
+            return  # NCCL-exchange steps replay eagerly: no collectives inside graphs
         self._each_buffer_state(horizon, lambda: None if self._graph_key() in self.graphs
                                 else self._capture())
+
+    def _graphs_ok(self) -> bool:
+        """Steps are graph-capturable on one GPU and with the peer-memory
+        density exchange (its epochs are device-side); the NCCL exchange
+        runs eagerly."""
+        return self.world == 1 or self.peer is not None
 
     def prepare_pipe_graphs(self, with_input: bool, horizon: int = None, group: int = None):
         """The same for run_pipelined's graphs (single steps and `group`-step
         blocks, both pipe parities; with_input: E comes from the pipe's device
         slots)."""
-        if self.world > 1 or (with_input and self.cfg.field_solve):
+        if not self._graphs_ok() or (with_input and self.cfg.field_solve):
             return
         group = self._pipe_group(group)
         self._pipe_buffers(group)
@@ -828,7 +836,7 @@ class Engine:
         try:
             left = steps
             while left > 0:
-                if self.world == 1 and left >= 2 and not self._sort_due(1) and not self._sort_due(2):
+                if self._graphs_ok() and left >= 2 and not self._sort_due(1) and not self._sort_due(2):
                     g = self.graphs.get(self._graph_key())
                     if g is None:
                         g = self.capture()

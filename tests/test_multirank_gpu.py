@@ -44,7 +44,8 @@ def _worker(rank, world, port, field, out, peer=False):
     for _ in range(9):
         rho, e = eng.step()
         rhos.append(rho.cpu().numpy().copy())
-    eng.replay(6)  # eager for N > 1
+    eng.replay(6)  # graphs with the peer exchange, eager with the process-group allreduce
+    assert (len(eng.graphs) > 0) == peer
     rho, _ = eng.step()
     rhos.append(rho.cpu().numpy().copy())
     eng.sync()
