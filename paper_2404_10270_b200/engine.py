@@ -257,6 +257,13 @@ class Engine:
                 else:
                     raise ValueError(f"unknown init mode {init!r}")
         self.deposit_current()
+        self._publish()
+
+    def _publish(self):
+        """Order the caller's current stream after the engine stream, so
+        state written by the engine (init, upload, sort) is what the caller
+        reads next."""
+        torch.cuda.current_stream(self.device).wait_stream(self.stream)
 
     def _sh(self):
         return ctypes.c_void_p(self.stream.cuda_stream)
@@ -300,6 +307,7 @@ class Engine:
                     raise ValueError("particle count mismatch")
                 s.upload(f)
         self.deposit_current()
+        self._publish()
 
     # -- step phases ------------------------------------------------------------
     def density(self, stream=None, clear_next: bool = True) -> torch.Tensor:
@@ -501,6 +509,7 @@ class Engine:
                     pbs = s.pb(n)
                     _lib.check(self.lib.pb_cell8_build(ctypes.byref(pbs), self._sh()), "pb_cell8_build")
             self._arr = None  # graphs are keyed by buffer addresses (_graph_key)
+        self._publish()
 
     def step(self, timed: bool = False, e_ext: torch.Tensor = None):
         """One full cycle.  Returns rho/E of this step (device tensors).
