@@ -866,6 +866,20 @@ class Engine:
             self.sync()
 
     # -- status handling ------------------------------------------------------------
+    def close(self):
+        """Release the peer-memory exchange buffers (N > 1): wait for the
+        engine's work, drop the tensors that alias them, unmap the peers'
+        buffers and free this rank's.  Every rank calls it; the engine is
+        unusable afterwards."""
+        if self.peer is None:
+            return
+        self.stream.synchronize()
+        self._side.synchronize()
+        self.graphs.clear()
+        self.bins_pp = self.rho = self.left = self.right = None
+        self.peer.close()
+        self.peer = None
+
     def sync(self):
         """Wait for enqueued work, fold the sticky device status into the
         host tallies, raise the first recorded error, and reset the status."""

@@ -52,6 +52,8 @@ def _worker(rank, world, port, field, out, peer=False):
     if rank == 0:
         np.save(out, np.array(rhos))
     dist.barrier()
+    eng.close()
+    dist.barrier()
     dist.destroy_process_group()
 
 
