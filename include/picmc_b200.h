@@ -233,6 +233,12 @@ int pb_solve_poisson_scan(const double *rho, double *phi, int64_t nc,
                           void *stream);
 int pb_compute_efield(const double *phi, double *e, int64_t nc, double dx,
                       int field_bc, void *stream);
+/* pb_compute_efield, then zero nwords words of clr_a and clr_b (either may
+ * be NULL): the serial field-solve cycle clears the bins read by
+ * pb_rho_epilogue here. */
+int pb_compute_efield_clear(const double *phi, double *e, int64_t nc,
+                            double dx, int field_bc, uint64_t *clr_a,
+                            uint64_t *clr_b, int64_t nwords, void *stream);
 
 /* smoothing (passes > 0: rho_s receives the smoothed density) + the scan
  * Poisson solve + E in one cooperative launch with grid-wide syncs between

@@ -136,6 +136,7 @@ _SIGS = {
     "pb_solve_poisson_scan": (ctypes.c_int, [_p, _p, _i64, _f64, _f64, ctypes.c_int,
                                              _f64, _f64, _p, _p]),
     "pb_compute_efield": (ctypes.c_int, [_p, _p, _i64, _f64, ctypes.c_int, _p]),
+    "pb_compute_efield_clear": (ctypes.c_int, [_p, _p, _i64, _f64, ctypes.c_int, _p, _p, _i64, _p]),
     "pb_field_pipeline": (ctypes.c_int, [_p, _p, _p, _p, _i64, ctypes.c_int, _f64, _f64, ctypes.c_int,
                                          _f64, _f64, _p, _p]),
     "pb_stream_sol": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int, _p]),

@@ -60,6 +60,7 @@ __global__ void k_rho_epilogue(const uint64_t *__restrict__ bins, CoefArgs ca,
                                double *__restrict__ rho,
                                uint64_t *__restrict__ clear,
                                uint64_t *__restrict__ counter) {
+  pdl_enter();
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g > nc) return;
   // Step fusion: zero the other (ping-pong) bin set for the coming mover
@@ -175,9 +176,10 @@ static int rho_epilogue(const uint64_t *bins, const double *coef, int ndep, int6
   for (int s = 0; s < ndep; ++s) ca.c[s] = coef[s];
   const int threads = 256;
   const int64_t blocks = (nc + 1 + threads - 1) / threads;
-  pb::k_rho_epilogue<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(
-      bins, ca, ndep, nc, field_bc, left, right, rho, clear, counter);
-  PB_CHECK_LAUNCH("k_rho_epilogue");
+  cudaError_t e = pb::launch_pdl(pb::k_rho_epilogue, dim3((unsigned)blocks), dim3(threads), 0,
+                                  (cudaStream_t)stream, bins, ca, ndep, nc, field_bc, left, right,
+                                  rho, clear, counter);
+  if (e != cudaSuccess) return pb::cuda_status(e, "k_rho_epilogue");
   return PB_OK;
 }
 

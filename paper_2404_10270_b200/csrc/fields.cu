@@ -427,6 +427,22 @@ __global__ void __launch_bounds__(kMbThreads) k_field_coop(const CoopArgs c) {
   for (int64_t j = gtid; j <= nc; j += gsz) efield_node(a.phi, c.e, nc, c.two_dx, a.field_bc, j);
 }
 
+// E from phi, then zero bin sets whose density has been taken (the serial
+// field-solve cycle reads the bins with the one-kernel epilogue, which does
+// not clear them -- neighbouring nodes read the same cells -- and clears
+// them here, one launch later, before the push deposits again).
+__global__ void k_efield_clear(const double *__restrict__ phi, double *__restrict__ e, int64_t nc,
+                               double two_dx, int field_bc, uint64_t *__restrict__ clr_a,
+                               uint64_t *__restrict__ clr_b, int64_t nwords) {
+  pdl_enter();
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g <= nc) efield_node(phi, e, nc, two_dx, field_bc, g);
+  for (int64_t w = g; w < nwords; w += (int64_t)gridDim.x * blockDim.x) {
+    if (clr_a) clr_a[w] = 0;
+    if (clr_b) clr_b[w] = 0;
+  }
+}
+
 static unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 static PoissonArgs poisson_args(const double *rho, double *phi, int64_t nc, double dx, double eps0,
@@ -625,4 +641,18 @@ extern "C" int pb_field_pipeline(const double *rho, double *rho_s, double *phi, 
   rc = pb_solve_poisson_scan(src, phi, nc, dx, eps0, field_bc, phi_left, phi_right, scratch, stream);
   if (rc) return rc;
   return pb_compute_efield(phi, e, nc, dx, field_bc, stream);
+}
+
+extern "C" int pb_compute_efield_clear(const double *phi, double *e, int64_t nc, double dx,
+                                       int field_bc, uint64_t *clr_a, uint64_t *clr_b,
+                                       int64_t nwords, void *stream) {
+  if (nc < 3 || !phi || !e || nwords < 0) {
+    pb::set_error("pb_compute_efield_clear: bad arguments");
+    return PB_ERR_INVALID;
+  }
+  cudaError_t err = pb::launch_pdl(pb::k_efield_clear, dim3(pb::blocks_for(nc + 1, 256)), dim3(256), 0,
+                                   (cudaStream_t)stream, phi, e, nc, 2.0 * dx, field_bc, clr_a, clr_b,
+                                   nwords);
+  if (err != cudaSuccess) return pb::cuda_status(err, "k_efield_clear");
+  return PB_OK;
 }

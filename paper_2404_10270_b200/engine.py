@@ -106,6 +106,9 @@ class Engine:
     # (configs 4 and 3), so it is opt-in: PB_FUSED_FIELD=1
     fused_field = os.environ.get("PB_FUSED_FIELD", "0") == "1"
     supports_peer = True  # the fused peer-memory density exchange (N > 1)
+    # serial field-solve cycle: density in one pb_rho_epilogue launch, bins
+    # cleared by the E kernel (PB_DENSITY_ONE=0: pb_density_step's two launches)
+    density_one = os.environ.get("PB_DENSITY_ONE", "1") != "0"
 
     def __init__(self, config, device=None, *, rank: int = 0, world: int = 1,
                  group=None, init: str = "host", check_every: int = 1, peer: bool = None):
@@ -369,7 +372,7 @@ class Engine:
                                                  self.field_bc, self.status.data_ptr(),
                                                  ctypes.c_void_p(st.cuda_stream)), "pb_peer_density_step")
 
-    def field(self, rho: torch.Tensor, stream=None) -> torch.Tensor:
+    def field(self, rho: torch.Tensor, stream=None, clear=None) -> torch.Tensor:
         cfg = self.cfg
         if not cfg.field_solve:
             return self.e  # stays identically zero (harness.py:177-178)
@@ -393,8 +396,16 @@ class Engine:
             _lib.check(solve(src.data_ptr(), self.phi.data_ptr(), self.nc, self.grid.dx_m,
                              cfg.consts.epsilon0, self.field_bc, cfg.phi_left,
                              cfg.phi_right, scr, sh), "poisson")
-            _lib.check(self.lib.pb_compute_efield(self.phi.data_ptr(), self.e.data_ptr(), self.nc,
-                                                  self.grid.dx_m, self.field_bc, sh), "pb_compute_efield")
+            if clear is not None:
+                # the bins read by the one-kernel epilogue (and the set the
+                # coming push deposits into) are zeroed with E
+                a, b = clear
+                _lib.check(self.lib.pb_compute_efield_clear(
+                    self.phi.data_ptr(), self.e.data_ptr(), self.nc, self.grid.dx_m, self.field_bc,
+                    a.data_ptr(), b.data_ptr(), a.numel(), sh), "pb_compute_efield_clear")
+            else:
+                _lib.check(self.lib.pb_compute_efield(self.phi.data_ptr(), self.e.data_ptr(), self.nc,
+                                                      self.grid.dx_m, self.field_bc, sh), "pb_compute_efield")
         return self.e
 
     def _subset(self, which):
@@ -425,6 +436,18 @@ class Engine:
             return [], list(range(len(self.sp)))
         return neutral, rest
 
+    def _density_one(self) -> torch.Tensor:
+        """left/right/rho in one pb_rho_epilogue launch; the bins stay set
+        until the E kernel of the same step clears them."""
+        with torch.cuda.stream(self.stream):
+            if self.world > 1:
+                reduce_bins(self.bins, self.group)
+            _lib.check(self.lib.pb_rho_epilogue(
+                self.bins.data_ptr(), self._coef_c, self.ndep, self.nc, self.field_bc, self.left.data_ptr(),
+                self.right.data_ptr(), self.rho.data_ptr(), self._sh()), "pb_rho_epilogue")
+        self._next_clear = True
+        return self.rho
+
     def _field_cycle(self):
         """Field-solve step body.  The species that need no field (neutral
         movers) are pushed on the engine stream while the density epilogue
@@ -433,8 +456,14 @@ class Engine:
         movers this is the plain serial cycle."""
         neutral, rest = self._field_split()
         if not neutral:
-            rho = self.density()
-            e = self.field(rho)
+            if self.density_one and not self.fused_field and self.peer is None:
+                # one-kernel epilogue (no self-clear: neighbouring nodes read
+                # the same cells); E clears the bins (bitwise density())
+                rho = self._density_one()
+                e = self.field(rho, clear=(self.bins_pp[self.cur], self.bins_pp[1 - self.cur]))
+            else:
+                rho = self.density()
+                e = self.field(rho)
             if self.cfg.smoothing_passes > 0:
                 rho = self.rho_s
             self.push(e)

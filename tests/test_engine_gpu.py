@@ -743,3 +743,41 @@ def test_full_c5_sampled_particles_bitwise_vs_oracle(cuda):
     assert int(bins[:, 1].sum()) == sum(s.n for s in eng.sp if s.deposit >= 0)
     del eng
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("bc", ["periodic", "dirichlet"])
+@pytest.mark.parametrize("passes", [0, 1])
+def test_one_kernel_density_matches_two_kernel_epilogue(cuda, bc, passes):
+    """Serial field-solve cycle: the one-launch epilogue (pb_rho_epilogue)
+    with the bins cleared by the E kernel gives bitwise the two-launch
+    pb_density_step cycle -- rho, rho_s, phi, E, partials, both bin sets and
+    every particle -- eager and graph-replayed."""
+    from oracle import oracle
+    from paper_2404_10270_b200 import Engine
+
+    kw = dict(field_solve=True, smoothing_passes=passes, boundary=bc, phi_left=1.5, phi_right=-0.5)
+    if bc == "dirichlet":
+        kw["particle_boundary"] = "absorbing"
+    cfg = _mk_config(nc=3000, ppc0=4, **kw)
+    flats = _random_flats(cfg, 19, vscale=0.45)
+    a = Engine(cfg, device=cuda, check_every=0)
+    b = Engine(cfg, device=cuda, check_every=0)
+    a.density_one, b.density_one = False, True
+    a.upload(flats)
+    b.upload(flats)
+    for _ in range(3):
+        a.step()
+        b.step()
+    b.prepare_graphs(40)
+    for _ in range(6):
+        a.step()
+    b.replay(6)
+    a.sync()
+    b.sync()
+    for name in ("rho", "rho_s", "phi", "e", "left", "right"):
+        assert bits_equal(getattr(a, name).cpu().numpy(), getattr(b, name).cpu().numpy()), name
+    assert np.array_equal(a.moved, b.moved) and np.array_equal(a.absorbed, b.absorbed)
+    assert np.array_equal(a.bins_pp[0].cpu().numpy(), b.bins_pp[0].cpu().numpy())
+    assert np.array_equal(a.bins_pp[1].cpu().numpy(), b.bins_pp[1].cpu().numpy())
+    for x, y in zip(a.download(), b.download()):
+        assert np.array_equal(oracle.canonical(x.cell, x.fields()), oracle.canonical(y.cell, y.fields()))
