@@ -439,6 +439,105 @@ static size_t offsets_tmp_bytes(int64_t nc) {
   return a256((size_t)(nc + 1) * 8) + a256(scan_temp_bytes(nc));
 }
 
+// ---- canonical resort as a scatter (no full key sort) ----------------------
+// The canonical order is (dest cell, moved, rank): within every cell first
+// the particles that stayed, in their pre-move rank order, then the
+// incomers in rank order.  The stayers' relative order is unchanged, so
+// their new slot is new_off[cell] + (stayers with a smaller rank in the cell)
+// = new_off[c] + G[rank] - G[offp[c]] with G the exclusive prefix count of
+// stayers over the pre-move ranks; only the movers (~0.6% of electrons per
+// step) are sorted by key.  Same final order as sorting every key.
+__global__ void k_scat_classify(const uint64_t *__restrict__ keys, int64_t n, int rank_bits,
+                                uint32_t *__restrict__ stay_by_rank, int64_t *__restrict__ cnt_stay,
+                                int64_t *__restrict__ cnt_in, uint64_t *__restrict__ mkeys,
+                                uint32_t *__restrict__ midx, unsigned long long *__restrict__ mcount) {
+  const uint64_t rmask = (1ull << rank_bits) - 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = keys[i];
+    if (key == kDeadKey) continue;
+    const int64_t dest = (int64_t)((key >> rank_bits) >> 1);
+    const bool mv = (key >> rank_bits) & 1ull;
+    const uint64_t rank = key & rmask;
+    if (!mv) {
+      stay_by_rank[rank] = 1u;
+      atomicAdd((unsigned long long *)&cnt_stay[dest], 1ull);
+    } else {
+      const unsigned long long t = atomicAdd(mcount, 1ull);
+      mkeys[t] = key;
+      midx[t] = (uint32_t)i;
+      atomicAdd((unsigned long long *)&cnt_in[dest], 1ull);
+    }
+  }
+}
+
+struct ScatArgs {
+  const double *src[5];
+  double *dst[5];
+  int nf;
+  int rank_bits;
+  const uint64_t *keys;
+  const uint32_t *G;
+  const int64_t *offp, *new_off, *cnt_stay, *in_off;
+  const uint64_t *mkeys_s;
+  const uint32_t *midx_s;
+  int32_t *cell_out;
+};
+
+__global__ void k_scat_stay(const __grid_constant__ ScatArgs a, int64_t n) {
+  const uint64_t rmask = (1ull << a.rank_bits) - 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = a.keys[i];
+    if (key == kDeadKey || ((key >> a.rank_bits) & 1ull)) continue;
+    const int64_t c = (int64_t)((key >> a.rank_bits) >> 1);
+    const uint64_t rank = key & rmask;
+    const int64_t pos = a.new_off[c] + (int64_t)a.G[rank] - (int64_t)a.G[a.offp[c]];
+#pragma unroll
+    for (int f = 0; f < 5; ++f)
+      if (f < a.nf) a.dst[f][pos] = __ldg(a.src[f] + i);
+    a.cell_out[pos] = (int32_t)c;
+  }
+}
+
+__global__ void k_scat_movers(const __grid_constant__ ScatArgs a, int64_t m) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = a.mkeys_s[t];
+    const int64_t d = (int64_t)((key >> a.rank_bits) >> 1);
+    const int64_t pos = a.new_off[d] + a.cnt_stay[d] + (t - a.in_off[d]);
+    const uint32_t i = a.midx_s[t];
+#pragma unroll
+    for (int f = 0; f < 5; ++f)
+      if (f < a.nf) a.dst[f][pos] = __ldg(a.src[f] + i);
+    a.cell_out[pos] = (int32_t)d;
+  }
+}
+
+__global__ void k_add_counts(const int64_t *__restrict__ a, const int64_t *__restrict__ b,
+                             int64_t *__restrict__ out, int64_t nc) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nc;
+       j += (int64_t)gridDim.x * blockDim.x)
+    out[j] = a[j] + b[j];
+}
+
+static bool canon_scatter_enabled() {
+  static const bool on = !(getenv("PB_CANON_SCATTER") && atoi(getenv("PB_CANON_SCATTER")) == 0);
+  return on;
+}
+
+static size_t scan_u32_bytes(int64_t n) {
+  size_t t = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, t, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                (int)(n + 1));
+  return t;
+}
+
+static size_t scatter_extra_bytes(int64_t n, int64_t nc) {
+  return 2 * a256((size_t)(n + 1) * 4) + a256((size_t)n * 8) + 3 * a256((size_t)(nc + 1) * 8) +
+         a256(8) + a256(scan_u32_bytes(n));
+}
+
 }  // namespace pb
 
 // ---------------------------------------------------------------------------
@@ -522,7 +621,8 @@ extern "C" size_t pb_canonical_scratch_bytes(int64_t n_cap, int64_t nc) {
   if (n_cap < 1) n_cap = 1;
   return 2 * pb::a256((size_t)n_cap * 8) + 2 * pb::a256((size_t)n_cap * 4) +
          pb::a256((size_t)(nc + 1) * 8) + pb::a256((size_t)nc * 8) +
-         pb::a256(pb::sort_temp_bytes(n_cap)) + pb::offsets_tmp_bytes(nc);
+         pb::a256(pb::sort_temp_bytes(n_cap)) + pb::offsets_tmp_bytes(nc) +
+         pb::scatter_extra_bytes(n_cap, nc);
 }
 
 extern "C" int pb_canonical_resort(const pb_species *src, const pb_species *dst,
@@ -589,13 +689,6 @@ extern "C" int pb_canonical_resort(const pb_species *src, const pb_species *dst,
   rc = pb::launch_canon_push(src, cv, e_nodes, nc, particle_bc, species_id, status, 0, rank_bits,
                              offp, keys, vals, st);
   if (rc) return rc;
-  size_t tb = pb::sort_temp_bytes(n_tot);
-  err = cub::DeviceRadixSort::SortPairs(sort_tmp, tb, keys, keys_s, vals, perm, (int)n_tot, 0,
-                                        key_bits, st);
-  if (err != cudaSuccess) return pb::cuda_status(err, "DeviceRadixSort::SortPairs");
-  // Dead keys have every bit set, so they also sort last inside key_bits.
-  err = cudaMemsetAsync(cv->counts, 0, (size_t)nc * 8, st);
-  if (err != cudaSuccess) return pb::cuda_status(err, "cudaMemsetAsync");
   pb::GatherArgs g;
   int nf = 0;
   g.src[nf] = src->x; g.dst[nf++] = dst->x;
@@ -607,6 +700,87 @@ extern "C" int pb_canonical_resort(const pb_species *src, const pb_species *dst,
     g.dst[nf++] = dst->yp;
   }
   g.nf = nf;
+  if (pb::canon_scatter_enabled()) {
+    // scatter path (see k_scat_classify): extra scratch after the sort path's
+    char *q = scan_tmp + pb::offsets_tmp_bytes(nc);
+    uint32_t *stay = (uint32_t *)q;
+    q += pb::a256((size_t)(n_tot + 1) * 4);
+    uint32_t *G = (uint32_t *)q;
+    q += pb::a256((size_t)(n_tot + 1) * 4);
+    uint64_t *mkeys_s = (uint64_t *)q;
+    q += pb::a256((size_t)n_tot * 8);
+    int64_t *cnt_stay = (int64_t *)q;
+    q += pb::a256((size_t)(nc + 1) * 8);
+    int64_t *cnt_in = (int64_t *)q;
+    q += pb::a256((size_t)(nc + 1) * 8);
+    int64_t *in_off = (int64_t *)q;
+    q += pb::a256((size_t)(nc + 1) * 8);
+    unsigned long long *mcount = (unsigned long long *)q;
+    q += pb::a256(8);
+    char *u32_tmp = q;
+    const int64_t R = n_tot;  // pre-move ranks lie in [0, offp[nc]) <= n_tot
+    err = cudaMemsetAsync(stay, 0, (size_t)(R + 1) * 4, st);
+    if (err == cudaSuccess) err = cudaMemsetAsync(cnt_stay, 0, (size_t)(nc + 1) * 8, st);
+    if (err == cudaSuccess) err = cudaMemsetAsync(cnt_in, 0, (size_t)(nc + 1) * 8, st);
+    if (err == cudaSuccess) err = cudaMemsetAsync(mcount, 0, 8, st);
+    if (err != cudaSuccess) return pb::cuda_status(err, "cudaMemsetAsync");
+    int64_t blocks = (n_tot + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    pb::k_scat_classify<<<(unsigned)blocks, 256, 0, st>>>(keys, n_tot, rank_bits, stay, cnt_stay,
+                                                          cnt_in, keys_s, vals, mcount);
+    PB_CHECK_LAUNCH("k_scat_classify");
+    size_t tb = pb::scan_u32_bytes(R);
+    err = cub::DeviceScan::ExclusiveSum(u32_tmp, tb, stay, G, (int)(R + 1), st);
+    if (err != cudaSuccess) return pb::cuda_status(err, "DeviceScan (stayers)");
+    pb::k_add_counts<<<148, 256, 0, st>>>(cnt_stay, cnt_in, cv->counts, nc);
+    PB_CHECK_LAUNCH("k_add_counts");
+    rc = pb::offsets_from_counts(cv->counts, cv->offs, nc, scan_tmp, st);
+    if (rc) return rc;
+    rc = pb::offsets_from_counts(cnt_in, in_off, nc, scan_tmp, st);
+    if (rc) return rc;
+    unsigned long long m = 0;
+    err = cudaMemcpyAsync(&m, mcount, 8, cudaMemcpyDeviceToHost, st);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+    if (err != cudaSuccess) return pb::cuda_status(err, "mover count");
+    if (m > 0) {
+      size_t sb = pb::sort_temp_bytes((int64_t)m);
+      err = cub::DeviceRadixSort::SortPairs(sort_tmp, sb, keys_s, mkeys_s, vals, perm, (int)m, 0,
+                                            key_bits, st);
+      if (err != cudaSuccess) return pb::cuda_status(err, "DeviceRadixSort::SortPairs (movers)");
+    }
+    pb::ScatArgs sa;
+    for (int f = 0; f < 5; ++f) {
+      sa.src[f] = f < nf ? g.src[f] : nullptr;
+      sa.dst[f] = f < nf ? g.dst[f] : nullptr;
+    }
+    sa.nf = nf;
+    sa.rank_bits = rank_bits;
+    sa.keys = keys;
+    sa.G = G;
+    sa.offp = offp;
+    sa.new_off = cv->offs;
+    sa.cnt_stay = cnt_stay;
+    sa.in_off = in_off;
+    sa.mkeys_s = mkeys_s;
+    sa.midx_s = perm;
+    sa.cell_out = dst->cell;
+    pb::k_scat_stay<<<(unsigned)blocks, 256, 0, st>>>(sa, n_tot);
+    PB_CHECK_LAUNCH("k_scat_stay");
+    if (m > 0) {
+      int64_t mb = ((int64_t)m + 255) / 256;
+      if (mb > 148 * 16) mb = 148 * 16;
+      pb::k_scat_movers<<<(unsigned)mb, 256, 0, st>>>(sa, (int64_t)m);
+      PB_CHECK_LAUNCH("k_scat_movers");
+    }
+    return PB_OK;
+  }
+  size_t tb = pb::sort_temp_bytes(n_tot);
+  err = cub::DeviceRadixSort::SortPairs(sort_tmp, tb, keys, keys_s, vals, perm, (int)n_tot, 0,
+                                        key_bits, st);
+  if (err != cudaSuccess) return pb::cuda_status(err, "DeviceRadixSort::SortPairs");
+  // Dead keys have every bit set, so they also sort last inside key_bits.
+  err = cudaMemsetAsync(cv->counts, 0, (size_t)nc * 8, st);
+  if (err != cudaSuccess) return pb::cuda_status(err, "cudaMemsetAsync");
   int64_t blocks = (n_tot + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   pb::k_canon_gather<<<(unsigned)blocks, 256, 0, st>>>(g, perm, keys_s, n_tot, rank_bits,
