@@ -5,8 +5,7 @@ mkdir -p /tmp/v
 i=0
 while IFS= read -r flags; do
   i=$((i+1))
-  if [ -z "$flags" ]; then lib=paper_2404_10270_b200/libpicmc_b200.so;
-  elif [ "$flags" = "OLD" ]; then lib=build/old/libold.so; else
+  if [ -z "$flags" ]; then lib=paper_2404_10270_b200/libpicmc_b200.so; else
     lib=/tmp/v/l$i.so
     make -s -C paper_2404_10270_b200/csrc OUT=$lib BUILD=/tmp/v/b$i EXTRA="$flags" > /tmp/v/m$i 2>&1 || { cat /tmp/v/m$i | tail -5; continue; }
   fi
