@@ -700,7 +700,12 @@ extern "C" int pb_canonical_resort(const pb_species *src, const pb_species *dst,
     g.dst[nf++] = dst->yp;
   }
   g.nf = nf;
-  if (pb::canon_scatter_enabled()) {
+  // (small stores keep the full key sort: the scatter path's host read of
+  // the mover count costs more than sorting ~1M keys; PB_CANON_SCATTER_MIN
+  // moves the threshold, read per call so tests can exercise both paths)
+  const char *smin = getenv("PB_CANON_SCATTER_MIN");
+  const int64_t scatter_min = smin ? atoll(smin) : (int64_t)1 << 20;
+  if (pb::canon_scatter_enabled() && n_tot >= scatter_min) {
     // scatter path (see k_scat_classify): extra scratch after the sort path's
     char *q = scan_tmp + pb::offsets_tmp_bytes(nc);
     uint32_t *stay = (uint32_t *)q;

@@ -4,7 +4,7 @@ import torch
 from dataclasses import replace
 from paper_2404_10270_b200 import load_config
 from paper_2404_10270_b200.canonical import CanonicalEngine
-cfg = load_config('configs/c2_collisions_100k.toml')
+cfg = load_config(sys.argv[1] if len(sys.argv) > 1 else 'configs/c2_collisions_100k.toml')
 cfg = replace(cfg, n_steps=0)
 eng = CanonicalEngine(cfg, device=torch.device('cuda', 0), init='device', check_every=0)
 for _ in range(3): eng.step()

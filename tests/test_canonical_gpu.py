@@ -82,8 +82,12 @@ def _run(cfg):
     return m, hist
 
 
+@pytest.mark.parametrize("resort", ["sort", "scatter"])
 @pytest.mark.parametrize("name", RUNS_ALL)
-def test_canonical_run_matches_reference_bitwise(cuda, name):
+def test_canonical_run_matches_reference_bitwise(cuda, name, resort, monkeypatch):
+    """resort: the full key sort (stores under PB_CANON_SCATTER_MIN, here all)
+    or the scatter path (stayers by prefix count, movers sorted) forced on."""
+    monkeypatch.setenv("PB_CANON_SCATTER_MIN", "0" if resort == "scatter" else str(1 << 40))
     g = load_golden(f"{name}.npz")
     cfg = cfg_from(g, slot_order="canonical")
     m, h = _run(cfg)
@@ -151,16 +155,17 @@ def test_canonical_extensions_match_oracle(cuda, boundary):
         assert h["totals"][-1][0] < h["totals"][0][0] + m.tally.ionization
 
 
-def test_desk_criterion01_bitwise_and_ode(cuda):
+def test_desk_criterion01_bitwise_and_ode(cuda, monkeypatch):
     """pkg/configs/desk.toml to the ODE half-depletion step (the reference's
     acceptance criterion 01, pkg/tests/test_acceptance.py:73-117): every
     per-step diagnostic row, the last rho and the final stores equal the
     reference run bit for bit, and the neutral total is within 5% of the
-    ODE oracle."""
+    ODE oracle.  The canonical resort runs on its scatter path throughout."""
     import os
 
     from paper_2404_10270_b200 import load_config, run_simulation
 
+    monkeypatch.setenv("PB_CANON_SCATTER_MIN", "0")
     g = load_golden("run_desk_criterion01.npz")
     cfg = load_config(os.path.join(os.path.dirname(__file__), "..", "configs", "desk.toml"))
     steps = int(g["steps"])
