@@ -452,21 +452,36 @@ __global__ void k_scat_classify(const uint64_t *__restrict__ keys, int64_t n, in
                                 int64_t *__restrict__ cnt_in, uint64_t *__restrict__ mkeys,
                                 uint32_t *__restrict__ midx, unsigned long long *__restrict__ mcount) {
   const uint64_t rmask = (1ull << rank_bits) - 1;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t key = keys[i];
-    if (key == kDeadKey) continue;
-    const int64_t dest = (int64_t)((key >> rank_bits) >> 1);
-    const bool mv = (key >> rank_bits) & 1ull;
-    const uint64_t rank = key & rmask;
-    if (!mv) {
-      stay_by_rank[rank] = 1u;
-      atomicAdd((unsigned long long *)&cnt_stay[dest], 1ull);
-    } else {
-      const unsigned long long t = atomicAdd(mcount, 1ull);
-      mkeys[t] = key;
-      midx[t] = (uint32_t)i;
-      atomicAdd((unsigned long long *)&cnt_in[dest], 1ull);
+  const unsigned lane = threadIdx.x & 31;
+  // grid-stride over whole warps so every lane reaches the warp collectives
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x; b < n; b += stride) {
+    const int64_t i = b + threadIdx.x;
+    const uint64_t key = i < n ? keys[i] : kDeadKey;
+    const bool live = key != kDeadKey;
+    const int64_t dest = live ? (int64_t)((key >> rank_bits) >> 1) : -1;
+    const bool mv = live && ((key >> rank_bits) & 1ull);
+    const bool stay = live && !mv;
+    if (stay) stay_by_rank[key & rmask] = 1u;
+    // stayers of a warp mostly share one cell: one atomic per distinct cell
+    const unsigned grp = __match_any_sync(0xffffffffu, stay ? dest : -1);
+    if (stay && lane == (unsigned)(__ffs(grp) - 1))
+      atomicAdd((unsigned long long *)&cnt_stay[dest], (unsigned long long)__popc(grp));
+    // movers are rare: one counter reservation per warp
+    const unsigned mb = __ballot_sync(0xffffffffu, mv);
+    if (mb) {
+      const unsigned leader = (unsigned)(__ffs(mb) - 1);
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(mcount, (unsigned long long)__popc(mb));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (mv) {
+        unsigned lt;
+        asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+        const unsigned long long t = base + __popc(mb & lt);
+        mkeys[t] = key;
+        midx[t] = (uint32_t)i;
+        atomicAdd((unsigned long long *)&cnt_in[dest], 1ull);
+      }
     }
   }
 }
