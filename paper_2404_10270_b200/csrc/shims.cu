@@ -80,6 +80,40 @@ __global__ void k_deposit_partials(const double *__restrict__ x,
   }
 }
 
+// The same sums with one thread per cell: the sequential add chain is the
+// latency, so 32 cells per warp in flight (loads issued four ahead) beat a
+// warp replaying one cell's chain.
+__global__ void k_deposit_partials_tpc(const double *__restrict__ x,
+                                       const int64_t *__restrict__ offs,
+                                       const int64_t *__restrict__ counts, int64_t nc,
+                                       double *__restrict__ left, double *__restrict__ right) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nc;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const double *p = x + offs[j];
+    const int64_t cnt = counts[j];
+    double sl = 0.0, sr = 0.0;
+    int64_t k = 0;
+    for (; k + 4 <= cnt; k += 4) {
+      const double a = p[k], b = p[k + 1], c = p[k + 2], d = p[k + 3];
+      sl = __dadd_rn(sl, __dsub_rn(1.0, a));
+      sr = __dadd_rn(sr, a);
+      sl = __dadd_rn(sl, __dsub_rn(1.0, b));
+      sr = __dadd_rn(sr, b);
+      sl = __dadd_rn(sl, __dsub_rn(1.0, c));
+      sr = __dadd_rn(sr, c);
+      sl = __dadd_rn(sl, __dsub_rn(1.0, d));
+      sr = __dadd_rn(sr, d);
+    }
+    for (; k < cnt; ++k) {
+      const double a = p[k];
+      sl = __dadd_rn(sl, __dsub_rn(1.0, a));
+      sr = __dadd_rn(sr, a);
+    }
+    left[j] = sl;
+    right[j] = sr;
+  }
+}
+
 // gather (_kernels.pyx:37-57): live order output, start[j] = sum(counts[:j]).
 __global__ void k_gather(const double *__restrict__ nodes,
                          const double *__restrict__ x,
@@ -172,6 +206,15 @@ extern "C" int pb_deposit_partials(const double *x, const int64_t *offs,
   if (!offs || !counts || !left || !right) {
     pb::set_error("pb_deposit_partials: NULL array argument");
     return PB_ERR_INVALID;
+  }
+  static const bool tpc = !(getenv("PB_DEPOSIT_TPC") && atoi(getenv("PB_DEPOSIT_TPC")) == 0);
+  if (tpc) {
+    int64_t blocks = (nc + 255) / 256;
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    pb::k_deposit_partials_tpc<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        x, offs, counts, nc, left, right);
+    PB_CHECK_LAUNCH("k_deposit_partials_tpc");
+    return PB_OK;
   }
   pb::k_deposit_partials<<<pb::shim_grid(nc), pb::kShimThreads, 0, (cudaStream_t)stream>>>(
       x, offs, counts, nc, left, right);
