@@ -264,20 +264,54 @@ struct CanonPushArgs {
   pb_status *st;
   uint64_t *keys;
   uint32_t *vals;
+  // scatter resort: classify the keys in the same pass (scat_classify_warp), or null
+  uint32_t *stay_by_rank;
+  int64_t *cnt_stay, *cnt_in;
+  uint64_t *mkeys;
+  uint32_t *midx;
+  unsigned long long *mcount;
 };
 
-template <int KIND, int BC>
-__global__ void __launch_bounds__(256) k_canon_push(const __grid_constant__ CanonPushArgs a) {
-  const pb_species &s = a.s;
-  int moved = 0, abs_l = 0, abs_r = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n_tot;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    a.vals[i] = (uint32_t)i;
-    const int32_t c = s.cell[i];
-    if (c < 0) {
-      a.keys[i] = kDeadKey;
-      continue;
+// the scatter resort's classification of one warp's keys: stayers flagged by rank and
+// counted per cell, movers appended (see k_scat_stay)
+__device__ __forceinline__ void scat_classify_warp(uint64_t key, int64_t i, int rank_bits,
+                                                   uint32_t *stay_by_rank, int64_t *cnt_stay,
+                                                   int64_t *cnt_in, uint64_t *mkeys, uint32_t *midx,
+                                                   unsigned long long *mcount) {
+  const unsigned lane = threadIdx.x & 31;
+  const bool live = key != kDeadKey;
+  const int64_t dest = live ? (int64_t)((key >> rank_bits) >> 1) : -1;
+  const bool mv = live && ((key >> rank_bits) & 1ull);
+  const bool stay = live && !mv;
+  if (stay) stay_by_rank[key & ((1ull << rank_bits) - 1)] = 1u;
+  const unsigned grp = __match_any_sync(0xffffffffu, stay ? dest : -1);
+  if (stay && lane == (unsigned)(__ffs(grp) - 1))
+    atomicAdd((unsigned long long *)&cnt_stay[dest], (unsigned long long)__popc(grp));
+  const unsigned mb = __ballot_sync(0xffffffffu, mv);
+  if (mb) {
+    const unsigned leader = (unsigned)(__ffs(mb) - 1);
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(mcount, (unsigned long long)__popc(mb));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (mv) {
+      unsigned lt;
+      asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+      const unsigned long long t = base + __popc(mb & lt);
+      mkeys[t] = key;
+      midx[t] = (uint32_t)i;
+      atomicAdd((unsigned long long *)&cnt_in[dest], 1ull);
     }
+  }
+}
+
+template <int KIND, int BC>
+__device__ __forceinline__ uint64_t canon_push_one(const CanonPushArgs &a, int64_t i, int &moved,
+                                                   int &abs_l, int &abs_r) {
+  const pb_species &s = a.s;
+  a.vals[i] = (uint32_t)i;
+  const int32_t c = s.cell[i];
+  if (c < 0) return kDeadKey;
+  {
     const int64_t rank = a.rank_offset + (i < a.n_old ? a.offp[c] + (i - a.offs[c])
                                                       : a.offp[c] + a.cnt_after[c] + a.nb_k[i - a.n_old]);
     int32_t dest = c;
@@ -303,12 +337,29 @@ __global__ void __launch_bounds__(256) k_canon_push(const __grid_constant__ Cano
         dest = o.cell;
         if (BC == PB_BC_ABSORBING && o.wall >= 0) {
           if (o.wall == 0) ++abs_l; else ++abs_r;
-          a.keys[i] = kDeadKey;
-          continue;
+          return kDeadKey;
         }
       }
     }
-    a.keys[i] = ((((uint64_t)dest << 1) | (mv ? 1u : 0u)) << a.rank_bits) | (uint64_t)rank;
+    return ((((uint64_t)dest << 1) | (mv ? 1u : 0u)) << a.rank_bits) | (uint64_t)rank;
+  }
+}
+
+template <int KIND, int BC>
+__global__ void __launch_bounds__(256) k_canon_push(const __grid_constant__ CanonPushArgs a) {
+  int moved = 0, abs_l = 0, abs_r = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // warp-aligned grid stride: every lane reaches the classification collectives
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x; b < a.n_tot; b += stride) {
+    const int64_t i = b + threadIdx.x;
+    uint64_t key = kDeadKey;
+    if (i < a.n_tot) {
+      key = canon_push_one<KIND, BC>(a, i, moved, abs_l, abs_r);
+      a.keys[i] = key;
+    }
+    if (a.stay_by_rank)
+      scat_classify_warp(key, i, a.rank_bits, a.stay_by_rank, a.cnt_stay, a.cnt_in, a.mkeys, a.midx,
+                         a.mcount);
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
@@ -397,8 +448,18 @@ static int offsets_from_counts(const int64_t *counts, int64_t *offs, int64_t nc,
 static int launch_canon_push(const pb_species *src, const pb_canon *cv, const double *e_nodes,
                              int64_t nc, int particle_bc, int species_id, pb_status *status,
                              int64_t rank_offset, int rank_bits, const int64_t *offp,
-                             uint64_t *keys, uint32_t *vals, cudaStream_t st) {
+                             uint64_t *keys, uint32_t *vals, cudaStream_t st,
+                             const CanonPushArgs *cls = nullptr) {
   CanonPushArgs a;
+  memset(&a, 0, sizeof(a));
+  if (cls) {  // the scatter resort's classification outputs
+    a.stay_by_rank = cls->stay_by_rank;
+    a.cnt_stay = cls->cnt_stay;
+    a.cnt_in = cls->cnt_in;
+    a.mkeys = cls->mkeys;
+    a.midx = cls->midx;
+    a.mcount = cls->mcount;
+  }
   a.s = *src;
   a.n_old = cv->n_old;
   a.n_tot = cv->n_old + cv->n_tail;
@@ -446,46 +507,8 @@ static size_t offsets_tmp_bytes(int64_t nc) {
 // their new slot is new_off[cell] + (stayers with a smaller rank in the cell)
 // = new_off[c] + G[rank] - G[offp[c]] with G the exclusive prefix count of
 // stayers over the pre-move ranks; only the movers (~0.6% of electrons per
-// step) are sorted by key.  Same final order as sorting every key.
-__global__ void k_scat_classify(const uint64_t *__restrict__ keys, int64_t n, int rank_bits,
-                                uint32_t *__restrict__ stay_by_rank, int64_t *__restrict__ cnt_stay,
-                                int64_t *__restrict__ cnt_in, uint64_t *__restrict__ mkeys,
-                                uint32_t *__restrict__ midx, unsigned long long *__restrict__ mcount) {
-  const uint64_t rmask = (1ull << rank_bits) - 1;
-  const unsigned lane = threadIdx.x & 31;
-  // grid-stride over whole warps so every lane reaches the warp collectives
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x; b < n; b += stride) {
-    const int64_t i = b + threadIdx.x;
-    const uint64_t key = i < n ? keys[i] : kDeadKey;
-    const bool live = key != kDeadKey;
-    const int64_t dest = live ? (int64_t)((key >> rank_bits) >> 1) : -1;
-    const bool mv = live && ((key >> rank_bits) & 1ull);
-    const bool stay = live && !mv;
-    if (stay) stay_by_rank[key & rmask] = 1u;
-    // stayers of a warp mostly share one cell: one atomic per distinct cell
-    const unsigned grp = __match_any_sync(0xffffffffu, stay ? dest : -1);
-    if (stay && lane == (unsigned)(__ffs(grp) - 1))
-      atomicAdd((unsigned long long *)&cnt_stay[dest], (unsigned long long)__popc(grp));
-    // movers are rare: one counter reservation per warp
-    const unsigned mb = __ballot_sync(0xffffffffu, mv);
-    if (mb) {
-      const unsigned leader = (unsigned)(__ffs(mb) - 1);
-      unsigned long long base = 0;
-      if (lane == leader) base = atomicAdd(mcount, (unsigned long long)__popc(mb));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      if (mv) {
-        unsigned lt;
-        asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
-        const unsigned long long t = base + __popc(mb & lt);
-        mkeys[t] = key;
-        midx[t] = (uint32_t)i;
-        atomicAdd((unsigned long long *)&cnt_in[dest], 1ull);
-      }
-    }
-  }
-}
-
+// step) are sorted by key (the push classifies its keys as it writes them:
+// scat_classify_warp).  Same final order as sorting every key.
 struct ScatArgs {
   const double *src[5];
   double *dst[5];
@@ -701,9 +724,6 @@ extern "C" int pb_canonical_resort(const pb_species *src, const pb_species *dst,
     pb::set_error("pb_canonical_resort: key needs %d bits", key_bits);
     return PB_ERR_INVALID;
   }
-  rc = pb::launch_canon_push(src, cv, e_nodes, nc, particle_bc, species_id, status, 0, rank_bits,
-                             offp, keys, vals, st);
-  if (rc) return rc;
   pb::GatherArgs g;
   int nf = 0;
   g.src[nf] = src->x; g.dst[nf++] = dst->x;
@@ -720,8 +740,12 @@ extern "C" int pb_canonical_resort(const pb_species *src, const pb_species *dst,
   // moves the threshold, read per call so tests can exercise both paths)
   const char *smin = getenv("PB_CANON_SCATTER_MIN");
   const int64_t scatter_min = smin ? atoll(smin) : (int64_t)1 << 20;
-  if (pb::canon_scatter_enabled() && n_tot >= scatter_min) {
-    // scatter path (see k_scat_classify): extra scratch after the sort path's
+  if (!(pb::canon_scatter_enabled() && n_tot >= scatter_min)) {
+    rc = pb::launch_canon_push(src, cv, e_nodes, nc, particle_bc, species_id, status, 0, rank_bits,
+                               offp, keys, vals, st);
+    if (rc) return rc;
+  } else {
+    // scatter path (see k_scat_stay): extra scratch after the sort path's
     char *q = scan_tmp + pb::offsets_tmp_bytes(nc);
     uint32_t *stay = (uint32_t *)q;
     q += pb::a256((size_t)(n_tot + 1) * 4);
@@ -744,11 +768,20 @@ extern "C" int pb_canonical_resort(const pb_species *src, const pb_species *dst,
     if (err == cudaSuccess) err = cudaMemsetAsync(cnt_in, 0, (size_t)(nc + 1) * 8, st);
     if (err == cudaSuccess) err = cudaMemsetAsync(mcount, 0, 8, st);
     if (err != cudaSuccess) return pb::cuda_status(err, "cudaMemsetAsync");
+    // the push classifies its keys as it writes them
+    pb::CanonPushArgs cls;
+    memset(&cls, 0, sizeof(cls));
+    cls.stay_by_rank = stay;
+    cls.cnt_stay = cnt_stay;
+    cls.cnt_in = cnt_in;
+    cls.mkeys = keys_s;
+    cls.midx = perm;
+    cls.mcount = mcount;
+    rc = pb::launch_canon_push(src, cv, e_nodes, nc, particle_bc, species_id, status, 0, rank_bits,
+                               offp, keys, vals, st, &cls);
+    if (rc) return rc;
     int64_t blocks = (n_tot + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    pb::k_scat_classify<<<(unsigned)blocks, 256, 0, st>>>(keys, n_tot, rank_bits, stay, cnt_stay,
-                                                          cnt_in, keys_s, vals, mcount);
-    PB_CHECK_LAUNCH("k_scat_classify");
     size_t tb = pb::scan_u32_bytes(R);
     err = cub::DeviceScan::ExclusiveSum(u32_tmp, tb, stay, G, (int)(R + 1), st);
     if (err != cudaSuccess) return pb::cuda_status(err, "DeviceScan (stayers)");
@@ -764,7 +797,7 @@ extern "C" int pb_canonical_resort(const pb_species *src, const pb_species *dst,
     if (err != cudaSuccess) return pb::cuda_status(err, "mover count");
     if (m > 0) {
       size_t sb = pb::sort_temp_bytes((int64_t)m);
-      err = cub::DeviceRadixSort::SortPairs(sort_tmp, sb, keys_s, mkeys_s, vals, perm, (int)m, 0,
+      err = cub::DeviceRadixSort::SortPairs(sort_tmp, sb, keys_s, mkeys_s, perm, vals, (int)m, 0,
                                             key_bits, st);
       if (err != cudaSuccess) return pb::cuda_status(err, "DeviceRadixSort::SortPairs (movers)");
     }
@@ -782,7 +815,7 @@ extern "C" int pb_canonical_resort(const pb_species *src, const pb_species *dst,
     sa.cnt_stay = cnt_stay;
     sa.in_off = in_off;
     sa.mkeys_s = mkeys_s;
-    sa.midx_s = perm;
+    sa.midx_s = vals;
     sa.cell_out = dst->cell;
     pb::k_scat_stay<<<(unsigned)blocks, 256, 0, st>>>(sa, n_tot);
     PB_CHECK_LAUNCH("k_scat_stay");
