@@ -17,6 +17,8 @@ ranks), roofline (push kernel: algorithmic bytes / CUDA-event duration vs the
 measured HBM copy peak), cpu_baseline (the reference's own compiled kernels on
 this host's cores, bounded sample), e2e (public step API with per-step host
 E-field upload and rho download), clocks (nvidia-smi during the timed region).
+N > 1 ranks exchange the density through peer memory (one fused kernel per
+step, graph-replayed; config.density_exchange names the path used).
 """
 
 import argparse
@@ -318,7 +320,7 @@ def run_ours(args, rank, world, local_rank):
 
     # e2e: the public host-driven API (Engine.run_pipelined): every step copies
     # its E-field input H2D from pinned host memory and its rho result D2H into
-    # pinned host memory, which the host reads (one step late, while the GPU
+    # pinned host memory, which the host reads (one block of steps late, while the GPU
     # runs the next step).
     nodes = nc_total + 1
     e_host = torch.zeros(nodes, dtype=torch.float64).pin_memory()
@@ -428,7 +430,8 @@ def run_ours(args, rank, world, local_rank):
                 "h2d_bytes_per_step": 0 if cfg.field_solve else nodes * 8,
                 "d2h_bytes_per_step": nodes * 8,
                 "path": "Engine.run_pipelined(): per step E-field H2D from pinned memory + step + rho D2H "
-                        "into pinned memory read by the host (one step late, overlapped); max(device, wall)",
+                        "into pinned memory read by the host (one graph block of PB_PIPE_GROUP steps late, "
+                        "overlapped); max(device, wall)",
                 "graphs_captured_in_timed_region": e2e_graphs_timed},
         "gpu_launches": args.steps * launches_per_step + n_sort_kernels,
         "timing_windows_ms": {"steps_per_window": 200, "min": min(win_ms), "median": float(np.median(win_ms)),
