@@ -30,7 +30,11 @@
 
 namespace pb {
 
-constexpr int kPeerThreads = 256;
+// 64-thread blocks, at most one per SM: small enough (2.5K registers) to be
+// co-resident with the persistent mover (3 x 256 threads x 80 registers =
+// 61K of the SM's 64K), so in field-free steps the exchange runs beside the
+// push instead of waiting for SM slots in its tail.
+constexpr int kPeerThreads = 64;
 
 struct PeerArgs {
   const uint64_t *bins[PB_MAX_RANKS];
