@@ -39,16 +39,20 @@ class PeerBuffers:
         self.device = device
         self.own, self.ptrs, self._opened = {}, {}, []
         handles = {}
+        ok = 1
         for name, nbytes in sizes.items():
             p = ctypes.c_void_p()
             h = (ctypes.c_char * _lib.PB_PEER_HANDLE_BYTES)()
-            _lib.check(self.lib.pb_peer_alloc(int(nbytes), ctypes.byref(p), h), "pb_peer_alloc")
+            if self.lib.pb_peer_alloc(int(nbytes), ctypes.byref(p), h) != _lib.PB_OK:
+                ok = 0  # still join the exchange below, so no rank waits forever
+                break
             self.own[name] = p.value
             handles[name] = bytes(h)
         gathered = [None] * world
-        dist.all_gather_object(gathered, handles, group=group)
-        ok = 1
-        for name in sizes:
+        dist.all_gather_object(gathered, handles if ok else None, group=group)
+        if any(g is None for g in gathered):
+            ok = 0
+        for name in (sizes if ok else ()):
             self.ptrs[name] = [0] * world
             for r in range(world):
                 if r == rank:
