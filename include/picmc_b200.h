@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define PB_ABI_VERSION 1
+#define PB_ABI_VERSION 2
 
 #define PB_OK 0
 #define PB_ERR_INVALID 1
@@ -175,19 +175,23 @@ int pb_deposit_only(const pb_species *sp, int nsp, int64_t nc, uint64_t *bins,
 /* Weighted partials and stitched density from fixed-point bins:
  * left = sum_s coef_s * L_s, right likewise, in species order
  * (pkg/src/picmc/fields.py:67-77), rho per stitch_rho/deposit_charge
- * (fields.py:81-92, :115-117).  coef is a host array of ndep doubles. */
+ * (fields.py:81-92, :115-117).  coef is a host array of ndep doubles.
+ * Bin overflow: a cell holding >= 2^(64-PB_DEPOSIT_FRAC_BITS) = 65536
+ * particles of one species cannot be represented; if status is non-NULL
+ * such a cell sets status->code = PB_ERR_OVERFLOW (if still PB_OK) and
+ * status->overflow = the largest count seen. */
 int pb_rho_epilogue(const uint64_t *bins, const double *coef, int ndep,
                     int64_t nc, int field_bc, double *left, double *right,
-                    double *rho, void *stream);
+                    double *rho, pb_status *status_or_null, void *stream);
 
 /* The engine's per-step form of pb_rho_epilogue (two kernels): weighted
  * partials per cell, after which `bins` itself is zeroed (a bin set is clean
  * again once its density has been taken), then the stitch into rho.  If
- * non-NULL, `bins_next` (the other ping-pong set) and the word `counter` are
- * zeroed too.  Because it never touches the set the next mover deposits
- * into, it may run concurrently with that pb_push_deposit. */
+ * non-NULL, `bins_next` (the other ping-pong set) is zeroed too.  Because it
+ * never touches the set the next mover deposits into, it may run
+ * concurrently with that pb_push_deposit.  Overflow as pb_rho_epilogue. */
 int pb_density_step(uint64_t *bins, uint64_t *bins_next,
-                    uint64_t *counter, const double *coef, int ndep,
+                    pb_status *status_or_null, const double *coef, int ndep,
                     int64_t nc, int field_bc, double *left, double *right,
                     double *rho, void *stream);
 
@@ -429,14 +433,19 @@ typedef struct pb_peer_density {
   double *left[PB_MAX_RANKS];
   double *right[PB_MAX_RANKS];
   double *rho[PB_MAX_RANKS];
-  uint64_t *flags[PB_MAX_RANKS]; /* 2 * world zeroed words per rank */
+  uint64_t *flags[PB_MAX_RANKS]; /* PB_PEER_FLAG_WORDS zeroed words per rank:
+                                    arrive epochs, done counts, error word */
   int rank;
   int world;
   uint64_t epoch;                /* 1, 2, ... one per call (when epoch_dev is NULL) */
   uint64_t *epoch_dev;           /* or: a zeroed device counter of this rank, read as
                                     epoch - 1 and advanced after the exchange, so the
                                     call can be captured in a CUDA graph */
+  uint64_t timeout_ns;           /* barrier wait bound (0 = 60 s); on timeout the
+                                    failing epoch is published to every rank, and
+                                    every rank flags PB_ERR_PEER (sticky) */
 } pb_peer_density;
+#define PB_PEER_FLAG_WORDS (2 * PB_MAX_RANKS + 1)
 
 /* cudaMalloc + zero + IPC handle (PB_PEER_HANDLE_BYTES) for a buffer peers map. */
 int pb_peer_alloc(size_t bytes, void **ptr, void *handle_out);
@@ -445,8 +454,10 @@ int pb_peer_open(const void *handle, void **ptr);
 /* Unmap (owned = 0) or free (owned = 1). */
 int pb_peer_close(void *ptr, int owned);
 /* One density exchange + epilogue (see above); bins_next (optional) is
- * zeroed as well, like pb_density_step's. Timeouts set PB_ERR_PEER in
- * *status. */
+ * zeroed as well, like pb_density_step's.  A timeout or a peer's failure
+ * sets PB_ERR_PEER in *status on every rank and leaves the bins uncleared;
+ * bin overflow as pb_rho_epilogue.  PB_ERR_INVALID if the grid could not be
+ * co-resident. */
 int pb_peer_density_step(const pb_peer_density *p, uint64_t *bins_next,
                          const double *coef, int ndep, int64_t nc,
                          int field_bc, pb_status *status, void *stream);

@@ -36,6 +36,9 @@ PB_FIELD_DIRICHLET = 1
 PB_MAX_SPECIES = 8
 PB_CELL8_CHUNK = 2048
 PB_DEPOSIT_FRAC_BITS = 48
+# largest per-cell, per-species particle count the fixed-point bins represent
+PB_MAX_CELL_COUNT = (1 << (64 - PB_DEPOSIT_FRAC_BITS)) - 1
+ABI_VERSION = 2
 
 _p = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -89,7 +92,11 @@ PB_PEER_HANDLE_BYTES = 64
 class PbPeerDensity(ctypes.Structure):
     _fields_ = [("bins", _p * PB_MAX_RANKS), ("left", _p * PB_MAX_RANKS), ("right", _p * PB_MAX_RANKS),
                 ("rho", _p * PB_MAX_RANKS), ("flags", _p * PB_MAX_RANKS), ("rank", ctypes.c_int),
-                ("world", ctypes.c_int), ("epoch", ctypes.c_uint64), ("epoch_dev", _p)]
+                ("world", ctypes.c_int), ("epoch", ctypes.c_uint64), ("epoch_dev", _p),
+                ("timeout_ns", ctypes.c_uint64)]
+
+
+PB_PEER_FLAG_WORDS = 2 * PB_MAX_RANKS + 1
 
 
 class PbCellFields(ctypes.Structure):
@@ -119,7 +126,7 @@ _SIGS = {
     "pb_deposit_only": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int,
                                        _i64, _p, _p, _p]),
     "pb_rho_epilogue": (ctypes.c_int, [_p, ctypes.POINTER(_f64), ctypes.c_int, _i64,
-                                       ctypes.c_int, _p, _p, _p, _p]),
+                                       ctypes.c_int, _p, _p, _p, _p, _p]),
     "pb_density_step": (ctypes.c_int, [_p, _p, _p, ctypes.POINTER(_f64), ctypes.c_int, _i64,
                                        ctypes.c_int, _p, _p, _p, _p]),
     "pb_compact_scratch_bytes": (ctypes.c_size_t, [_i64]),
@@ -194,7 +201,7 @@ def load():
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args
-            if lib.pb_abi_version() != 1:
+            if lib.pb_abi_version() != ABI_VERSION:
                 raise ImportError("libpicmc_b200 ABI version mismatch")
             _lib = lib
     return _lib

@@ -34,11 +34,13 @@ int cuda_status(cudaError_t err, const char *what) {
 __device__ __forceinline__ void weighted_partials(const uint64_t *__restrict__ bins,
                                                   const double *__restrict__ coef,
                                                   int ndep, int64_t nc, int64_t j,
-                                                  double &left, double &right) {
+                                                  double &left, double &right,
+                                                  pb_status *st) {
   double l = 0.0, r = 0.0;
   for (int s = 0; s < ndep; ++s) {
     const uint64_t R = bins[(size_t)s * 2 * nc + j];
     const uint64_t C = bins[(size_t)s * 2 * nc + nc + j];
+    if (C >= kMaxCellCount) flag_overflow(st, C);
     const uint64_t L = (C << kFracBits) - R;
     const double lraw = __dmul_rn(__ull2double_rn(L), kFracInv);
     const double rraw = __dmul_rn(__ull2double_rn(R), kFracInv);
@@ -59,32 +61,31 @@ __global__ void k_rho_epilogue(const uint64_t *__restrict__ bins, CoefArgs ca,
                                double *__restrict__ right,
                                double *__restrict__ rho,
                                uint64_t *__restrict__ clear,
-                               uint64_t *__restrict__ counter) {
+                               pb_status *st) {
   pdl_enter();
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g > nc) return;
   // Step fusion: zero the other (ping-pong) bin set for the coming mover
-  // launch and reset the mover's work counter.
+  // launch.
   if (clear && g < nc)
     for (int s = 0; s < ndep; ++s) {
       clear[(size_t)s * 2 * nc + g] = 0;
       clear[(size_t)s * 2 * nc + nc + g] = 0;
     }
-  if (counter && g == 0) *counter = 0;
   double lg = 0.0, rg = 0.0, lp = 0.0, rp = 0.0;
   if (g < nc) {
-    weighted_partials(bins, ca.c, ndep, nc, g, lg, rg);
+    weighted_partials(bins, ca.c, ndep, nc, g, lg, rg, st);
     if (left) left[g] = lg;
     if (right) right[g] = rg;
   }
-  if (g > 0) weighted_partials(bins, ca.c, ndep, nc, g - 1, lp, rp);
+  if (g > 0) weighted_partials(bins, ca.c, ndep, nc, g - 1, lp, rp, nullptr);
   double v;
   if (g > 0 && g < nc) {
     v = __dadd_rn(rp, lg);  // rho[g] = R[g-1] + L[g] (fields.py:85)
   } else if (field_bc == PB_FIELD_PERIODIC) {
     double l0, r0, ll, rl;  // rho[0] = rho[nc] = R[nc-1] + L[0]
-    weighted_partials(bins, ca.c, ndep, nc, 0, l0, r0);
-    weighted_partials(bins, ca.c, ndep, nc, nc - 1, ll, rl);
+    weighted_partials(bins, ca.c, ndep, nc, 0, l0, r0, nullptr);
+    weighted_partials(bins, ca.c, ndep, nc, nc - 1, ll, rl, nullptr);
     v = __dadd_rn(rl, l0);
   } else if (g == 0) {
     v = __dmul_rn(lg, 2.0);  // walls own half a cell (fields.py:115-117)
@@ -102,13 +103,12 @@ __global__ void k_rho_epilogue(const uint64_t *__restrict__ bins, CoefArgs ca,
 // replay the epilogue runs on a side stream overlapped with the next push.
 __global__ void k_partials_clear(uint64_t *__restrict__ bins, CoefArgs ca, int ndep, int64_t nc,
                                  double *__restrict__ left, double *__restrict__ right,
-                                 uint64_t *__restrict__ clear, uint64_t *__restrict__ counter) {
+                                 uint64_t *__restrict__ clear, pb_status *st) {
   pdl_enter();
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (counter && g == 0) *counter = 0;
   if (g >= nc) return;
   double l, r;
-  weighted_partials(bins, ca.c, ndep, nc, g, l, r);
+  weighted_partials(bins, ca.c, ndep, nc, g, l, r, st);
   left[g] = l;
   right[g] = r;
   for (int s = 0; s < ndep; ++s) {
@@ -158,7 +158,7 @@ extern "C" int pb_device_sm_count(int *out) {
 
 static int rho_epilogue(const uint64_t *bins, const double *coef, int ndep, int64_t nc,
                         int field_bc, double *left, double *right, double *rho,
-                        uint64_t *clear, uint64_t *counter, void *stream) {
+                        uint64_t *clear, pb_status *status, void *stream) {
   if (ndep < 0 || ndep > PB_MAX_SPECIES) {
     pb::set_error("ndep=%d outside [0, %d]", ndep, PB_MAX_SPECIES);
     return PB_ERR_INVALID;
@@ -178,18 +178,18 @@ static int rho_epilogue(const uint64_t *bins, const double *coef, int ndep, int6
   const int64_t blocks = (nc + 1 + threads - 1) / threads;
   cudaError_t e = pb::launch_pdl(pb::k_rho_epilogue, dim3((unsigned)blocks), dim3(threads), 0,
                                   (cudaStream_t)stream, bins, ca, ndep, nc, field_bc, left, right,
-                                  rho, clear, counter);
+                                  rho, clear, status);
   if (e != cudaSuccess) return pb::cuda_status(e, "k_rho_epilogue");
   return PB_OK;
 }
 
 extern "C" int pb_rho_epilogue(const uint64_t *bins, const double *coef, int ndep, int64_t nc,
                                int field_bc, double *left, double *right, double *rho,
-                               void *stream) {
-  return rho_epilogue(bins, coef, ndep, nc, field_bc, left, right, rho, nullptr, nullptr, stream);
+                               pb_status *status, void *stream) {
+  return rho_epilogue(bins, coef, ndep, nc, field_bc, left, right, rho, nullptr, status, stream);
 }
 
-extern "C" int pb_density_step(uint64_t *bins, uint64_t *bins_next, uint64_t *counter,
+extern "C" int pb_density_step(uint64_t *bins, uint64_t *bins_next, pb_status *status,
                                const double *coef, int ndep, int64_t nc, int field_bc,
                                double *left, double *right, double *rho, void *stream) {
   if (bins_next == bins && bins != nullptr) {
@@ -209,7 +209,7 @@ extern "C" int pb_density_step(uint64_t *bins, uint64_t *bins_next, uint64_t *co
   const int threads = 256;
   const int64_t b1 = (nc + threads - 1) / threads, b2 = (nc + 1 + threads - 1) / threads;
   cudaError_t e = pb::launch_pdl(pb::k_partials_clear, dim3((unsigned)b1), dim3(threads), 0, st, bins,
-                                  ca, ndep, nc, left, right, bins_next, counter);
+                                  ca, ndep, nc, left, right, bins_next, status);
   if (e != cudaSuccess) return pb::cuda_status(e, "k_partials_clear");
   e = pb::launch_pdl(pb::k_stitch, dim3((unsigned)b2), dim3(threads), 0, st, (const double *)left,
                      (const double *)right, nc, field_bc, rho, 2.0);

@@ -33,6 +33,19 @@ constexpr double kFracInv = 1.0 / 281474976710656.0;   // 2^-48
 constexpr int kCountShift = 56;
 constexpr uint64_t kRMask = (uint64_t(1) << kCountShift) - 1;
 
+// The fixed-point bins of one species in one cell hold R = sum round(x*2^48)
+// <= C*2^48 and the epilogue forms C<<48: both wrap once a cell holds
+// kMaxCellCount particles of one species (summed over ranks).  Every reader
+// of the bins checks C against it and flags the step (PB_ERR_OVERFLOW, the
+// largest count seen in pb_status.overflow) instead of producing a wrong rho.
+constexpr uint64_t kMaxCellCount = uint64_t(1) << (64 - PB_DEPOSIT_FRAC_BITS);
+
+__device__ __forceinline__ void flag_overflow(pb_status *st, uint64_t count) {
+  if (!st) return;
+  atomicMax(reinterpret_cast<unsigned long long *>(&st->overflow), (unsigned long long)count);
+  atomicCAS(&st->code, PB_OK, PB_ERR_OVERFLOW);
+}
+
 // Quantise a cell-relative position in [0,1) to the deposit fixed point.
 __device__ __forceinline__ uint64_t quantize(double x) {
   return (uint64_t)__double2ull_rn(__dmul_rn(x, kFracScale));

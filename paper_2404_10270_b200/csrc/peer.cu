@@ -21,9 +21,15 @@
 //   B  done     -- every block of every rank has read the bins and written
 //                  its slice: the own bins may be cleared and rho is
 //                  complete on every rank.
-// The grid is persistent (<= resident capacity) so that every block of every
-// rank can reach the barriers.  Waits are bounded: a barrier that does not
-// complete within ~10 s sets PB_ERR_PEER in the status and falls through.
+// The grid is persistent (<= resident capacity, checked at launch) so that
+// every block of every rank can reach the barriers.  Waits are bounded by a
+// wall-clock timeout (%globaltimer; pb_peer_density.timeout_ns, default
+// 60 s).  A rank that times out publishes the failing epoch in the error word
+// of EVERY rank's flag block, sets PB_ERR_PEER in its status and leaves its
+// bins alone; every rank polls its own error word inside its waits, so all
+// ranks -- including one that arrives after the timeout -- flag the step
+// PB_ERR_PEER instead of computing rho from bins a peer may already have
+// cleared.  The error is sticky for the run: every later exchange fails too.
 #include <cstring>
 
 #include "common.cuh"
@@ -35,17 +41,20 @@ namespace pb {
 // 61K of the SM's 64K), so in field-free steps the exchange runs beside the
 // push instead of waiting for SM slots in its tail.
 constexpr int kPeerThreads = 64;
+constexpr int kErrWord = 2 * PB_MAX_RANKS;  // index of the error word in a flag block
 
 struct PeerArgs {
   const uint64_t *bins[PB_MAX_RANKS];
   double *left[PB_MAX_RANKS], *right[PB_MAX_RANKS], *rho[PB_MAX_RANKS];
-  unsigned long long *flags[PB_MAX_RANKS];  // [0, N): arrive epochs, [N, 2N): done counts
+  unsigned long long *flags[PB_MAX_RANKS];  // [0, N): arrive epochs, [N, 2N): done counts,
+                                            // [kErrWord]: first failed epoch (0 = none)
   uint64_t *clear_next;
   double coef[PB_MAX_SPECIES];
   int ndep, rank, world, field_bc;
   int64_t nc;
   unsigned long long epoch;
   const unsigned long long *epoch_dev;  // device epoch counter (graph replay), or null
+  unsigned long long timeout_ns;
   pb_status *st;
 };
 
@@ -57,19 +66,41 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
-// thread 0 of the block waits until flags[slot0 + r] >= target for every rank r
-__device__ bool peer_wait(const PeerArgs &a, int slot0, unsigned long long target) {
-  const unsigned long long *f = a.flags[a.rank] + slot0;
+// Mark the exchange failed on every rank (first failed epoch wins per rank).
+__device__ void peer_fail(const PeerArgs &a, unsigned long long epoch) {
+  for (int r = 0; r < a.world; ++r) atomicCAS_system(a.flags[r] + kErrWord, 0ull, epoch);
+  __threadfence_system();
+  atomicCAS(&a.st->code, PB_OK, PB_ERR_PEER);
+}
+
+// thread 0 of the block waits until flags[slot0 + r] >= target for every
+// rank r; false on timeout or when any rank has reported a failure.
+__device__ bool peer_wait(const PeerArgs &a, int slot0, unsigned long long target,
+                          unsigned long long epoch) {
+  const unsigned long long *f = a.flags[a.rank];
+  const unsigned long long t0 = global_ns();
   for (int r = 0; r < a.world; ++r) {
-    long long spins = 0;
-    while (ld_acquire_sys(f + r) < target) {
-      __nanosleep(64);
-      if (++spins > (1ll << 27)) {  // ~10 s: a peer is gone
+    while (ld_acquire_sys(f + slot0 + r) < target) {
+      if (ld_acquire_sys(f + kErrWord) != 0) {
         atomicCAS(&a.st->code, PB_OK, PB_ERR_PEER);
         return false;
       }
+      __nanosleep(64);
+      if (global_ns() - t0 > a.timeout_ns) {  // a peer is gone or far behind
+        peer_fail(a, epoch);
+        return false;
+      }
     }
+  }
+  if (ld_acquire_sys(f + kErrWord) != 0) {  // sticky: an earlier exchange failed
+    atomicCAS(&a.st->code, PB_OK, PB_ERR_PEER);
+    return false;
   }
   return true;
 }
@@ -86,6 +117,7 @@ __device__ __forceinline__ void reduced_partials(const PeerArgs &a, int64_t c, d
       R += a.bins[k][o];
       C += a.bins[k][o + a.nc];
     }
+    if (C >= kMaxCellCount) flag_overflow(a.st, C);
     const uint64_t L = (C << kFracBits) - R;
     const double lraw = __dmul_rn(__ull2double_rn(L), kFracInv);
     const double rraw = __dmul_rn(__ull2double_rn(R), kFracInv);
@@ -107,49 +139,66 @@ __global__ void __launch_bounds__(kPeerThreads) k_peer_density(const __grid_cons
     for (int r = 0; r < a.world; ++r) st_release_sys(a.flags[r] + a.rank, epoch);
   }
   __shared__ int ok;
-  if (threadIdx.x == 0) ok = peer_wait(a, 0, epoch);
+  __shared__ double s_right[kPeerThreads + 1];  // right partials of cells g0-1 .. g0+63
+  if (threadIdx.x == 0) ok = peer_wait(a, 0, epoch, epoch);
   __syncthreads();
   // this rank's cells [c0, c1) and nodes [c0, c1) (the last rank also node nc)
   const int64_t c0 = nc * a.rank / a.world, c1 = nc * (a.rank + 1) / a.world;
   const int64_t n1 = a.rank == a.world - 1 ? nc + 1 : c1;
   if (ok) {
-    for (int64_t g = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n1;
-         g += (int64_t)gridDim.x * blockDim.x) {
-      double lg = 0.0, rg = 0.0, lp = 0.0, rp = 0.0;
-      if (g < nc) {
+    // Each cell's reduced partials are computed once: a block covers 64
+    // consecutive nodes g0..g0+63 and cells g0-1..g0+63 (one halo cell,
+    // computed by thread 0), sharing the right partials through shared
+    // memory; only the periodic / wall end nodes recompute an end cell.
+    for (int64_t g0 = c0 + (int64_t)blockIdx.x * kPeerThreads; g0 < n1;
+         g0 += (int64_t)gridDim.x * kPeerThreads) {
+      const int64_t g = g0 + threadIdx.x;
+      double lg = 0.0, rg = 0.0;
+      if (g < nc && g < n1) {
         reduced_partials(a, g, lg, rg);
         for (int r = 0; r < a.world; ++r) {
           a.left[r][g] = lg;
           a.right[r][g] = rg;
         }
       }
-      double v;
-      if (g > 0 && g < nc) {
-        reduced_partials(a, g - 1, lp, rp);
-        v = __dadd_rn(rp, lg);  // rho[g] = R[g-1] + L[g] (fields.py:85)
-      } else if (a.field_bc == PB_FIELD_PERIODIC) {
-        double l0, r0, ll, rl;  // rho[0] = rho[nc] = R[nc-1] + L[0]
-        reduced_partials(a, 0, l0, r0);
-        reduced_partials(a, nc - 1, ll, rl);
-        v = __dadd_rn(rl, l0);
-      } else if (g == 0) {
-        v = __dmul_rn(lg, 2.0);  // walls own half a cell (fields.py:115-117)
-      } else {
-        reduced_partials(a, nc - 1, lp, rp);
-        v = __dmul_rn(rp, 2.0);
+      s_right[threadIdx.x + 1] = rg;
+      if (threadIdx.x == 0) {
+        double lh = 0.0, rh = 0.0;
+        if (g0 > 0) reduced_partials(a, g0 - 1, lh, rh);
+        s_right[0] = rh;
       }
-      for (int r = 0; r < a.world; ++r) a.rho[r][g] = v;
+      __syncthreads();
+      if (g < n1) {
+        double v;
+        if (g > 0 && g < nc) {
+          v = __dadd_rn(s_right[threadIdx.x], lg);  // rho[g] = R[g-1] + L[g] (fields.py:85)
+        } else if (a.field_bc == PB_FIELD_PERIODIC) {
+          double l0, r0, ll, rl;  // rho[0] = rho[nc] = R[nc-1] + L[0]
+          reduced_partials(a, 0, l0, r0);
+          reduced_partials(a, nc - 1, ll, rl);
+          v = __dadd_rn(rl, l0);
+        } else if (g == 0) {
+          v = __dmul_rn(lg, 2.0);  // walls own half a cell (fields.py:115-117)
+        } else {
+          v = __dmul_rn(s_right[threadIdx.x], 2.0);  // g == nc: cell nc-1 is g-1
+        }
+        for (int r = 0; r < a.world; ++r) a.rho[r][g] = v;
+      }
+      __syncthreads();
     }
   }
-  // B: this block has read every rank's bins and stored its outputs
+  // B: this block has read every rank's bins and stored its outputs.  The
+  // done count is added even after a failure, so the counts of all ranks stay
+  // aligned with epoch * blocks.
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
     for (int r = 0; r < a.world; ++r)
       atomicAdd_system(a.flags[r] + a.world + a.rank, 1ull);
-    ok = ok && peer_wait(a, a.world, epoch * (unsigned long long)gridDim.x);
+    ok = ok && peer_wait(a, a.world, epoch * (unsigned long long)gridDim.x, epoch);
   }
   __syncthreads();
+  if (!ok) return;  // a peer may still read these bins: leave them
   // every rank is past its reads: clear this rank's bins (and, if asked, the
   // set the coming push deposits into)
   uint64_t *mine = const_cast<uint64_t *>(a.bins[a.rank]);
@@ -236,6 +285,7 @@ extern "C" int pb_peer_density_step(const pb_peer_density *p, uint64_t *bins_nex
   a.epoch = p->epoch;
   a.epoch_dev = (const unsigned long long *)p->epoch_dev;
   a.clear_next = bins_next;
+  a.timeout_ns = p->timeout_ns ? p->timeout_ns : 60000000000ull;
   a.st = status;
   // persistent grid: every block must be resident to reach the barriers
   int sms = 0, dev = 0;
@@ -245,6 +295,16 @@ extern "C" int pb_peer_density_step(const pb_peer_density *p, uint64_t *bins_nex
   int64_t blocks = (per_rank + pb::kPeerThreads - 1) / pb::kPeerThreads;
   if (blocks > sms) blocks = sms;
   if (blocks < 1) blocks = 1;
+  // co-residency: the barriers need every block of the grid resident at once
+  int per_sm = 0;
+  cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pb::k_peer_density,
+                                                                 pb::kPeerThreads, 0);
+  if (oe != cudaSuccess) return pb::cuda_status(oe, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  if ((int64_t)per_sm * sms < blocks) {
+    pb::set_error("pb_peer_density_step: %lld blocks cannot be co-resident (%d per SM x %d SMs)",
+                  (long long)blocks, per_sm, sms);
+    return PB_ERR_INVALID;
+  }
   // the done count target is epoch * blocks on every rank: same grid everywhere
   cudaError_t e = pb::launch_pdl(pb::k_peer_density, dim3((unsigned)blocks), dim3(pb::kPeerThreads),
                                  0, (cudaStream_t)stream, a);

@@ -139,6 +139,13 @@ class Engine:
         self.partition = Partition(world, self.nc, partition_cells(self.nc, world))
         self.cell_lo, self.cell_hi = self.partition.ranges[rank]
         check_store_budget(config)
+        if 2 * int(config.ppc0) > _lib.PB_MAX_CELL_COUNT:
+            # the fixed-point bins hold < 2^16 particles per cell and species
+            # (csrc/common.cuh kMaxCellCount); leave room for fluctuations.
+            # Denser cells that still occur raise EngineError at the next sync.
+            raise ConfigError(f"ppc0={config.ppc0}: the fixed-point deposit represents at most "
+                              f"{_lib.PB_MAX_CELL_COUNT} particles of one species per cell; "
+                              f"ppc0 must be <= {_lib.PB_MAX_CELL_COUNT // 2}")
 
         self.stream = torch.cuda.Stream(self.device)
         self._side = torch.cuda.Stream(self.device)  # overlapped density epilogue
@@ -328,7 +335,7 @@ class Engine:
                 reduce_bins(self.bins, self.group)
             nxt = self.bins_pp[1 - self.cur].data_ptr() if clear_next else None
             _lib.check(self.lib.pb_density_step(
-                self.bins.data_ptr(), nxt, None, self._coef_c, self.ndep, self.nc, self.field_bc,
+                self.bins.data_ptr(), nxt, self.status.data_ptr(), self._coef_c, self.ndep, self.nc, self.field_bc,
                 self.left.data_ptr(), self.right.data_ptr(), self.rho.data_ptr(),
                 ctypes.c_void_p(st.cuda_stream)), "pb_density_step")
         self._next_clear = True
@@ -338,16 +345,17 @@ class Engine:
         from .peer import PeerBuffers
 
         pb = PeerBuffers({"bins0": nbins * 8, "bins1": nbins * 8, "rho": (nc + 1) * 8, "left": nc * 8,
-                          "right": nc * 8, "flags": 2 * _lib.PB_MAX_RANKS * 8},
+                          "right": nc * 8, "flags": _lib.PB_PEER_FLAG_WORDS * 8},
                          self.rank, self.world, self.group, self.device)
         if not pb.available:  # no P2P path on some pair: every rank keeps the NCCL allreduce
             pb.close()
             return
+        # exchange epochs live on the device (advanced by the exchange itself),
+        # so steps with the exchange can be captured in CUDA graphs; zeroed
+        # before the synchronize below, which orders it ahead of any exchange
+        self._peer_epoch_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
         torch.cuda.synchronize(self.device)  # the buffers were zeroed on the legacy stream
         self.peer = pb
-        # exchange epochs live on the device (advanced by the exchange itself),
-        # so steps with the exchange can be captured in CUDA graphs
-        self._peer_epoch_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.bins_pp = [pb.tensor("bins0", nbins, torch.int64), pb.tensor("bins1", nbins, torch.int64)]
         self.rho = pb.tensor("rho", nc + 1, torch.float64)
         self.left = pb.tensor("left", nc, torch.float64)
@@ -367,6 +375,7 @@ class Engine:
             d.flags[r] = pb.ptrs["flags"][r]
         d.rank, d.world, d.epoch = self.rank, self.world, 0
         d.epoch_dev = self._peer_epoch_dev.data_ptr()
+        d.timeout_ns = int(float(os.environ.get("PB_PEER_TIMEOUT_S", "60")) * 1e9)
         nxt = self.bins_pp[1 - self.cur].data_ptr() if clear_next else None
         _lib.check(self.lib.pb_peer_density_step(ctypes.byref(d), nxt, self._coef_c, self.ndep, self.nc,
                                                  self.field_bc, self.status.data_ptr(),
@@ -444,7 +453,8 @@ class Engine:
                 reduce_bins(self.bins, self.group)
             _lib.check(self.lib.pb_rho_epilogue(
                 self.bins.data_ptr(), self._coef_c, self.ndep, self.nc, self.field_bc, self.left.data_ptr(),
-                self.right.data_ptr(), self.rho.data_ptr(), self._sh()), "pb_rho_epilogue")
+                self.right.data_ptr(), self.rho.data_ptr(), self.status.data_ptr(), self._sh()),
+                "pb_rho_epilogue")
         self._next_clear = True
         return self.rho
 
@@ -615,11 +625,25 @@ class Engine:
                 "e": torch.zeros(2, group, nodes, dtype=torch.float64, device=dev),
                 "snap": torch.zeros(2, group, nodes, dtype=torch.float64, device=dev),
                 "host": torch.zeros(2, group, nodes, dtype=torch.float64).pin_memory(),
+                # absorbing walls: every step's live count per species
+                "nsnap": torch.zeros(2, group, len(self.sp), dtype=torch.int64, device=dev),
+                "nhost": torch.zeros(2, group, len(self.sp), dtype=torch.int64).pin_memory(),
             }
             # captured pipe graphs point at the old slots
             self.graphs = {k: g for k, g in self.graphs.items() if k[0] != "pipe"}
 
-    def run_pipelined(self, steps: int, e_source=None, on_result=None, group: int = None):
+    def _snap_counts(self, gp, j):
+        """Absorbing runs: snapshot every species' device live count of step
+        slot (gp, j) (stream order: after the step's compaction)."""
+        if not self.absorbing:
+            return
+        P = self._pipe
+        with torch.cuda.stream(self.stream):
+            for k, s in enumerate(self.sp):
+                P["nsnap"][gp, j, k:k + 1].copy_(s.n_dev, non_blocking=True)
+
+    def run_pipelined(self, steps: int, e_source=None, on_result=None, group: int = None,
+                      on_counts=None):
         """`steps` cycles driven from the host with the I/O overlapped.
 
         Steps run in blocks of `group` (default PB_PIPE_GROUP, 4; single
@@ -632,6 +656,8 @@ class Engine:
         b+1 before it waits for block b's results, then calls
         on_result(k, rho_host) for each of its steps -- every step's result
         is read, one block late, while the GPU works on the next block.
+        Absorbing runs also deliver each step's live counts per species to
+        on_counts(k, counts_host) (device snapshots, same D2H).
         Returns the number of results delivered (== steps)."""
         G = self._pipe_group(group)
         self._pipe_buffers(G)
@@ -649,6 +675,9 @@ class Engine:
             if on_result is not None:
                 for j in range(n):
                     on_result(k0 + j, P["host"][gp, j])
+            if on_counts is not None and self.absorbing:
+                for j in range(n):
+                    on_counts(k0 + j, P["nhost"][gp, j])
             delivered += n
 
         with_input = e_source is not None
@@ -689,6 +718,7 @@ class Engine:
                 self.stream.wait_stream(self._side)  # rho may come from the side stream
                 with torch.cuda.stream(self.stream):
                     P["snap"][gp, 0].copy_(rho, non_blocking=True)
+                self._snap_counts(gp, 0)
             with torch.cuda.stream(self.stream):
                 ev = torch.cuda.Event()
                 ev.record(self.stream)
@@ -698,6 +728,8 @@ class Engine:
             d2h.wait_event(ev)
             with torch.cuda.stream(d2h):
                 P["host"][gp, :n].copy_(P["snap"][gp, :n], non_blocking=True)
+                if self.absorbing:
+                    P["nhost"][gp, :n].copy_(P["nsnap"][gp, :n], non_blocking=True)
                 d = torch.cuda.Event()
                 d.record(d2h)
             d2h_done[gp] = d
@@ -736,6 +768,7 @@ class Engine:
                     _lib.check(self.lib.pb_compact(arr, m, self.status.data_ptr(),
                                                    self.compact_scratch.data_ptr(),
                                                    self.compact_scratch.numel(), self._sh()), "pb_compact")
+                self._snap_counts(gp, j)
                 if overlap:
                     snap_stream = self._side  # rho_j is final once epilogue j is done
                 else:
@@ -909,9 +942,11 @@ class Engine:
         self.peer.close()
         self.peer = None
 
-    def sync(self):
+    def sync(self, window: tuple = None):
         """Wait for enqueued work, fold the sticky device status into the
-        host tallies, raise the first recorded error, and reset the status."""
+        host tallies, raise the first recorded error, and reset the status.
+        window=(first, last): the steps run since the previous sync, named
+        in error messages when the status was not checked every step."""
         self.stream.synchronize()
         self._side.synchronize()
         raw = self.status.cpu().numpy()
@@ -931,10 +966,18 @@ class Engine:
             s = self.sp[isp]
             x = float(s.arr["x"][idx].item())
             cell = int(s.cell[idx].item())
+            where = f"step {self.step_index}" if window is None else f"steps {window[0]}-{window[1]}"
             raise CflViolation(
-                f"step {self.step_index}, phase resort: species {s.name!r} cell {cell}: "
+                f"{where}, phase resort: species {s.name!r} cell {cell}: "
                 f"displacement of {int(math.floor(x))} cells reaches across the whole domain"
             )
+        if st.code == _lib.PB_ERR_OVERFLOW:
+            raise EngineError(
+                f"step {self.step_index}: fixed-point deposit overflow: a cell holds {int(st.overflow)} "
+                f"particles of one species (the bins represent at most {_lib.PB_MAX_CELL_COUNT})")
+        if st.code == _lib.PB_ERR_PEER:
+            raise EngineError(f"step {self.step_index}: density exchange failed (a peer rank timed out "
+                              "or reported an error); this step's density is invalid on every rank")
         if st.code != _lib.PB_OK:
             raise EngineError(f"step {self.step_index}: device status {st.code}")
 

@@ -47,7 +47,11 @@ class RunMetrics:
 
 
 class _LazyStores(list):
-    """on_step's "stores": host copies of this rank's species, fetched on use."""
+    """on_step's "stores": a one-element list holding the host copy of THIS
+    rank's species (fetched on first use).  The reference passes every
+    worker's store (harness.py:246-253); with one process per GPU a rank
+    holds only its own shard, so len() is 1 on every rank -- gather across
+    ranks explicitly if all shards are needed."""
 
     def __init__(self, engine):
         super().__init__()
@@ -60,11 +64,11 @@ class _LazyStores(list):
             self._loaded = True
 
     def __len__(self):
-        return self._engine.world
+        return 1
 
     def __getitem__(self, i):
         self._load()
-        return super().__getitem__(0 if i in (0, -1) and self._engine.world == 1 else i)
+        return super().__getitem__(i)
 
     def __iter__(self):
         self._load()
@@ -95,16 +99,76 @@ def _global_totals(engine):
     return tot
 
 
+# Fast path (on_step=None): the device status is checked every CHECK_EVERY
+# steps instead of every step; an error names the window it occurred in.
+CHECK_EVERY = int(os.environ.get("PB_CHECK_EVERY", "128"))
+
+
+def _run_graphed(engine, config, names):
+    """on_step=None and no collisions: the steps run as replayed CUDA graphs
+    through Engine.run_pipelined (blocks of PB_PIPE_GROUP steps, every graph
+    captured before the timed loop, like the reference's init before t_run),
+    the status is checked every CHECK_EVERY steps, and the per-step
+    diagnostics come from device counters (absorbing walls: each step's live
+    counts snapshotted on device; otherwise the totals are invariant).
+    Returns (diagnostics rows 1..n, phase seconds)."""
+    n = int(config.n_steps)
+    engine.prepare_pipe_graphs(with_input=False, horizon=n)
+    tot0 = _global_totals(engine)
+    counts = np.zeros((n, len(names)), dtype=np.int64) if engine.absorbing else None
+    t_run = time.perf_counter()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(engine.stream)
+    done = 0
+    while done < n:
+        m = min(max(1, CHECK_EVERY), n - done)
+
+        def on_counts(k, c, base=done):
+            counts[base + k] = c.numpy()
+
+        engine.run_pipelined(m, on_counts=on_counts if counts is not None else None)
+        engine.sync(window=(done + 1, done + m))
+        done += m
+    ev1.record(engine.stream)
+    engine.stream.synchronize()
+    total = time.perf_counter() - t_run
+    if counts is not None and engine.world > 1:
+        import torch.distributed as dist
+
+        t = torch.from_numpy(counts).to(engine.device)
+        dist.all_reduce(t, group=engine.group)
+        counts = t.cpu().numpy()
+    zero = CollisionTally()
+    rows = [_diag_row(step, names, counts[step - 1] if counts is not None else tot0, zero)
+            for step in range(1, n + 1)]
+    phase = {k: 0.0 for k in PHASE_KEYS}
+    # one fused launch does gather + push + transfer + deposit: its device
+    # time is reported as the mover phase (field and epilogue kernels included)
+    phase["mover"] = ev0.elapsed_time(ev1) * 1e-3 if n else 0.0
+    phase["total"] = total if n else 0.0
+    return rows, phase
+
+
 def run_simulation(config, on_step=None, *, rank=0, world=1, group=None,
                    device=None, init="host") -> RunMetrics:
-    """Execute n_steps of the cycle on the GPU; returns timers and diagnostics."""
+    """Execute n_steps of the cycle on the GPU; returns timers and diagnostics.
+
+    With on_step=None (and no collisions) the steps replay as CUDA graphs with
+    the status checked every CHECK_EVERY steps (_run_graphed); with on_step
+    every step is run eagerly, checked, and its state handed to on_step."""
     canonical = config.canonical() if hasattr(config, "canonical") else False
     cls = CanonicalEngine if canonical else Engine
-    engine = cls(config, device=device, rank=rank, world=world, group=group, init=init)
+    fast = on_step is None and not canonical
+    engine = cls(config, device=device, rank=rank, world=world, group=group, init=init,
+                 check_every=0 if fast else 1)
     names = [sp.name for sp in config.species]
     zero = CollisionTally()
     diagnostics = [_diag_row(0, names, _global_totals(engine), zero)]
     tally_sum = CollisionTally()
+    if fast:
+        rows, phase = _run_graphed(engine, config, names)
+        diagnostics += rows
+        return _finish(config, engine, names, diagnostics, phase, tally_sum, world, rank, canonical)
     t0 = time.perf_counter()
     for step in range(1, config.n_steps + 1):
         rho, e = engine.step(timed=True)
@@ -122,6 +186,10 @@ def run_simulation(config, on_step=None, *, rank=0, world=1, group=None,
     engine.sync()
     phase = engine.phase_seconds()
     phase["total"] = time.perf_counter() - t0 if config.n_steps > 0 else 0.0
+    return _finish(config, engine, names, diagnostics, phase, tally_sum, world, rank, canonical)
+
+
+def _finish(config, engine, names, diagnostics, phase, tally_sum, world, rank, canonical):
     metrics = RunMetrics(
         phase_seconds=phase, diagnostics=diagnostics, config_hash=config.config_hash(),
         worker_count=world, layout="canonical_soa" if canonical else "flat_soa", backend=BACKEND,

@@ -140,3 +140,54 @@ def test_fused_move_aos_and_table_bitwise(seed, with_accel, with_yp, cu):
     t = tab[: int(counts[0])].copy()
     cu.fused_move_table(t, 0.3, -0.2, 2.0, True, True)
     assert bits_equal(t.ravel(), g[f"s{seed}_table"].ravel())
+
+
+def test_concurrent_block_calls_match_serial(ref, cu):
+    """The reference's call pattern (pkg/src/picmc/mover.py:251-270): one
+    fused_move per block of `grainsize` cells on the SAME species arrays,
+    from several threads at once.  Each call stages and writes back only its
+    block's slot span, so the result equals the serial compiled run."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(11)
+    nc, cap, grain = 301, 12, 7
+    counts = rng.integers(0, cap + 1, size=nc).astype(np.int64)
+    offs = np.arange(nc, dtype=np.int64) * cap
+    total = nc * cap
+    arrs = [np.zeros(total) for _ in range(4)]
+    for j in range(nc):
+        sl = slice(offs[j], offs[j] + counts[j])
+        arrs[0][sl] = rng.random(counts[j])
+        for a in arrs[1:]:
+            a[sl] = rng.standard_normal(counts[j]) * 0.4
+    accel = rng.standard_normal(nc + 1) * 0.05
+    a = [v.copy() for v in arrs]
+    b = [v.copy() for v in arrs]
+    blocks = [(lo, min(lo + grain, nc)) for lo in range(0, nc, grain)]
+    for lo, hi in blocks:
+        ref.fused_move(accel[lo:hi + 1], a[0], a[1], a[2], a[3], offs[lo:hi], counts[lo:hi], 3.0)
+    with ThreadPoolExecutor(8) as ex:
+        list(ex.map(lambda blk: cu.fused_move(accel[blk[0]:blk[1] + 1], b[0], b[1], b[2], b[3],
+                                              offs[blk[0]:blk[1]], counts[blk[0]:blk[1]], 3.0),
+                    blocks * 1))
+    for u, v in zip(a, b):
+        assert bits_equal(u, v)
+    # deposit / gather per block, concurrently, equal the serial calls
+    with ThreadPoolExecutor(8) as ex:
+        got = list(ex.map(lambda blk: cu.deposit_partials(b[0], offs[blk[0]:blk[1]],
+                                                          counts[blk[0]:blk[1]]), blocks))
+    for (lo, hi), (lc, rc) in zip(blocks, got):
+        lr, rr = ref.deposit_partials(a[0], offs[lo:hi], counts[lo:hi])
+        assert bits_equal(lr, lc) and bits_equal(rr, rc)
+        assert bits_equal(ref.gather(accel[lo:hi + 1], a[0], offs[lo:hi], counts[lo:hi]),
+                          cu.gather(accel[lo:hi + 1], b[0], offs[lo:hi], counts[lo:hi]))
+
+
+def test_block_span_out_of_bounds_raises(cu):
+    x, vx, vy, yp, offs, counts = packed(0)
+    bad = offs.copy()
+    bad[-1] = x.shape[0]
+    counts = counts.copy()
+    counts[-1] = 1
+    with pytest.raises(ValueError):
+        cu.fused_move(None, x, vx, vy, yp, bad, counts, 1.0)

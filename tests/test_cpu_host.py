@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for name in names:
         assert hasattr(lib, name), name
     assert set(names) == set(_lib.exported_names())
-    assert lib.pb_abi_version() == 1
+    assert lib.pb_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_library_argument_errors_without_gpu():

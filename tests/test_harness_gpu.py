@@ -217,3 +217,54 @@ def test_fused_field_pipeline_bitwise(cuda, nc, passes):
             assert bits_equal(a_s.cpu().numpy(), b_s.cpu().numpy()), code
         assert bits_equal(a_phi.cpu().numpy(), b_phi.cpu().numpy()), code
         assert bits_equal(a_e.cpu().numpy(), b_e.cpu().numpy()), code
+
+
+def _small_sheath(n_steps=60, nc=256, sort_every=10):
+    from paper_2404_10270_b200.config import load_config
+
+    cfg = load_config("configs/c3_sheath_absorbing.toml")
+    from dataclasses import replace
+
+    from paper_2404_10270_b200 import Grid1D
+
+    return replace(cfg, grid=Grid1D.from_cells(nc, nc * 1e-5), ppc0=40, n_steps=n_steps,
+                   sort_every=sort_every)
+
+
+@pytest.mark.parametrize("which", ["periodic_field", "sheath", "periodic_nofield"])
+def test_graphed_run_simulation_matches_per_step_path(cuda, which, monkeypatch):
+    """on_step=None replays CUDA graphs (status checked every CHECK_EVERY
+    steps, diagnostics from device counters); the per-step diagnostics and
+    phase keys equal the eager on_step path's, every step, exactly."""
+    from paper_2404_10270_b200 import harness, run_simulation
+
+    if which == "sheath":
+        cfg = _small_sheath()
+    else:
+        cfg = _cfg_from(load_golden(f"run_{which}.npz"), sort_every=5)
+    monkeypatch.setattr(harness, "CHECK_EVERY", 16)
+    fast = run_simulation(cfg)
+    slow = run_simulation(cfg, on_step=lambda s, st: None)
+    assert fast.diagnostics == slow.diagnostics
+    if which == "sheath":  # walls actually absorbed something, and counts moved
+        tot = [r["total_e"] for r in fast.diagnostics]
+        assert tot[-1] < tot[0] and len(set(tot)) > 2
+        assert fast.absorbed == slow.absorbed
+    assert set(fast.phase_seconds) == set(slow.phase_seconds)
+    assert fast.phase_seconds["total"] > 0.0
+
+
+def test_graphed_run_simulation_raises_cfl_in_window(cuda, monkeypatch):
+    """A domain-scale jump still raises CflViolation on the graphed path,
+    naming the window of steps since the last status check."""
+    from dataclasses import replace
+
+    from paper_2404_10270_b200 import harness, run_simulation
+    from paper_2404_10270_b200.errors import CflViolation
+
+    g = load_golden("run_periodic_nofield.npz")
+    cfg = _cfg_from(g)
+    cfg = replace(cfg, temperatures_ev=[1e9] + list(cfg.temperatures_ev[1:]), n_steps=40)
+    monkeypatch.setattr(harness, "CHECK_EVERY", 16)
+    with pytest.raises(CflViolation, match=r"steps 1-16, phase resort"):
+        run_simulation(cfg)

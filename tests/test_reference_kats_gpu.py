@@ -52,7 +52,7 @@ def device_rho(defs, flats, weights, nc, bc="periodic"):
     rho = torch.zeros(nc + 1, dtype=torch.float64, device=dev)
     cc = (ctypes.c_double * max(ndep, 1))(*coef)
     code = _lib.PB_FIELD_PERIODIC if bc == "periodic" else _lib.PB_FIELD_DIRICHLET
-    _lib.check(lib.pb_density_step(bins.data_ptr(), None, None, cc, ndep, nc, code, left.data_ptr(),
+    _lib.check(lib.pb_density_step(bins.data_ptr(), None, status.data_ptr(), cc, ndep, nc, code, left.data_ptr(),
                                    right.data_ptr(), rho.data_ptr(), sh))
     return rho.cpu().numpy(), np.array(coef)
 

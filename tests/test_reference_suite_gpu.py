@@ -1,0 +1,81 @@
+"""The reference's OWN tests, run against the cuda backend.
+
+The unmodified reference (baseline/_ref, installed by
+scripts/install_reference.sh together with its pkg/tests and pkg/configs)
+is imported with the cuda backend selected through its
+`picmc.backends` seam (tests/refsuite/picmc_cuda_plugin.py: the two-line
+change of INTEGRATION.md §4).  The reference then drives the cuda kernels
+through its own call pattern: `mover_phase` submits one task per block of
+`grainsize` cells on the same species arrays to a threaded `Scheduler`
+(pkg/src/picmc/mover.py:227-271, scheduler.py:143-159), `deposit_charge`
+calls `deposit_partials` per block, and `run_simulation` runs with
+worker_count 1..8.  The suite must pass unmodified:
+
+* pkg/tests/test_mover.py (incl. test_mover_phase_parallel_matches_serial_
+  bitwise: workers = 4, grainsize = 3),
+* pkg/tests/test_fields.py, test_harness.py, test_decomposition.py,
+* pkg/tests/test_acceptance.py criteria 04 (decomposition transparency,
+  workers 1/2/4/8, 100 steps with collisions and the field solve) and 08
+  (free-streaming exactness, 1000 steps, workers = 2),
+* pkg/tests/test_backends.py with `load_backend("compiled")` answered by the
+  cuda backend, so pure (NumPy) vs cuda is compared bit for bit.
+"""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+SUITE = os.path.join(REF, "picmc_suite")
+
+
+def _run(tmp_path, args, substitute=False, timeout=900):
+    if not os.path.isdir(os.path.join(SUITE, "tests")):
+        pytest.fail("reference suite missing: run scripts/install_reference.sh (baseline/_ref)")
+    calls = tmp_path / "calls.json"
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([os.path.join(ROOT, "tests", "refsuite"), ROOT, REF,
+                                         env.get("PYTHONPATH", "")])
+    env["PICMC_CUDA_CALLS"] = str(calls)
+    env["PICMC_CUDA_SUBSTITUTE"] = "1" if substitute else "0"
+    cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "picmc_cuda_plugin", "-p",
+           "no:cacheprovider", f"--rootdir={SUITE}", *args]
+    r = subprocess.run(cmd, cwd=SUITE, env=env, capture_output=True, text=True, timeout=timeout)
+    tail = (r.stdout + r.stderr)[-4000:]
+    assert r.returncode == 0, tail
+    got = json.loads(calls.read_text())
+    assert got["backend"] == "cuda"
+    assert os.path.realpath(got["picmc"]).startswith(os.path.realpath(REF))
+    return got["calls"], tail
+
+
+def test_reference_mover_fields_harness(tmp_path):
+    calls, tail = _run(tmp_path, ["tests/test_mover.py", "tests/test_fields.py",
+                                  "tests/test_harness.py", "tests/test_decomposition.py"])
+    assert calls.get("fused_move", 0) > 100 and calls.get("deposit_partials", 0) > 10, calls
+    assert "passed" in tail and "failed" not in tail
+
+
+def test_reference_acceptance_04_08(tmp_path):
+    calls, tail = _run(tmp_path, [
+        "tests/test_acceptance.py::test_criterion_04_decomposition_transparency",
+        "tests/test_acceptance.py::test_criterion_08_free_streaming_exactness"])
+    assert "[criterion 04] PASS" in tail and "[criterion 08] PASS" in tail, tail
+    # criterion 08 alone: 1000 steps x 2 species x 5 blocks of 7 cells
+    assert calls.get("fused_move", 0) >= 10000, calls
+
+
+def test_reference_backends_pure_vs_cuda(tmp_path):
+    calls, tail = _run(tmp_path, [
+        "tests/test_backends.py",
+        "--deselect", "tests/test_backends.py::test_backend_selector",
+        "--deselect", "tests/test_backends.py::test_backend_names"], substitute=True)
+    for k in ("deposit_partials", "gather", "fused_move", "fused_move_table", "fused_move_aos"):
+        assert calls.get(k, 0) > 0, calls
+    assert "skipped" not in tail, tail
