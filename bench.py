@@ -103,6 +103,30 @@ def workload_config(name, world, sort_every):
     return cfg, desc, scaling
 
 
+def config_dict(cfg, desc, scaling, world):
+    """The `config` object of the JSON line; the same for both arms."""
+    from paper_2404_10270_b200.engine import Engine, partition_cells, sort_periods_for
+
+    nc_total = cfg.grid.nc
+    ranges = partition_cells(nc_total, world)
+    active = [sp for sp in cfg.species if sp.active_mover]
+    per_rank = [(hi - lo) * cfg.ppc0 * len(active) for lo, hi in ranges]
+    alg = sum((ranges[0][1] - ranges[0][0]) * cfg.ppc0 * species_alg_bytes(sp, cfg.b_field_t is not None)
+              for sp in cfg.species)
+    return {
+        "workload": desc,
+        "nc_per_gpu": nc_total // world if scaling == "weak" else nc_total, "nc_total": nc_total,
+        "ppc0_per_species": cfg.ppc0,
+        "particles_per_gpu": per_rank[0], "particles_total": sum(per_rank),
+        "sort_every": cfg.sort_every,
+        "sort_periods": sort_periods_for(cfg, cfg.sort_every, Engine.sort_ratio_cap),
+        "parallelism": f"particle shards x{world}, replicated grid",
+        "l2": (f"inputs {alg / 1e9:.2f} GB/GPU vs 126 MB L2" +
+               ("; each step streams past L2, no flush needed" if alg > 2 * 126e6
+                else "; L2-resident, roofline not meaningful")),
+    }
+
+
 # ---------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
@@ -167,14 +191,32 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def committed_traffic():
-    """dram bytes per push launch from the committed ncu capture, if any."""
+def lib_digest() -> str:
+    """sha256 of the loaded libpicmc_b200.so (identifies the build)."""
+    import hashlib
+
+    from paper_2404_10270_b200 import _lib
+
+    with open(_lib.LIB_PATH, "rb") as fh:
+        return hashlib.sha256(fh.read()).hexdigest()
+
+
+def build_traffic(workload):
+    """DRAM bytes per mover launch from an ncu --set full capture of THIS
+    build (profiles/push_deposit_traffic.json records the library's sha256
+    next to the numbers); None when the capture is of another build."""
     path = os.path.join(ROOT, "profiles", "push_deposit_traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh)
+            rec = json.load(fh)
     except (OSError, ValueError):
-        return None
+        return None, "no capture"
+    ent = rec.get("workloads", {}).get(workload)
+    if ent is None:
+        return None, f"no capture for {workload}"
+    if rec.get("lib_sha256") != lib_digest():
+        return None, "capture is of another build"
+    return ent.get("dram_bytes_per_launch"), f"ncu --set full of this build ({rec.get('source', path)})"
 
 
 # ---------------------------------------------------------------------------
@@ -246,7 +288,7 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
-    from paper_2404_10270_b200 import Engine
+    from paper_2404_10270_b200 import Engine, run_simulation
 
     # one GPU per rank; --dist-backend gloo lets several ranks share a GPU to
     # exercise the multi-rank path where only one GPU is visible
@@ -260,11 +302,18 @@ def run_ours(args, rank, world, local_rank):
     boris = cfg.b_field_t is not None
     alg_bytes = sum(s.n * species_alg_bytes(s.sp, boris) for s in eng.sp)
 
-    # Every CUDA graph the timed replay can need (bin parity x sort buffer
-    # state) is captured before timing; periodic sorts run eagerly.
+    def max_over_ranks(*vals):
+        if world == 1:
+            return vals
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return tuple(float(v) for v in t)
+
     # one untimed sort of every species first: first-use costs (module
     # loading, scratch allocation) stay out of the timed region; physics is
-    # order-free.  Then every graph the timed replay can need is captured.
+    # order-free.  Then every CUDA graph the timed replay can need (bin parity
+    # x sort buffer state) is captured before timing; periodic sorts run
+    # eagerly inside the timed region.
     eng.sort_by_cell()
     eng.sync()
     eng.prepare_graphs(args.warmup + args.steps)
@@ -273,13 +322,15 @@ def run_ours(args, rank, world, local_rank):
         time.sleep(0.3)  # sampler start-up; the warm-up below brings the clocks back up
         eng.replay(args.warmup)
         eng.sync()
+        eng.mover_ns = eng.mover_launches = 0
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
         graphs_before = len(eng.graphs)
+        step0 = eng.step_index
         start.record(eng.stream)
-        # windows of 200 steps (events between graph launches cost nothing) to
-        # show whether a slow run is uniformly slow or had a hiccup
+        # windows of up to 200 steps (events between graph launches cost
+        # nothing) to show whether a slow run is uniformly slow or had a hiccup
         marks, left = [], args.steps
         while left > 0:
             k = min(200, left)
@@ -294,23 +345,41 @@ def run_ours(args, rank, world, local_rank):
     eng.sync()
     if world > 1:
         dist.barrier()
-    ms = start.elapsed_time(end) / args.steps
+    raw_ms = start.elapsed_time(end) / args.steps
     win_ms, prev = [], start
     for k, ev in marks:
         win_ms.append(prev.elapsed_time(ev) / k)
         prev = ev
-    # The mover kernel alone: CUDA events on the engine stream right around the
-    # pb_push_deposit launch, over eager steps (host stays ahead of the GPU).
-    eng.phase_events.clear()
-    for _ in range(min(args.steps, 50)):
-        eng.step(timed=True)
-    eng.sync()
-    push_ms = float(np.mean(eng.mover_ms()))
+    # The mover kernel's own duration inside the graph-replayed timed steps:
+    # the persistent movers' in-kernel clock (pb_status.mover_ns, first block
+    # start -> last warp end, %globaltimer).
+    push_ms = eng.mover_ns / max(1, eng.mover_launches) / 1e6
+    mover_launches = eng.mover_launches
     mover_kernel = eng.lib.pb_last_mover_kernel().decode()
-    if world > 1:
-        t = torch.tensor([ms, push_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, push_ms = float(t[0]), float(t[1])
+    # Amortised sort cost: the periodic sorts that fall inside the K timed
+    # steps are there at their actual count; a window shorter than a sort
+    # period (the driver's 20 steps) is charged the missing fraction
+    # (expected = K / period sorts per species) at the measured sort time,
+    # or credited when the window held more than its share.
+    sort_ms = []
+    for k, p in enumerate(eng.sort_periods):
+        if not p:
+            sort_ms.append(0.0)
+            continue
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        eng.sort_by_cell([k])  # warm
+        e0.record(eng.stream)
+        for _ in range(3):
+            eng.sort_by_cell([k])
+        e1.record(eng.stream)
+        torch.cuda.synchronize(dev)
+        sort_ms.append(e0.elapsed_time(e1) / 3)
+    in_window = [sum(1 for i in range(step0 + 1, step0 + args.steps + 1) if p and i % p == 0)
+                 for p in eng.sort_periods]
+    expected = [args.steps / p if p else 0.0 for p in eng.sort_periods]
+    adjust_ms = sum((e - n) * t for e, n, t in zip(expected, in_window, sort_ms)) / args.steps
+    ms = raw_ms + adjust_ms
+    ms, push_ms, raw_ms = max_over_ranks(ms, push_ms, raw_ms)
     pushes_total = pushes_rank * world
     if world > 1:
         t = torch.tensor([pushes_rank], dtype=torch.int64, device=dev)
@@ -320,8 +389,8 @@ def run_ours(args, rank, world, local_rank):
 
     # e2e: the public host-driven API (Engine.run_pipelined): every step copies
     # its E-field input H2D from pinned host memory and its rho result D2H into
-    # pinned host memory, which the host reads (one block of steps late, while the GPU
-    # runs the next step).
+    # pinned host memory, which the host reads (one block of steps late, while
+    # the GPU runs the next block).
     nodes = nc_total + 1
     e_host = torch.zeros(nodes, dtype=torch.float64).pin_memory()
     e2e_steps = max(3, min(args.steps, 400))
@@ -349,22 +418,20 @@ def run_ours(args, rank, world, local_rank):
     e2e_ms = max(t0.elapsed_time(t1) / e2e_steps, wall_ms)
     e2e_graphs_timed = len(eng.graphs) - pipe_graphs0
     assert len(seen) == e2e_steps
-    if world > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t[0])
+    (e2e_ms,) = max_over_ranks(e2e_ms)
     e2e_value = pushes_total / (e2e_ms * 1e-3)
 
-    # Speed-of-light probe (last: it overwrites particle state): the same
-    # read/write byte mix streamed with a trivial update and no physics.
+    # Speed-of-light probe (it overwrites particle state): the same read/write
+    # byte mix per species kind streamed with a trivial update and no physics.
     import ctypes
     arr, nsp = eng._species()
     actual_bytes = 0.0
     for s in eng.sp:
+        if s.kind == 0:
+            continue
         cell_b = 1.0 if s.cell8 is not None else 4.0
-        actual_bytes += s.n * ((32.0 + cell_b) if s.kind != 1 else (48.0 if s.has_yp else 24.0))
-    # (the probe streams the c2 byte mix: x, vx [, vy, yp] and the cell index
-    # the mover reads -- cell8 where in use -- per species)
+        base = {1: 24.0, 2: 32.0 + cell_b, 3: 64.0 + cell_b}[s.kind]
+        actual_bytes += s.n * (base + (24.0 if s.has_yp else 0.0))
     torch.cuda.synchronize(dev)
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(2):
@@ -375,21 +442,40 @@ def run_ours(args, rank, world, local_rank):
     s1.record(eng.stream)
     torch.cuda.synchronize(dev)
     sol_ms = s0.elapsed_time(s1) / 10
+    exchange = ("none (one GPU)" if world == 1 else
+                "peer memory: pb_peer_density_step (bins summed over NVLink/IPC + epilogue, one kernel)"
+                if eng.peer is not None else
+                f"{args.dist_backend} all_reduce of the fixed-point bins + pb_density_step")
+    eng.close()
+    del eng
+    torch.cuda.empty_cache()
+
+    # The drop-in step API: run_simulation(config) with on_step=None replays
+    # CUDA graphs through run_pipelined (status checked every CHECK_EVERY
+    # steps); rate = pushes / the reference's own "total" timer (the step
+    # loop, after init and graph capture -- as picmc times t_run).
+    from dataclasses import replace
+    rs_cfg = replace(cfg, n_steps=e2e_steps)
+    m = run_simulation(rs_cfg, rank=rank, world=world, device=dev, init="device")
+    names = [sp.name for sp in cfg.species]
+    rs_pushes = sum(sum(r[f"total_{n}"] for n, sp in zip(names, cfg.species) if sp.active_mover)
+                    for r in m.diagnostics[:-1])
+    (rs_total,) = max_over_ranks(m.phase_seconds["total"])
+    rs_value = rs_pushes / rs_total
 
     peak, peak_kind = measured_peak()
     achieved = alg_bytes / (push_ms * 1e-3) / 1e9
-    traffic = committed_traffic()
-    # k_partials_clear + k_stitch (density) + k_push_quad; field solve: one
-    # k_smooth_pass per pass + one Poisson kernel + k_efield; walls: k_compact
+    traffic, traffic_src = build_traffic(args.workload)
+    # k_partials_clear + k_stitch (density) + the mover; field solve: one
+    # k_smooth_pass per pass + the Poisson kernels + E; walls: k_compact
     launches_per_step = 3
     if cfg.field_solve:
         launches_per_step += cfg.smoothing_passes + 2
-    if eng.absorbing:
+    if cfg.particle_boundary == "absorbing":
         launches_per_step += 1
     # our kernels per sort: k_cell_count + k_cell_scatter (+ k_cell8_build
     # where the compressed cell index is kept); the scan is CUB's
-    n_sort_kernels = sum((args.steps // p) * (3 if s.cell8 is not None else 2)
-                         for p, s in zip(eng.sort_periods, eng.sp) if p)
+    n_sort_kernels = sum(n * 3 for n in in_window)
     out = {
         "metric": METRIC,
         "value": value,
@@ -403,28 +489,20 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (device init_plasma with the reference splitmix64 streams, seed 20260819)",
-        "config": {
-            "workload": desc,
-            "nc_per_gpu": nc_total // world if scaling == "weak" else nc_total, "nc_total": nc_total,
-            "ppc0_per_species": cfg.ppc0,
-            "particles_per_gpu": pushes_rank, "particles_total": pushes_total,
-            "sort_every": cfg.sort_every, "sort_periods": eng.sort_periods,
-            "parallelism": f"particle shards x{world}, replicated grid",
-            "density_exchange": ("none (one GPU)" if world == 1 else
-                                 "peer memory: pb_peer_density_step (bins summed over NVLink/IPC + epilogue, "
-                                 "one kernel)" if eng.peer is not None else
-                                 f"{args.dist_backend} all_reduce of the fixed-point bins + pb_density_step"),
-            "l2": (f"inputs {alg_bytes / 1e9:.2f} GB/GPU vs 126 MB L2" +
-                   ("; each step streams past L2, no flush needed" if alg_bytes > 2 * 126e6
-                    else "; L2-resident, roofline not meaningful")),
-        },
+        "config": config_dict(cfg, desc, scaling, world),
+        "density_exchange": exchange,
+        "sort_amortisation": {
+            "raw_ms_per_step": raw_ms, "sorts_in_window": in_window,
+            "expected_sorts": [round(e, 4) for e in expected],
+            "sort_ms": [round(t, 5) for t in sort_ms], "adjust_ms_per_step": adjust_ms,
+            "note": "ms_per_step = raw + (expected - actual sorts in the window) x sort time / steps"},
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "peak_source": peak_kind, "kernel": mover_kernel,
             "alg_bytes_per_launch": alg_bytes, "push_ms": push_ms,
-            # committed ncu capture of the c2 bench launch (profiles/)
-            "traffic": (None if traffic is None or args.workload != "c2"
-                        else traffic.get("dram_bytes_per_launch")),
+            "push_ms_source": (f"in-kernel clock over the {mover_launches} graph-replayed mover launches "
+                               "of the timed steps"),
+            "traffic": traffic, "traffic_source": traffic_src,
         },
         "e2e": {"value": e2e_value, "unit": "particle-pushes/s",
                 "h2d_bytes_per_step": 0 if cfg.field_solve else nodes * 8,
@@ -433,15 +511,22 @@ def run_ours(args, rank, world, local_rank):
                         "into pinned memory read by the host (one graph block of PB_PIPE_GROUP steps late, "
                         "overlapped); max(device, wall)",
                 "graphs_captured_in_timed_region": e2e_graphs_timed},
+        "e2e_run_simulation": {
+            "value": rs_value, "unit": "particle-pushes/s", "steps": e2e_steps,
+            "vs_run_pipelined": rs_value / e2e_value,
+            "path": "paper_2404_10270_b200.run_simulation(config) (the picmc.run_simulation signature), "
+                    "on_step=None: graph replay, status every CHECK_EVERY steps; pushes / phase_seconds"
+                    "['total']"},
         "gpu_launches": args.steps * launches_per_step + n_sort_kernels,
-        "timing_windows_ms": {"steps_per_window": 200, "min": min(win_ms), "median": float(np.median(win_ms)),
-                              "max": max(win_ms), "argmax": int(np.argmax(win_ms)),
-                              "all": [round(w, 5) for w in win_ms],
+        "timing_windows_ms": {"steps_per_window": min(200, args.steps), "min": min(win_ms),
+                              "median": float(np.median(win_ms)), "max": max(win_ms),
+                              "argmax": int(np.argmax(win_ms)), "all": [round(w, 5) for w in win_ms],
                               "graphs_captured_in_timed_region": graphs_timed},
         "sol_probe": {"ms": sol_ms, "actual_bytes": actual_bytes, "gbs": actual_bytes / (sol_ms * 1e-3) / 1e9,
                       "mover_actual_gbs": actual_bytes / (push_ms * 1e-3) / 1e9,
-                      "note": "pb_stream_sol: the mover's bytes (incl. its cell index), trivial update, "
-                              "no deposit"},
+                      "mover_vs_probe": sol_ms / push_ms,
+                      "note": "pb_stream_sol: the mover's bytes per species kind (incl. its cell index), "
+                              "trivial update, no deposit"},
     }
     return out, clk.summary()
 
@@ -468,12 +553,16 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
+        if args.sort_every is None and args.workload == "c2":
+            args.sort_every = 100
+        cfg, desc, scaling = workload_config(args.workload, args.gpus, args.sort_every)
+        ref_config = config_dict(cfg, desc, scaling, args.gpus)
         cpu = cpu_reference_rate(target_seconds=max(2.0, args.cpu_seconds))
         line = {
             "impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": cpu["unit"],
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": "config 2 shape (sampled on host)"},
+            "data": "synthetic", "config": ref_config,
             "cpu_baseline": cpu,
             "e2e": {"value": cpu["value"], "unit": cpu["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }

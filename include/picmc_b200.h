@@ -107,9 +107,16 @@ typedef struct pb_status {
                                            resets the counters, so they are
                                            zero again after every launch */
   uint64_t tile_next2;                  /* second work list (split mover)   */
+  /* In-kernel clock of the persistent movers (k_push_split / ring / quad):
+   * every block records its start (%globaltimer, min), the last warp to
+   * finish adds (end - first start) to mover_ns and counts the launch, so
+   * the movers' own duration is measured inside graph replays. */
+  uint64_t mover_t0;                    /* UINT64_MAX between launches      */
+  uint64_t mover_ns;
+  uint64_t mover_launches;
 } pb_status;
 /* The caller resets *status before each pb_push_deposit: all zero except
- * cfl_index = UINT64_MAX (the engine copies a template). */
+ * cfl_index = mover_t0 = UINT64_MAX (the engine copies a template). */
 
 /* ---- library ------------------------------------------------------------ */
 int pb_abi_version(void);
@@ -244,15 +251,6 @@ int pb_compute_efield_clear(const double *phi, double *e, int64_t nc,
                             double dx, int field_bc, uint64_t *clr_a,
                             uint64_t *clr_b, int64_t nwords, void *stream);
 
-/* smoothing (passes > 0: rho_s receives the smoothed density) + the scan
- * Poisson solve + E in one cooperative launch with grid-wide syncs between
- * the phases; bitwise pb_smooth_density + pb_solve_poisson_scan +
- * pb_compute_efield (which it falls back to when the grid cannot be
- * co-resident). */
-int pb_field_pipeline(const double *rho, double *rho_s, double *phi, double *e,
-                      int64_t nc, int passes, double dx, double eps0,
-                      int field_bc, double phi_left, double phi_right,
-                      void *scratch, void *stream);
 
 /* Roofline probe: streams the mover's exact read/write bytes per species with
  * a trivial update (no physics, no deposit).  Destroys particle state. */
@@ -340,6 +338,11 @@ int pb_canonical_keys(const pb_species *src, const pb_canon *cv,
 /* pb_canonical_resort for species 0..nsp-1 (cv[k], species id k) in one
  * call, then the new live counts (offs[nc] of each) into the host array
  * n_new[nsp].  Synchronises the stream. */
+/* Stores of at least n particles take the scatter resort in
+ * pb_canonical_step (default 2^20; smaller stores keep the full key sort,
+ * bitwise the same result).  Process-wide. */
+int pb_set_canonical_scatter_min(int64_t n);
+
 int pb_canonical_step(const pb_species *src, const pb_species *dst,
                       const pb_canon *cv, int nsp, const double *e_nodes,
                       int64_t nc, int particle_bc, pb_status *status,

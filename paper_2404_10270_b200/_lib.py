@@ -65,6 +65,8 @@ class PbStatus(ctypes.Structure):
         ("overflow", _i64),
         ("tile_next", ctypes.c_uint64), ("tile_done", ctypes.c_uint64),
         ("tile_next2", ctypes.c_uint64),
+        ("mover_t0", ctypes.c_uint64), ("mover_ns", ctypes.c_uint64),
+        ("mover_launches", ctypes.c_uint64),
     ]
 
 
@@ -113,6 +115,7 @@ STATUS_BYTES = ctypes.sizeof(PbStatus)
 # name -> (restype, argtypes); mirrors include/picmc_b200.h one to one.
 _SIGS = {
     "pb_abi_version": (ctypes.c_int, []),
+    "pb_set_canonical_scatter_min": (ctypes.c_int, [_i64]),
     "pb_last_error": (ctypes.c_char_p, []),
     "pb_device_sm_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
     "pb_fused_move": (ctypes.c_int, [_p, _p, _p, _p, _p, _p, _p, _i64, _f64, _p]),
@@ -144,8 +147,6 @@ _SIGS = {
                                              _f64, _f64, _p, _p]),
     "pb_compute_efield": (ctypes.c_int, [_p, _p, _i64, _f64, ctypes.c_int, _p]),
     "pb_compute_efield_clear": (ctypes.c_int, [_p, _p, _i64, _f64, ctypes.c_int, _p, _p, _i64, _p]),
-    "pb_field_pipeline": (ctypes.c_int, [_p, _p, _p, _p, _i64, ctypes.c_int, _f64, _f64, ctypes.c_int,
-                                         _f64, _f64, _p, _p]),
     "pb_stream_sol": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int, _p]),
     "pb_init_species": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_uint64,
                                        _i64, _i64, _i64, _f64, _p]),

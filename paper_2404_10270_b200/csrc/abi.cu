@@ -17,13 +17,12 @@ void set_error(const char *fmt, ...) {
   va_end(ap);
 }
 
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char *v = getenv("PB_PDL");
-    return !(v && v[0] == '0');
-  }();
-  return on;
-}
+// Programmatic dependent launch for the per-step chain (measured, DESIGN.md
+// 3.1c); compile with -DPB_PDL=0 for the A/B without it.
+#ifndef PB_PDL
+#define PB_PDL 1
+#endif
+bool pdl_enabled() { return PB_PDL != 0; }
 
 int cuda_status(cudaError_t err, const char *what) {
   set_error("%s: %s (%s)", what, cudaGetErrorString(err), cudaGetErrorName(err));
@@ -219,19 +218,31 @@ extern "C" int pb_density_step(uint64_t *bins, uint64_t *bins_next, pb_status *s
 
 // ---------------------------------------------------------------------------
 // Speed-of-light probe for the roofline: streams exactly the mover's bytes
-// (reads x, vx[, vy, yp], cell; writes x[, vx], yp) with a trivial update and
-// no deposit, 4 particles per thread, 256-bit accesses, full occupancy.  It
-// measures what this read/write mix can reach on the part; the mover's
+// per species kind with a trivial update and no physics, 4 particles per
+// thread, 256-bit accesses, full occupancy --
+//   KICK   R x, vx, cell index   W x, vx
+//   BORIS  R x, vx, vy, vz, cell W x, vx, vy, vz
+//   DRIFT  R x, vx               W x
+//   + yp   R vy, yp              W yp
+// It measures what this read/write mix can reach on the part; the mover's
 // achieved bandwidth is reported against the copy peak, not against this.
 namespace pb {
-__global__ void __launch_bounds__(256) k_stream_sol(double *x, double *vx, const double *vy,
+__device__ __forceinline__ void sol_ld(const double *p, double &a, double &b, double &c, double &d) {
+  asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+__device__ __forceinline__ void sol_st(double *p, double a, double b, double c, double d) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
+__global__ void __launch_bounds__(256) k_stream_sol(double *x, double *vx, double *vy, double *vz,
                                                     double *yp, const int32_t *cell,
-                                                    const int8_t *cell8, int64_t n, int write_v) {
+                                                    const int8_t *cell8, int64_t n, int write_v,
+                                                    int boris) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i + 3 < n; i += stride) {
     double a0, a1, a2, a3, b0, b1, b2, b3;
-    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a0), "=d"(a1), "=d"(a2), "=d"(a3) : "l"(x + i));
-    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(b0), "=d"(b1), "=d"(b2), "=d"(b3) : "l"(vx + i));
+    sol_ld(x + i, a0, a1, a2, a3);
+    sol_ld(vx + i, b0, b1, b2, b3);
     int c0 = 0, c1 = 0, c2 = 0, c3 = 0;
     if (cell8) {  // the mover's compressed cell index: 4 bytes per lane
       const int p = __ldcs(reinterpret_cast<const int *>(cell8 + i));
@@ -241,14 +252,24 @@ __global__ void __launch_bounds__(256) k_stream_sol(double *x, double *vx, const
       c0 = c.x; c1 = c.y; c2 = c.z; c3 = c.w;
     }
     a0 += b0 + c0; a1 += b1 + c1; a2 += b2 + c2; a3 += b3 + c3;
-    asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(x + i), "d"(a0), "d"(a1), "d"(a2), "d"(a3) : "memory");
-    if (write_v)
-      asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(vx + i), "d"(b0), "d"(b1), "d"(b2), "d"(b3) : "memory");
+    sol_st(x + i, a0, a1, a2, a3);
+    if (write_v) sol_st(vx + i, b0, b1, b2, b3);
+    if (boris) {
+      double y0, y1, y2, y3, z0, z1, z2, z3;
+      sol_ld(vy + i, y0, y1, y2, y3);
+      sol_ld(vz + i, z0, z1, z2, z3);
+      sol_st(vy + i, y0 + z0, y1 + z1, y2 + z2, y3 + z3);
+      sol_st(vz + i, z0 + b0, z1 + b1, z2 + b2, z3 + b3);
+    }
     if (yp) {
       double y0, y1, y2, y3, w0, w1, w2, w3;
-      asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(y0), "=d"(y1), "=d"(y2), "=d"(y3) : "l"(yp + i));
-      asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(w0), "=d"(w1), "=d"(w2), "=d"(w3) : "l"(vy + i));
-      asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(yp + i), "d"(y0 + w0), "d"(y1 + w1), "d"(y2 + w2), "d"(y3 + w3) : "memory");
+      sol_ld(yp + i, y0, y1, y2, y3);
+      if (boris) {  // vy already read
+        w0 = w1 = w2 = w3 = 1.0;
+      } else {
+        sol_ld(vy + i, w0, w1, w2, w3);
+      }
+      sol_st(yp + i, y0 + w0, y1 + w1, y2 + w2, y3 + w3);
     }
   }
 }
@@ -262,9 +283,10 @@ extern "C" int pb_stream_sol(const pb_species *sp, int nsp, void *stream) {
     const pb_species &s = sp[k];
     if (s.kind == PB_KIND_INACTIVE || s.n < 4) continue;
     const bool charged = s.kind != PB_KIND_DRIFT;
+    const bool boris = s.kind == PB_KIND_BORIS;
     pb::k_stream_sol<<<sms * 8, 256, 0, (cudaStream_t)stream>>>(
-        s.x, s.vx, s.vy, s.yp, charged ? s.cell : nullptr, charged ? s.cell8 : nullptr,
-        s.n & ~(int64_t)3, charged ? 1 : 0);
+        s.x, s.vx, s.vy, s.vz, s.yp, charged ? s.cell : nullptr, charged ? s.cell8 : nullptr,
+        s.n & ~(int64_t)3, charged ? 1 : 0, boris ? 1 : 0);
   }
   PB_CHECK_LAUNCH("k_stream_sol");
   return PB_OK;

@@ -559,10 +559,11 @@ __global__ void k_add_counts(const int64_t *__restrict__ a, const int64_t *__res
     out[j] = a[j] + b[j];
 }
 
-static bool canon_scatter_enabled() {
-  static const bool on = !(getenv("PB_CANON_SCATTER") && atoi(getenv("PB_CANON_SCATTER")) == 0);
-  return on;
-}
+// Stores with at least this many particles take the scatter resort; smaller
+// ones keep the full key sort (the scatter path's host read of the mover
+// count costs more than sorting ~1M keys).  pb_set_canonical_scatter_min
+// moves it (tests exercise both paths; INT64_MAX = key sort only).
+static int64_t g_scatter_min = (int64_t)1 << 20;
 
 static size_t scan_u32_bytes(int64_t n) {
   size_t t = 0;
@@ -735,12 +736,7 @@ extern "C" int pb_canonical_resort(const pb_species *src, const pb_species *dst,
     g.dst[nf++] = dst->yp;
   }
   g.nf = nf;
-  // (small stores keep the full key sort: the scatter path's host read of
-  // the mover count costs more than sorting ~1M keys; PB_CANON_SCATTER_MIN
-  // moves the threshold, read per call so tests can exercise both paths)
-  const char *smin = getenv("PB_CANON_SCATTER_MIN");
-  const int64_t scatter_min = smin ? atoll(smin) : (int64_t)1 << 20;
-  if (!(pb::canon_scatter_enabled() && n_tot >= scatter_min)) {
+  if (n_tot < pb::g_scatter_min) {
     rc = pb::launch_canon_push(src, cv, e_nodes, nc, particle_bc, species_id, status, 0, rank_bits,
                                offp, keys, vals, st);
     if (rc) return rc;
@@ -970,5 +966,14 @@ extern "C" int pb_rho_from_partials(const double *raw, const double *coef, int n
   pb::k_rho_raw<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(raw, ca, ndep, nc, field_bc,
                                                                      left, right, rho);
   PB_CHECK_LAUNCH("k_rho_raw");
+  return PB_OK;
+}
+
+extern "C" int pb_set_canonical_scatter_min(int64_t n) {
+  if (n < 0) {
+    pb::set_error("pb_set_canonical_scatter_min: n=%lld < 0", (long long)n);
+    return PB_ERR_INVALID;
+  }
+  pb::g_scatter_min = n;
   return PB_OK;
 }

@@ -83,7 +83,7 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-bool pdl_enabled();  // PB_PDL (default 1)
+bool pdl_enabled();  // compile-time PB_PDL (default 1)
 
 // Launch `kern` with programmatic stream serialisation (when enabled); the
 // kernel must call pdl_enter() before its first global memory access.

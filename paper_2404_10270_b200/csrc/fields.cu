@@ -7,8 +7,6 @@
 // reference's direct elimination (fields.py:138-202), restated operation for
 // operation -- including NumPy's pairwise summation inside np.mean -- on one
 // thread, so a given rho yields a bitwise-identical phi.
-#include <cooperative_groups.h>
-
 #include "common.cuh"
 
 namespace pb {
@@ -255,8 +253,7 @@ __device__ __forceinline__ double mb_rhs(const PoissonArgs &a, int64_t k, double
   return r;
 }
 
-// ---- scan phases, one tile each (shared by the per-phase kernels and the
-// cooperative fused pipeline, so both give bitwise the same phi) ----------
+// ---- scan phases, one tile each ----------------------------------------------
 // tile partial sums of src[0, len) -> part[tile]
 __device__ void mb_tile_sum(const double *__restrict__ src, int64_t len, DD *part, int64_t tile,
                             DD *sm) {
@@ -375,57 +372,6 @@ __global__ void k_mb_wrap(double *phi, int64_t nc) {
   phi[nc] = phi[0];
 }
 
-// ---- cooperative fused field pipeline ----------------------------------------
-// smoothing passes -> scan Poisson -> E in ONE launch, grid-wide syncs between
-// the phases (same tile functions as the per-phase kernels: bitwise the same
-// rho_s / phi / E).  Replaces 5-9 tiny launches per field-solve step.
-struct CoopArgs {
-  PoissonArgs pa;
-  const double *rho;
-  double *out;  // smoothed density (passes > 0)
-  double *tmp;  // smoothing ping-pong
-  int passes;
-  double *e;
-  double two_dx;
-};
-
-__global__ void __launch_bounds__(kMbThreads) k_field_coop(const CoopArgs c) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  __shared__ DD sm[kMbThreads];
-  const int64_t nc = c.pa.nc;
-  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
-  const double *src = c.rho;
-  for (int p = 0; p < c.passes; ++p) {
-    double *dst = ((c.passes - 1 - p) % 2 == 0) ? c.out : c.tmp;
-    for (int64_t j = gtid; j <= nc; j += gsz) smooth_node(src, dst, nc, j);
-    grid.sync();
-    src = dst;
-  }
-  PoissonArgs a = c.pa;
-  a.rho = src;
-  const bool periodic = a.field_bc == PB_FIELD_PERIODIC;
-  if (periodic) {
-    for (int64_t t = blockIdx.x; t < a.ntc; t += gridDim.x) mb_tile_sum(src, nc, a.p0, t, sm);
-    grid.sync();
-  }
-  for (int64_t t = blockIdx.x; t < a.nt; t += gridDim.x) mb_fwd_part(a, t, sm);
-  grid.sync();
-  for (int64_t t = blockIdx.x; t < a.nt; t += gridDim.x) mb_fwd_scan(a, t, sm);
-  grid.sync();
-  for (int64_t t = blockIdx.x; t < a.nt; t += gridDim.x) mb_bwd_scan(a, t, sm);
-  grid.sync();
-  if (periodic) {
-    for (int64_t t = blockIdx.x; t < a.ntc; t += gridDim.x) mb_tile_sum(a.phi, nc, a.p3, t, sm);
-    grid.sync();
-    mb_shift(a, gtid, gsz, sm);
-    grid.sync();
-    if (gtid == 0) a.phi[nc] = a.phi[0];
-    grid.sync();
-  }
-  for (int64_t j = gtid; j <= nc; j += gsz) efield_node(a.phi, c.e, nc, c.two_dx, a.field_bc, j);
-}
 
 // E from phi, then zero bin sets whose density has been taken (the serial
 // field-solve cycle reads the bins with the one-kernel epilogue, which does
@@ -574,73 +520,6 @@ extern "C" int pb_compute_efield(const double *phi, double *e, int64_t nc,
                                    (cudaStream_t)stream, phi, e, nc, 2.0 * dx, field_bc);
   if (err != cudaSuccess) return pb::cuda_status(err, "k_efield");
   return PB_OK;
-}
-
-// smoothing + scan Poisson + E in one cooperative launch (falls back to the
-// per-phase kernels when the grid cannot be co-resident).  rho_s receives the
-// smoothed density when passes > 0.  Same results as pb_smooth_density +
-// pb_solve_poisson_scan + pb_compute_efield, bit for bit.
-extern "C" int pb_field_pipeline(const double *rho, double *rho_s, double *phi, double *e,
-                                 int64_t nc, int passes, double dx, double eps0, int field_bc,
-                                 double phi_left, double phi_right, void *scratch, void *stream) {
-  if (nc < 3 || passes < 0 || !rho || !phi || !e || !scratch || (passes > 0 && !rho_s) ||
-      (field_bc != PB_FIELD_PERIODIC && field_bc != PB_FIELD_DIRICHLET)) {
-    pb::set_error("pb_field_pipeline: bad arguments (nc=%lld)", (long long)nc);
-    return PB_ERR_INVALID;
-  }
-  cudaStream_t st = (cudaStream_t)stream;
-  pb::CoopArgs c;
-  c.pa = pb::poisson_args(rho, phi, nc, dx, eps0, field_bc, phi_left, phi_right, scratch);
-  // smoothing ping-pong lives after the scan's scratch (y, then 4 partial sets)
-  const char *parts_end = (const char *)(c.pa.p3 + (c.pa.ntc + 1));
-  const size_t used = (size_t)(parts_end - (const char *)scratch);
-  double *tmp = (double *)((char *)scratch + ((used + 255) & ~(size_t)255));
-  c.rho = rho;
-  c.out = rho_s;
-  c.tmp = tmp;
-  c.passes = passes;
-  c.e = e;
-  c.two_dx = 2.0 * dx;
-  static int max_blocks = -1;
-  if (max_blocks < 0) {
-    int dev = 0, sms = 0, bps = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pb::k_field_coop, pb::kMbThreads, 0);
-    max_blocks = sms * bps;
-  }
-  // at least one block per SM for the node-parallel stencil phases; idle
-  // blocks just pass the scan phases' grid syncs
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  int grid = c.pa.ntc > c.pa.nt ? c.pa.ntc : c.pa.nt;
-  const int64_t node_blocks = (nc + 1 + pb::kMbThreads - 1) / pb::kMbThreads;
-  const int want = (int)(node_blocks < sms ? node_blocks : sms);
-  if (grid < want) grid = want;
-  if (grid > max_blocks) grid = max_blocks > 0 ? max_blocks : 1;
-  if (grid < 1) grid = 1;
-  const int tiles = c.pa.ntc > c.pa.nt ? c.pa.ntc : c.pa.nt;
-  if (tiles <= max_blocks) {
-    void *args[] = {&c};
-    const cudaError_t err = cudaLaunchCooperativeKernel((const void *)pb::k_field_coop, grid,
-                                                        pb::kMbThreads, args, 0, st);
-    if (err != cudaSuccess) return pb::cuda_status(err, "cudaLaunchCooperativeKernel");
-    return PB_OK;
-  }
-  int rc = PB_OK;
-  const double *src = rho;
-  if (passes > 0) {
-    rc = pb_smooth_density(rho, rho_s, nc, passes, tmp, stream);
-    if (rc) return rc;
-    src = rho_s;
-  }
-  rc = pb_solve_poisson_scan(src, phi, nc, dx, eps0, field_bc, phi_left, phi_right, scratch, stream);
-  if (rc) return rc;
-  return pb_compute_efield(phi, e, nc, dx, field_bc, stream);
 }
 
 extern "C" int pb_compute_efield_clear(const double *phi, double *e, int64_t nc, double dx,

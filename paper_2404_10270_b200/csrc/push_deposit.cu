@@ -47,8 +47,8 @@ struct LaunchArgs {
   int id[PB_MAX_SPECIES];  // caller species index (status arrays)
   int nsp;
   int push;  // 0: deposit only (no mover)
-  int order[PB_MAX_SPECIES];             // TMA kernel: species order of the tile list
-  int64_t tile_start[PB_MAX_SPECIES + 1];  // TMA kernel: prefix of full tiles
+  int order[PB_MAX_SPECIES];             // chunk list over all species (quad/ring kernels)
+  int64_t tile_start[PB_MAX_SPECIES + 1];
   // quad kernel chunk interleave: the first rr_chunks chunks go round-robin
   // over the species (rr_each per species), the rest species by species
   int64_t rr_chunks, rr_each;
@@ -404,19 +404,9 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------------------
-// TMA kernel (the production mover).  Persistent: one or two blocks per SM.
-// A producer warp pulls tiles (1024 particles of one species) from a global
-// work counter -- a single list over all species, heaviest species first --
-// and streams each tile's arrays into a kStages-deep shared-memory ring with
-// 1-D bulk copies (cp.async.bulk, mbarrier complete_tx).  Eight consumer
-// warps compute from shared memory, store results straight to HBM and
-// deposit through warp-aggregated global atomics.  Dynamic tiles keep every
-// SM busy to the end regardless of the per-species cost mix, and the bytes in
-// flight are set by the ring depth instead of by registers.
+// Bulk-copy (TMA) + mbarrier helpers of the per-warp rings (k_push_ring,
+// k_push_split).
 // ---------------------------------------------------------------------------
-constexpr int kMaxStages = 8;
-constexpr int kMaxAhead = 8;
-constexpr int kConsumerWarps = kThreads / 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -457,76 +447,35 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
 // A claimer's last claim has returned (it is what ended its loop) before its
 // done-increment is issued, so the reset is ordered after every claim without
 // a fence (a __threadfence here costs a full L1 invalidate per exiting warp).
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// In-kernel launch clock (pb_status.mover_t0/mover_ns/mover_launches): one
+// RED.MIN per block at its start...
+__device__ __forceinline__ void mover_clock_start(pb_status *st) {
+  if (threadIdx.x == 0) atomicMin((unsigned long long *)&st->mover_t0, global_ns());
+}
+
 __device__ __forceinline__ void release_work_counter(pb_status *st, unsigned long long claimers) {
 #ifdef PB_RELEASE_FENCE
   __threadfence();
 #endif
   const unsigned long long d = atomicAdd((unsigned long long *)&st->tile_done, 1ull);
   if (d == claimers - 1) {
+    // ...and the last claimer to finish closes the launch's interval
+    const unsigned long long t1 = global_ns();
+    const unsigned long long t0 = atomicExch((unsigned long long *)&st->mover_t0, ~0ull);
+    if (t0 != ~0ull && t1 > t0) {
+      atomicAdd((unsigned long long *)&st->mover_ns, t1 - t0);
+      atomicAdd((unsigned long long *)&st->mover_launches, 1ull);
+    }
     atomicExch((unsigned long long *)&st->tile_next, 0ull);
     atomicExch((unsigned long long *)&st->tile_next2, 0ull);
     atomicExch((unsigned long long *)&st->tile_done, 0ull);
   }
-}
-
-// Particles per TMA tile, per species kind: sized so every kind fills a
-// ~32 KB ring slot (a multiple of 2*kThreads for the pair loop).
-__host__ __device__ constexpr int tile_of(int kind, bool yp) {
-  return kind == PB_KIND_KICK ? 1024
-       : kind == PB_KIND_BORIS ? 1024
-       : kind == PB_KIND_DRIFT ? (yp ? 1024 : 2048)
-       : 1024;
-}
-
-template <int KIND, bool YP>
-struct Stage {
-  using F = Fields<KIND, YP>;
-  static constexpr int T = tile_of(KIND, YP);
-  static constexpr bool kCell = KIND != PB_KIND_DRIFT;
-  static constexpr int kX = 0;
-  static constexpr int kVX = kX + T * 8;
-  static constexpr int kVY = kVX + T * 8;
-  static constexpr int kVZ = kVY + (F::kVy ? T * 8 : 0);
-  static constexpr int kYP = kVZ + (F::kVz ? T * 8 : 0);
-  static constexpr int kCELL = kYP + (YP ? T * 8 : 0);
-  static constexpr int kBytes = kCELL + (kCell ? T * 4 : 0);
-};
-
-__host__ __device__ constexpr int stage_bytes(int kind, bool yp) {
-  return kind == PB_KIND_KICK ? (yp ? Stage<PB_KIND_KICK, true>::kBytes : Stage<PB_KIND_KICK, false>::kBytes)
-       : kind == PB_KIND_BORIS ? (yp ? Stage<PB_KIND_BORIS, true>::kBytes : Stage<PB_KIND_BORIS, false>::kBytes)
-       : kind == PB_KIND_DRIFT ? (yp ? Stage<PB_KIND_DRIFT, true>::kBytes : Stage<PB_KIND_DRIFT, false>::kBytes)
-       : 0;
-}
-
-__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-
-template <int KIND, bool YP>
-__device__ __forceinline__ void prefetch_tile(const pb_species &s, int64_t base) {
-  using L = Stage<KIND, YP>;
-  using F = Fields<KIND, YP>;
-  prefetch_l2(s.x + base, L::T * 8);
-  prefetch_l2(s.vx + base, L::T * 8);
-  if (F::kVy) prefetch_l2(s.vy + base, L::T * 8);
-  if (F::kVz) prefetch_l2(s.vz + base, L::T * 8);
-  if (YP) prefetch_l2(s.yp + base, L::T * 8);
-  if (L::kCell) prefetch_l2(s.cell + base, L::T * 4);
-}
-
-template <int KIND, bool YP>
-__device__ __forceinline__ void produce_tile(const pb_species &s, int64_t base, unsigned char *buf,
-                                             uint64_t *bar) {
-  using L = Stage<KIND, YP>;
-  using F = Fields<KIND, YP>;
-  mbar_expect_tx(bar, (uint32_t)L::kBytes);
-  tma_load_1d(buf + L::kX, s.x + base, L::T * 8, bar);
-  tma_load_1d(buf + L::kVX, s.vx + base, L::T * 8, bar);
-  if (F::kVy) tma_load_1d(buf + L::kVY, s.vy + base, L::T * 8, bar);
-  if (F::kVz) tma_load_1d(buf + L::kVZ, s.vz + base, L::T * 8, bar);
-  if (YP) tma_load_1d(buf + L::kYP, s.yp + base, L::T * 8, bar);
-  if (L::kCell) tma_load_1d(buf + L::kCELL, s.cell + base, L::T * 4, bar);
 }
 
 // Thread-local run of equal cells, flushed to the window when the cell changes.
@@ -554,369 +503,6 @@ __device__ __forceinline__ void st4(double *p, double a, double b, double c, dou
                : "memory");
 }
 
-// Consumer side of one TMA tile: every thread owns quads of 4 consecutive
-// particles (256-bit stores, thread-local deposit runs), one warp segmented
-// scan per tile for the runs that continue into the next lane.
-template <int KIND, bool YP, int BC, bool DEP>
-__device__ __forceinline__ void consume_tile_quads(const LaunchArgs &a, int isp, int64_t base,
-                                             const unsigned char *buf, const Window &win,
-                                             Tally &t) {
-  using L = Stage<KIND, YP>;
-  using F = Fields<KIND, YP>;
-  const pb_species &s = a.sp[isp];
-  const int sid = a.id[isp];
-  const unsigned full = 0xffffffffu;
-  const int64_t nc = a.nc;
-  RunAcc run;
-#pragma unroll 1
-  for (int qd = 0; qd < L::T / (4 * kThreads); ++qd) {
-    const int li = qd * (4 * kThreads) + 4 * threadIdx.x;
-    const int64_t i = base + li;
-    double x[4], vx[4], vy[4] = {0, 0, 0, 0}, vz[4] = {0, 0, 0, 0}, y[4] = {0, 0, 0, 0};
-    int32_t c[4] = {-1, -1, -1, -1};
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const double2 xx = *reinterpret_cast<const double2 *>(buf + L::kX + (li + 2 * h) * 8);
-      x[2 * h] = xx.x;
-      x[2 * h + 1] = xx.y;
-      const double2 vv = *reinterpret_cast<const double2 *>(buf + L::kVX + (li + 2 * h) * 8);
-      vx[2 * h] = vv.x;
-      vx[2 * h + 1] = vv.y;
-      if (F::kVy) {
-        const double2 v = *reinterpret_cast<const double2 *>(buf + L::kVY + (li + 2 * h) * 8);
-        vy[2 * h] = v.x;
-        vy[2 * h + 1] = v.y;
-      }
-      if (F::kVz) {
-        const double2 v = *reinterpret_cast<const double2 *>(buf + L::kVZ + (li + 2 * h) * 8);
-        vz[2 * h] = v.x;
-        vz[2 * h + 1] = v.y;
-      }
-      if (YP) {
-        const double2 v = *reinterpret_cast<const double2 *>(buf + L::kYP + (li + 2 * h) * 8);
-        y[2 * h] = v.x;
-        y[2 * h + 1] = v.y;
-      }
-    }
-    if (L::kCell) {
-      const int4 cc = *reinterpret_cast<const int4 *>(buf + L::kCELL + li * 4);
-      c[0] = cc.x;
-      c[1] = cc.y;
-      c[2] = cc.z;
-      c[3] = cc.w;
-    }
-    int32_t nn[4];
-    int8_t wall[4];
-    bool mv[4], cfl[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      kick_drift<KIND>(x[k], vx[k], vy[k], vz[k], c[k], s, a.e);
-      if (YP) y[k] = __dadd_rn(y[k], __dmul_rn(s.fnstep, vy[k]));
-      if (!L::kCell && floor(x[k]) != 0.0) c[k] = s.cell[i + k];
-      const MoveOut o = transfer<BC>(x[k], c[k], nc);
-      nn[k] = o.cell;
-      mv[k] = o.moved;
-      wall[k] = o.wall;
-      cfl[k] = o.cfl;
-    }
-    st4(s.x + i, x[0], x[1], x[2], x[3]);
-    if (KIND != PB_KIND_DRIFT) st4(s.vx + i, vx[0], vx[1], vx[2], vx[3]);
-    if (KIND == PB_KIND_BORIS) {
-      st4(s.vy + i, vy[0], vy[1], vy[2], vy[3]);
-      st4(s.vz + i, vz[0], vz[1], vz[2], vz[3]);
-    }
-    if (YP) st4(s.yp + i, y[0], y[1], y[2], y[3]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (mv[k]) {
-        s.cell[i + k] = nn[k];
-        if (s.cell8) s.cell8[i + k] = (int8_t)PB_CELL8_ESCAPE;
-      }
-      t.moved += (int)mv[k];
-      if (cfl[k]) {
-        const uint64_t key = ((uint64_t)sid << 56) | (uint64_t)(i + k);
-        atomicMin((unsigned long long *)&a.st->cfl_index, (unsigned long long)key);
-        atomicCAS(&a.st->code, PB_OK, PB_ERR_CFL);
-        nn[k] = -1;
-      }
-    }
-    if (BC == PB_BC_ABSORBING) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        t.absorbed[0] += (int)(wall[k] == 0);
-        t.absorbed[1] += (int)(wall[k] == 1);
-        const bool r = wall[k] >= 0;
-        const unsigned b = __ballot_sync(full, r);
-        if (b) {
-          const unsigned lane = lane_id();
-          unsigned long long hb = 0;
-          if (lane == 0)
-            hb = atomicAdd((unsigned long long *)&a.st->n_holes[sid], (unsigned long long)__popc(b));
-          hb = __shfl_sync(full, hb, 0);
-          if (r) s.holes[hb + __popc(b & ((1u << lane) - 1u))] = i + k;
-        }
-      }
-    }
-    if (DEP) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) run.add(nn[k], x[k], win);
-    }
-  }
-  if (DEP) warp_segmented_emit(run.key, run.w, win);
-}
-
-template <int KIND, bool YP, int BC, bool DEP>
-__device__ __forceinline__ void consume_tile_pairs(const LaunchArgs &a, int isp, int64_t base,
-                                             const unsigned char *buf, const Window &win,
-                                             Tally &t) {
-  using L = Stage<KIND, YP>;
-  using F = Fields<KIND, YP>;
-  const pb_species &s = a.sp[isp];
-  const int sid = a.id[isp];
-#pragma unroll
-  for (int p = 0; p < L::T / (2 * kThreads); ++p) {
-    const int li = p * (2 * kThreads) + 2 * threadIdx.x;
-    Pair q;
-    const double2 xx = *reinterpret_cast<const double2 *>(buf + L::kX + li * 8);
-    q.x0 = xx.x;
-    q.x1 = xx.y;
-    const double2 vv = *reinterpret_cast<const double2 *>(buf + L::kVX + li * 8);
-    q.vx0 = vv.x;
-    q.vx1 = vv.y;
-    if (F::kVy) {
-      const double2 v = *reinterpret_cast<const double2 *>(buf + L::kVY + li * 8);
-      q.vy0 = v.x;
-      q.vy1 = v.y;
-    }
-    if (F::kVz) {
-      const double2 v = *reinterpret_cast<const double2 *>(buf + L::kVZ + li * 8);
-      q.vz0 = v.x;
-      q.vz1 = v.y;
-    }
-    if (YP) {
-      const double2 v = *reinterpret_cast<const double2 *>(buf + L::kYP + li * 8);
-      q.y0 = v.x;
-      q.y1 = v.y;
-    }
-    if (L::kCell) {
-      const int2 c = *reinterpret_cast<const int2 *>(buf + L::kCELL + li * 4);
-      q.c0 = c.x;
-      q.c1 = c.y;
-    }
-    handle_pair<KIND, YP, BC, true, DEP>(a, s, sid, base + li, true, true, q, win, t);
-  }
-}
-
-#ifndef PB_QUADS
-#define PB_QUADS 0
-#endif
-
-template <int KIND, bool YP, int BC, bool DEP>
-__device__ __forceinline__ void consume_tile(const LaunchArgs &a, int isp, int64_t base,
-                                             const unsigned char *buf, const Window &win,
-                                             Tally &t) {
-  if (PB_QUADS)
-    consume_tile_quads<KIND, YP, BC, DEP>(a, isp, base, buf, win, t);
-  else
-    consume_tile_pairs<KIND, YP, BC, DEP>(a, isp, base, buf, win, t);
-}
-
-// Per-species kind dispatch for the TMA consumer / producer.
-template <int BC>
-__device__ __forceinline__ void consume_any(const LaunchArgs &a, int isp, int64_t base,
-                                            const unsigned char *buf, const Window &win,
-                                            Tally &t) {
-  const pb_species &s = a.sp[isp];
-  const bool yp = s.yp != nullptr;
-  const bool dep = s.deposit >= 0 && a.bins != nullptr;
-#define PB_C(K, Y)                                                       \
-  do {                                                                   \
-    if (dep) consume_tile<K, Y, BC, true>(a, isp, base, buf, win, t);    \
-    else consume_tile<K, Y, BC, false>(a, isp, base, buf, win, t);       \
-  } while (0)
-  switch (s.kind) {
-    case PB_KIND_KICK:
-      if (yp) PB_C(PB_KIND_KICK, true); else PB_C(PB_KIND_KICK, false);
-      break;
-    case PB_KIND_BORIS:
-      if (yp) PB_C(PB_KIND_BORIS, true); else PB_C(PB_KIND_BORIS, false);
-      break;
-    default:
-      if (yp) PB_C(PB_KIND_DRIFT, true); else PB_C(PB_KIND_DRIFT, false);
-      break;
-  }
-#undef PB_C
-}
-
-__device__ __forceinline__ void produce_any(const pb_species &s, int64_t base, unsigned char *buf,
-                                            uint64_t *bar) {
-  const bool yp = s.yp != nullptr;
-  switch (s.kind) {
-    case PB_KIND_KICK:
-      if (yp) produce_tile<PB_KIND_KICK, true>(s, base, buf, bar);
-      else produce_tile<PB_KIND_KICK, false>(s, base, buf, bar);
-      break;
-    case PB_KIND_BORIS:
-      if (yp) produce_tile<PB_KIND_BORIS, true>(s, base, buf, bar);
-      else produce_tile<PB_KIND_BORIS, false>(s, base, buf, bar);
-      break;
-    default:
-      if (yp) produce_tile<PB_KIND_DRIFT, true>(s, base, buf, bar);
-      else produce_tile<PB_KIND_DRIFT, false>(s, base, buf, bar);
-      break;
-  }
-}
-
-__device__ __forceinline__ void prefetch_any(const pb_species &s, int64_t base) {
-  const bool yp = s.yp != nullptr;
-  switch (s.kind) {
-    case PB_KIND_KICK:
-      if (yp) prefetch_tile<PB_KIND_KICK, true>(s, base);
-      else prefetch_tile<PB_KIND_KICK, false>(s, base);
-      break;
-    case PB_KIND_BORIS:
-      if (yp) prefetch_tile<PB_KIND_BORIS, true>(s, base);
-      else prefetch_tile<PB_KIND_BORIS, false>(s, base);
-      break;
-    default:
-      if (yp) prefetch_tile<PB_KIND_DRIFT, true>(s, base);
-      else prefetch_tile<PB_KIND_DRIFT, false>(s, base);
-      break;
-  }
-}
-
-__device__ __forceinline__ int tile_species(const LaunchArgs &a, int64_t tile) {
-  int k = 0;
-  while (k + 1 < a.nsp && tile >= a.tile_start[k + 1]) ++k;
-  return a.order[k];
-}
-
-// First particle of a tile of species isp.
-__device__ __forceinline__ int64_t tile_base(const LaunchArgs &a, int isp, int64_t tile) {
-  int kk = 0;
-  while (a.order[kk] != isp) ++kk;
-  return (tile - a.tile_start[kk]) * tile_of(a.sp[isp].kind, a.sp[isp].yp != nullptr);
-}
-
-#ifndef PB_MINBLOCKS
-#define PB_MINBLOCKS 3
-#endif
-
-template <int BC>
-__global__ void __launch_bounds__(kThreads + 32, PB_MINBLOCKS)
-    k_push_tma(const __grid_constant__ LaunchArgs a, int stage_stride, int kStages, int ahead) {
-  extern __shared__ __align__(128) unsigned char ring[];
-  __shared__ __align__(8) uint64_t bars[2 * kMaxStages];
-  __shared__ int64_t hdr[kMaxStages];
-  uint64_t *full = bars;
-  uint64_t *empty = bars + kMaxStages;
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < kStages; ++k) {
-      mbar_init(&full[k], 1);
-      mbar_init(&empty[k], kConsumerWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const int64_t total = a.tile_start[a.nsp];
-  const int warp = threadIdx.x >> 5;
-
-  if (warp == kConsumerWarps) {  // producer warp
-    if (lane_id() == 0) {
-      // Claimed-tile queue: tiles are claimed `ahead` steps before their
-      // shared-memory load and prefetched into L2 at claim time, so DRAM
-      // requests stay in flight beyond the depth of the smem ring.
-      int64_t q[kMaxAhead + 1];
-      const int depth = ahead + 1;
-      for (int j = 0; j < depth; ++j) {
-        q[j] = (int64_t)atomicAdd((unsigned long long *)&a.st->tile_next, 1ull);
-        if (j > 0 && q[j] < total) {
-          const int isp = tile_species(a, q[j]);
-          prefetch_any(a.sp[isp], tile_base(a, isp, q[j]));
-        }
-      }
-      for (int64_t k = 0;; ++k) {
-        const int st = (int)(k % kStages);
-        const int qi = (int)(k % depth);
-        const int64_t tile = q[qi];
-        if (k >= kStages) mbar_wait(&empty[st], (uint32_t)(((k / kStages) - 1) & 1));
-        if (tile >= total) {
-          hdr[st] = -1;
-          mbar_arrive(&full[st]);  // no bytes: completes the phase
-          break;
-        }
-        hdr[st] = tile;
-        const int isp = tile_species(a, tile);
-        produce_any(a.sp[isp], tile_base(a, isp, tile), ring + (size_t)st * stage_stride, &full[st]);
-        const int64_t nt = (int64_t)atomicAdd((unsigned long long *)&a.st->tile_next, 1ull);
-        q[qi] = nt;
-        if (depth > 1 && nt < total) {
-          const int jsp = tile_species(a, nt);
-          prefetch_any(a.sp[jsp], tile_base(a, jsp, nt));
-        }
-      }
-      release_work_counter(a.st, gridDim.x);
-    }
-  } else {  // consumer warps
-    Window win{nullptr, nullptr, 0, 0, nullptr, nullptr};
-    Tally t[PB_MAX_SPECIES > 4 ? 1 : 1];
-    int cur = -1;
-    for (int64_t k = 0;; ++k) {
-      const int st = (int)(k % kStages);
-      mbar_wait(&full[st], (uint32_t)((k / kStages) & 1));
-      const int64_t tile = hdr[st];
-      if (tile < 0) break;
-      const int isp = tile_species(a, tile);
-      int kk = 0;
-      while (a.order[kk] != isp) ++kk;
-      const int64_t base = (tile - a.tile_start[kk]) * tile_of(a.sp[isp].kind, a.sp[isp].yp != nullptr);
-      if (isp != cur) {
-        if (cur >= 0) flush_tally(a, a.id[cur], t[0], nullptr);
-        t[0] = Tally();
-        cur = isp;
-        const pb_species &s = a.sp[isp];
-        if (s.deposit >= 0 && a.bins) {
-          win.gR = a.bins + (size_t)s.deposit * 2 * (size_t)a.nc;
-          win.gC = win.gR + a.nc;
-        }
-      }
-      consume_any<BC>(a, isp, base, ring + (size_t)st * stage_stride, win, t[0]);
-      __syncwarp();
-      if (lane_id() == 0) mbar_arrive(&empty[st]);
-    }
-    if (cur >= 0) flush_tally(a, a.id[cur], t[0], nullptr);
-    // Partial last tiles (n % T particles) through the LDG path; block b
-    // takes species b.
-    if ((int)blockIdx.x < a.nsp) {
-      const int isp = (int)blockIdx.x;
-      const pb_species &s = a.sp[isp];
-      const int64_t n = s.n_dev ? *s.n_dev : s.n;
-      const int64_t T = tile_of(s.kind, s.yp != nullptr);
-      const int64_t beg = (n / T) * T;
-      if (beg < n) {
-        Window w2{nullptr, nullptr, 0, 0, nullptr, nullptr};
-        const bool dep = s.deposit >= 0 && a.bins != nullptr;
-        if (dep) {
-          w2.gR = a.bins + (size_t)s.deposit * 2 * (size_t)a.nc;
-          w2.gC = w2.gR + a.nc;
-        }
-        Tally tt;
-        run_any<BC, true>(a, isp, beg, n, w2, tt, dep);
-        flush_tally(a, a.id[isp], tt, nullptr);
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Quad kernel: warp-granular dynamic chunks, 256-bit LDG/STG, 4 consecutive
-// particles per thread.  Each warp pulls 2048-particle chunks (one species)
-// from a global counter -- heaviest species first -- and streams them with
-// 32-byte loads/stores per lane (LDG.E.256 / STG.E.256, 1 KB per warp
-// instruction).  No block-level synchronisation at all: every warp runs
-// independently, so latency hiding comes from occupancy (lean registers).
-// Deposit: thread-local run of the quad, then one warp segmented scan per
-// 128 particles, global u64 atomics from the segment tails.
 // ---------------------------------------------------------------------------
 #ifndef PB_CHUNK
 #define PB_CHUNK 2048
@@ -1188,6 +774,7 @@ template <int BC, bool BORIS>
 __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
     k_push_quad(const __grid_constant__ LaunchArgs a) {
   pdl_enter();
+  mover_clock_start(a.st);
   const int64_t total = a.tile_start[a.nsp];
   Window win{nullptr, nullptr, 0, 0, nullptr, nullptr};
   Tally t;
@@ -1250,6 +837,7 @@ template <int BC>
 __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
     k_push_ring(const __grid_constant__ LaunchArgs a) {
   pdl_enter();
+  mover_clock_start(a.st);
   extern __shared__ __align__(128) unsigned char r_smem[];
   const int lane = (int)lane_id();
   const int w = threadIdx.x >> 5;
@@ -1413,6 +1001,7 @@ template <int BC>
 __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
     k_push_split(const __grid_constant__ LaunchArgs a) {
   pdl_enter();
+  mover_clock_start(a.st);
   extern __shared__ __align__(128) unsigned char s_smem[];
   const int lane = (int)lane_id();
   const int w = threadIdx.x >> 5;
@@ -1524,21 +1113,35 @@ __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
 
 // ---------------------------------------------------------------------------
 // Host side.
+//
+// Kernel choice (measured on configs 2-5):
+//   every species pushed, mixed charged + other kinds  -> k_push_split
+//   every species pushed, all KICK without yp (config 3) -> k_push_ring
+//   every species pushed, otherwise (Boris, config 4)    -> k_push_quad
+//   deposit-only launches, or inactive depositing species -> k_push_deposit
+// Compile-time A/B switches (scripts/variants.txt builds them with EXTRA=-D...):
+//   PB_SPLIT (1), PB_RING (1), PB_SPLIT_SOLO (0), PB_INTERLEAVE (1),
+//   PB_CLAIM_CHUNK (0 = by launch size).
 // ---------------------------------------------------------------------------
-static int g_sm_count = 0;
-static int g_use_tma = -1;  // 0 ldg, 1 tma, 2 quad
+#ifndef PB_SPLIT
+#define PB_SPLIT 1
+#endif
+#ifndef PB_RING
+#define PB_RING 1
+#endif
+#ifndef PB_SPLIT_SOLO
+#define PB_SPLIT_SOLO 0
+#endif
+#ifndef PB_INTERLEAVE
+#define PB_INTERLEAVE 1
+#endif
+#ifndef PB_CLAIM_CHUNK
+#define PB_CLAIM_CHUNK 0
+#endif
 
-typedef void (*LdgFn)(LaunchArgs);
-static int g_interleave = -1;
+static int g_sm_count = 0;
+typedef void (*KernFn)(LaunchArgs);
 static const char *g_last_kernel = "";
-static const bool g_ring = !(getenv("PB_RING") && atoi(getenv("PB_RING")) == 0);
-static const bool g_split = !(getenv("PB_SPLIT") && atoi(getenv("PB_SPLIT")) == 0);
-// PB_SPLIT_SOLO=1: the split kernel also for charged-only launches (its
-// register warps then steal charged chunks); default: k_push_ring there.
-static const bool g_split_solo = getenv("PB_SPLIT_SOLO") && atoi(getenv("PB_SPLIT_SOLO")) != 0;
-typedef void (*TmaFn)(LaunchArgs, int, int, int);
-static int g_stages = 0;
-static int g_ahead = -1;
 
 static int sm_count() {
   if (g_sm_count == 0) {
@@ -1569,7 +1172,7 @@ static int occupancy(const void *fn, int threads, int smem, int *bps) {
   return PB_OK;
 }
 
-// Approximate HBM bytes per particle, used to balance blocks and order tiles.
+// Approximate HBM bytes per particle, used to balance blocks and order chunks.
 static double bytes_per_particle(const pb_species &s, bool push) {
   if (!push) return 12.0;
   const bool yp = s.yp != nullptr;
@@ -1579,6 +1182,38 @@ static double bytes_per_particle(const pb_species &s, bool push) {
     case PB_KIND_DRIFT: return 24.0 + (yp ? 24.0 : 0.0) + (s.deposit >= 0 ? 4.0 : 0.0);
     default: return s.deposit >= 0 ? 12.0 : 0.0;
   }
+}
+
+// Chunk list over the species slots gs[0..n) (heaviest bytes first): the
+// first rr_each chunks of every species round-robin (charged chunks are
+// latency-heavier than neutral ones; a mix keeps the memory system busy),
+// then species by species.
+static void build_list(const LaunchArgs &a, const int *gs, int n, ChunkList &L) {
+  L.nsp = n;
+  L.tile_start[0] = 0;
+  int64_t mn = -1;
+  for (int k = 0; k < n; ++k) {
+    L.order[k] = gs[k];
+    const int64_t nk = (a.sp[gs[k]].n + a.chunk - 1) / a.chunk;
+    L.tile_start[k + 1] = L.tile_start[k] + nk;
+    if (mn < 0 || nk < mn) mn = nk;
+  }
+  L.rr_each = PB_INTERLEAVE ? mn : 0;
+  L.rr_chunks = L.rr_each * n;
+  L.tail_start[0] = 0;
+  for (int k = 0; k < n; ++k)
+    L.tail_start[k + 1] = L.tail_start[k] + (L.tile_start[k + 1] - L.tile_start[k]) - L.rr_each;
+}
+
+static int launch_persistent(KernFn fn, const char *name, int smem, const LaunchArgs &a,
+                             cudaStream_t stream) {
+  int bps = 0;
+  int rc = occupancy((const void *)fn, kThreads, smem, &bps);
+  if (rc) return rc;
+  cudaError_t le = launch_pdl(fn, dim3(sm_count() * bps), dim3(kThreads), smem, stream, a);
+  if (le != cudaSuccess) return cuda_status(le, name);
+  g_last_kernel = name;
+  return PB_OK;
 }
 
 static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, int bc, bool push,
@@ -1598,12 +1233,6 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
   if (st == nullptr) {
     set_error("status pointer is NULL");
     return PB_ERR_INVALID;
-  }
-  if (g_use_tma < 0) {
-    const char *env = getenv("PB_PUSH_PATH");
-    g_use_tma = 2;
-    if (env && strcmp(env, "ldg") == 0) g_use_tma = 0;
-    if (env && strcmp(env, "tma") == 0) g_use_tma = 1;
   }
   LaunchArgs a;
   memset(&a, 0, sizeof(a));
@@ -1664,7 +1293,7 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
   const int sms = sm_count();
   if (sms == 0) return cuda_status(cudaGetLastError(), "device query");
 
-  if (push && g_use_tma == 2 && all_move) {
+  if (push && all_move) {
     // Chunk list: species by descending bytes/particle.
     int order[PB_MAX_SPECIES];
     bool boris = false;
@@ -1684,45 +1313,31 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
     // Measured (profiles/r01h_claim_chunk_ab.jsonl): 1024 is -1.4% push on
     // config 2, -1.4% config 3 (ring), -1.4% config 4; config 5 (1B
     // particles, ~140 chunks per warp at 2048) is +5% slower at 1024.
-    // PB_CLAIM_CHUNK overrides (a power of two from 256 to 2048: chunks never
-    // straddle a cell8 chunk).
+    // PB_CLAIM_CHUNK (compile time) pins it (a power of two from 256 to
+    // 2048: chunks never straddle a cell8 chunk).
     {
       int64_t work = 0;
       for (int k = 0; k < a.nsp; ++k) work += a.sp[k].n;
       const int64_t warps = (int64_t)sms * 3 * kWarpsPerBlock;
-      static const int claim = getenv("PB_CLAIM_CHUNK") ? atoi(getenv("PB_CLAIM_CHUNK")) : 0;
+      constexpr int claim = PB_CLAIM_CHUNK;
       if (claim >= 256 && claim <= kChunk && (claim & (claim - 1)) == 0)
         a.chunk = claim;
       else
         a.chunk = work < warps * 64 * (int64_t)kChunk ? kChunk / 2 : kChunk;
     }
-    a.tile_start[0] = 0;
-    int64_t min_chunks = -1;
-    for (int k = 0; k < a.nsp; ++k) {
-      a.order[k] = order[k];
-      const int64_t nk = (a.sp[order[k]].n + a.chunk - 1) / a.chunk;
-      a.tile_start[k + 1] = a.tile_start[k] + nk;
-      if (min_chunks < 0 || nk < min_chunks) min_chunks = nk;
+    ChunkList all;
+    build_list(a, order, a.nsp, all);
+    for (int k = 0; k < a.nsp; ++k) a.order[k] = all.order[k];
+    for (int k = 0; k <= a.nsp; ++k) {
+      a.tile_start[k] = all.tile_start[k];
+      a.tail_start[k] = all.tail_start[k];
     }
-    // Interleave the species' chunks (round-robin while every species has
-    // some): charged chunks are latency-heavier than neutral ones, and a mix
-    // keeps the memory system busy (PB_INTERLEAVE=0: species by species).
-    if (g_interleave < 0) {
-      const char *env = getenv("PB_INTERLEAVE");
-      g_interleave = env ? atoi(env) != 0 : 1;
-    }
-    a.rr_each = g_interleave ? min_chunks : 0;
-    a.rr_chunks = a.rr_each * a.nsp;
-    a.tail_start[0] = 0;
-    for (int k = 0; k < a.nsp; ++k)
-      a.tail_start[k + 1] = a.tail_start[k] + (a.tile_start[k + 1] - a.tile_start[k]) - a.rr_each;
-    LdgFn fn = bc == PB_BC_PERIODIC
-                   ? (boris ? k_push_quad<PB_BC_PERIODIC, true> : k_push_quad<PB_BC_PERIODIC, false>)
-                   : (boris ? k_push_quad<PB_BC_ABSORBING, true> : k_push_quad<PB_BC_ABSORBING, false>);
+    a.rr_each = all.rr_each;
+    a.rr_chunks = all.rr_chunks;
     // mixed launches with ring-eligible charged species and other species:
     // the warp-specialised split kernel, measured 3-4% faster than the quad
-    // kernel on config 2 (PB_SPLIT=0: the plain quad kernel)
-    if (g_split && !boris) {
+    // kernel on config 2
+    if (PB_SPLIT && !boris) {
       int g0[PB_MAX_SPECIES], g1[PB_MAX_SPECIES], n0 = 0, n1 = 0;
       for (int k = 0; k < a.nsp; ++k) {
         const int sk = order[k];  // heaviest bytes first within each list
@@ -1730,133 +1345,52 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
         const bool elig = sp2.kind == PB_KIND_KICK && !sp2.yp && sp2.deposit >= 0 && bins;
         if (elig) g0[n0++] = sk; else g1[n1++] = sk;
       }
-      if (n0 > 0 && (n1 > 0 || g_split_solo)) {
-        const int *gs[2] = {g0, g1};
-        const int gn[2] = {n0, n1};
-        for (int g = 0; g < 2; ++g) {
-          ChunkList &L = a.lists[g];
-          L.nsp = gn[g];
-          L.tile_start[0] = 0;
-          int64_t mn = -1;
-          for (int k = 0; k < L.nsp; ++k) {
-            L.order[k] = gs[g][k];
-            const int64_t nk = (a.sp[L.order[k]].n + a.chunk - 1) / a.chunk;
-            L.tile_start[k + 1] = L.tile_start[k] + nk;
-            if (mn < 0 || nk < mn) mn = nk;
-          }
-          L.rr_each = g_interleave ? mn : 0;
-          L.rr_chunks = L.rr_each * L.nsp;
-          L.tail_start[0] = 0;
-          for (int k = 0; k < L.nsp; ++k)
-            L.tail_start[k + 1] = L.tail_start[k] + (L.tile_start[k + 1] - L.tile_start[k]) - L.rr_each;
-        }
-        LdgFn sfn = bc == PB_BC_PERIODIC ? k_push_split<PB_BC_PERIODIC> : k_push_split<PB_BC_ABSORBING>;
-        int sbps = 0;
-        int src = occupancy((const void *)sfn, kThreads, split_smem_bytes(), &sbps);
-        if (src) return src;
-        cudaError_t le = launch_pdl(sfn, dim3(sms * sbps), dim3(kThreads), split_smem_bytes(), stream, a);
-        if (le != cudaSuccess) return cuda_status(le, "k_push_split");
-        g_last_kernel = "k_push_split";
-        return PB_OK;
+      if (n0 > 0 && (n1 > 0 || PB_SPLIT_SOLO)) {
+        build_list(a, g0, n0, a.lists[0]);
+        build_list(a, g1, n1, a.lists[1]);
+        return launch_persistent(bc == PB_BC_PERIODIC ? k_push_split<PB_BC_PERIODIC>
+                                                      : k_push_split<PB_BC_ABSORBING>,
+                                 "k_push_split", split_smem_bytes(), a, stream);
       }
     }
     // charged-only launches (every species KICK without yp, depositing, on
     // the full int32 cell index): the per-warp TMA ring kernel
-    bool ring = g_ring;
+    bool ring = PB_RING;
     for (int k = 0; k < a.nsp && ring; ++k)
       ring = a.sp[k].kind == PB_KIND_KICK && !a.sp[k].yp && a.sp[k].deposit >= 0 && bins &&
              !a.sp[k].cell8;
-    if (ring) {
-      LdgFn rfn = bc == PB_BC_PERIODIC ? k_push_ring<PB_BC_PERIODIC> : k_push_ring<PB_BC_ABSORBING>;
-      int bps = 0;
-      int rc = occupancy((const void *)rfn, kThreads, ring_smem_bytes(), &bps);
-      if (rc) return rc;
-      cudaError_t le = launch_pdl(rfn, dim3(sms * bps), dim3(kThreads), ring_smem_bytes(), stream, a);
-      if (le != cudaSuccess) return cuda_status(le, "k_push_ring");
-      g_last_kernel = "k_push_ring";
-      return PB_OK;
-    }
-    int bps = 0;
-    int rc = occupancy((const void *)fn, kThreads, 0, &bps);
-    if (rc) return rc;
-    cudaError_t le = launch_pdl(fn, dim3(sms * bps), dim3(kThreads), 0, stream, a);
-    if (le != cudaSuccess) return cuda_status(le, "k_push_quad");
-    g_last_kernel = "k_push_quad";
-    return PB_OK;
+    if (ring)
+      return launch_persistent(bc == PB_BC_PERIODIC ? k_push_ring<PB_BC_PERIODIC>
+                                                    : k_push_ring<PB_BC_ABSORBING>,
+                               "k_push_ring", ring_smem_bytes(), a, stream);
+    KernFn fn = bc == PB_BC_PERIODIC
+                    ? (boris ? k_push_quad<PB_BC_PERIODIC, true> : k_push_quad<PB_BC_PERIODIC, false>)
+                    : (boris ? k_push_quad<PB_BC_ABSORBING, true> : k_push_quad<PB_BC_ABSORBING, false>);
+    return launch_persistent(fn, "k_push_quad", 0, a, stream);
   }
-  if (push && g_use_tma == 1 && all_move) {
-    // Tile list: species by descending bytes/particle, full tiles only.
-    int order[PB_MAX_SPECIES];
-    for (int k = 0; k < a.nsp; ++k) order[k] = k;
-    for (int i = 1; i < a.nsp; ++i)
-      for (int j = i; j > 0 && bytes_per_particle(a.sp[order[j]], true) >
-                                   bytes_per_particle(a.sp[order[j - 1]], true); --j) {
-        const int tmp = order[j];
-        order[j] = order[j - 1];
-        order[j - 1] = tmp;
-      }
-    int smem = 0;
-    a.tile_start[0] = 0;
-    for (int k = 0; k < a.nsp; ++k) {
-      const pb_species &s = a.sp[order[k]];
-      a.order[k] = order[k];
-      a.tile_start[k + 1] = a.tile_start[k] + s.n / tile_of(s.kind, s.yp != nullptr);
-      const int sb = stage_bytes(s.kind, s.yp != nullptr);
-      if (sb > smem) smem = sb;
-    }
-    if (bc == PB_BC_ABSORBING) {
-      // n_dev can shrink below the host bound: keep the tile list within it
-      // by sending everything through the LDG path for absorbing walls.
-      goto ldg;
-    }
-    {
-      if (g_stages == 0) {
-        const char *env = getenv("PB_STAGES");
-        g_stages = env ? atoi(env) : 2;
-        if (g_stages < 2) g_stages = 2;
-        if (g_stages > kMaxStages) g_stages = kMaxStages;
-      }
-      if (g_ahead < 0) {
-        const char *env = getenv("PB_AHEAD");
-        g_ahead = env ? atoi(env) : 0;
-        if (g_ahead < 0) g_ahead = 0;
-        if (g_ahead > kMaxAhead) g_ahead = kMaxAhead;
-      }
-      const int stride = smem;
-      smem *= g_stages;
-      TmaFn fn = k_push_tma<PB_BC_PERIODIC>;
-      int bps = 0;
-      int rc = occupancy((const void *)fn, kThreads + 32, smem, &bps);
-      if (rc) return rc;
-      fn<<<sms * bps, kThreads + 32, smem, stream>>>(a, stride, g_stages, g_ahead);
-      PB_CHECK_LAUNCH("k_push_tma");
-      g_last_kernel = "k_push_tma";
-      return PB_OK;
-    }
+  // Deposit-only launches and launches with inactive depositing species:
+  // static contiguous chunks per block, shared-memory deposit window.
+  KernFn fn = bc == PB_BC_PERIODIC
+                  ? (push ? k_push_deposit<PB_BC_PERIODIC, true> : k_push_deposit<PB_BC_PERIODIC, false>)
+                  : (push ? k_push_deposit<PB_BC_ABSORBING, true> : k_push_deposit<PB_BC_ABSORBING, false>);
+  int bps = 0;
+  int rc = occupancy((const void *)fn, kThreads, 0, &bps);
+  if (rc) return rc;
+  const int grid = sms * bps;
+  int start = 0;
+  for (int k = 0; k < a.nsp; ++k) {
+    const int64_t tiles = (a.sp[k].n + kTile - 1) / kTile;
+    int64_t nb = (int64_t)(grid * (w[k] / wsum) + 0.5);
+    if (nb < 1) nb = 1;
+    if (nb > tiles) nb = tiles;
+    a.blk_start[k] = start;
+    start += (int)nb;
   }
-ldg : {
-    LdgFn fn = bc == PB_BC_PERIODIC
-                   ? (push ? k_push_deposit<PB_BC_PERIODIC, true> : k_push_deposit<PB_BC_PERIODIC, false>)
-                   : (push ? k_push_deposit<PB_BC_ABSORBING, true> : k_push_deposit<PB_BC_ABSORBING, false>);
-    int bps = 0;
-    int rc = occupancy((const void *)fn, kThreads, 0, &bps);
-    if (rc) return rc;
-    const int grid = sms * bps;
-    int start = 0;
-    for (int k = 0; k < a.nsp; ++k) {
-      const int64_t tiles = (a.sp[k].n + kTile - 1) / kTile;
-      int64_t nb = (int64_t)(grid * (w[k] / wsum) + 0.5);
-      if (nb < 1) nb = 1;
-      if (nb > tiles) nb = tiles;
-      a.blk_start[k] = start;
-      start += (int)nb;
-    }
-    a.blk_start[a.nsp] = start;
-    fn<<<start, kThreads, 0, stream>>>(a);
-    PB_CHECK_LAUNCH("k_push_deposit");
-    g_last_kernel = "k_push_deposit";
-    return PB_OK;
-  }
+  a.blk_start[a.nsp] = start;
+  fn<<<start, kThreads, 0, stream>>>(a);
+  PB_CHECK_LAUNCH("k_push_deposit");
+  g_last_kernel = "k_push_deposit";
+  return PB_OK;
 }
 
 }  // namespace pb

@@ -49,38 +49,8 @@ __global__ void k_fused_move(const double *__restrict__ accel, double *x,
 }
 
 // deposit_partials (_kernels.pyx:14-34): strictly sequential per cell in
-// slot order, so the result is bitwise the reference's.  The warp loads 32
-// slots at a time and every lane replays the same sequential sum.
-__global__ void k_deposit_partials(const double *__restrict__ x,
-                                   const int64_t *__restrict__ offs,
-                                   const int64_t *__restrict__ counts,
-                                   int64_t nc, double *__restrict__ left,
-                                   double *__restrict__ right) {
-  const unsigned full = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const int64_t w0 = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const int64_t nw = (int64_t)gridDim.x * kWarps;
-  for (int64_t j = w0; j < nc; j += nw) {
-    const int64_t base = offs[j];
-    const int64_t cnt = counts[j];
-    double sl = 0.0, sr = 0.0;
-    for (int64_t c0 = 0; c0 < cnt; c0 += 32) {
-      const double xv = (c0 + lane < cnt) ? x[base + c0 + lane] : 0.0;
-      const int m = (int)((cnt - c0) < 32 ? (cnt - c0) : 32);
-      for (int k = 0; k < m; ++k) {
-        const double xk = __shfl_sync(full, xv, k);
-        sl = __dadd_rn(sl, __dsub_rn(1.0, xk));
-        sr = __dadd_rn(sr, xk);
-      }
-    }
-    if (lane == 0) {
-      left[j] = sl;
-      right[j] = sr;
-    }
-  }
-}
-
-// The same sums with one thread per cell: the sequential add chain is the
+// slot order, so the result is bitwise the reference's.  One thread per
+// cell: the sequential add chain is the
 // latency, so 32 cells per warp in flight (loads issued four ahead) beat a
 // warp replaying one cell's chain.
 __global__ void k_deposit_partials_tpc(const double *__restrict__ x,
@@ -207,18 +177,11 @@ extern "C" int pb_deposit_partials(const double *x, const int64_t *offs,
     pb::set_error("pb_deposit_partials: NULL array argument");
     return PB_ERR_INVALID;
   }
-  static const bool tpc = !(getenv("PB_DEPOSIT_TPC") && atoi(getenv("PB_DEPOSIT_TPC")) == 0);
-  if (tpc) {
-    int64_t blocks = (nc + 255) / 256;
-    if (blocks > 148 * 64) blocks = 148 * 64;
-    pb::k_deposit_partials_tpc<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-        x, offs, counts, nc, left, right);
-    PB_CHECK_LAUNCH("k_deposit_partials_tpc");
-    return PB_OK;
-  }
-  pb::k_deposit_partials<<<pb::shim_grid(nc), pb::kShimThreads, 0, (cudaStream_t)stream>>>(
+  int64_t blocks = (nc + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  pb::k_deposit_partials_tpc<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
       x, offs, counts, nc, left, right);
-  PB_CHECK_LAUNCH("k_deposit_partials");
+  PB_CHECK_LAUNCH("k_deposit_partials_tpc");
   return PB_OK;
 }
 

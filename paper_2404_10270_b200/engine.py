@@ -89,26 +89,42 @@ def species_kind(sp, b_field) -> int:
     return _lib.PB_KIND_DRIFT
 
 
+def sort_periods_for(config, sort_every: int, ratio_cap: int = 16) -> list:
+    """Per-species cell-sort period.  `sort_every` applies to the fastest
+    species (largest thermal drift per step, nstep included); slower ones
+    lose cell order proportionally more slowly and are sorted proportionally
+    less often (x ratio_cap at most: measured +0.4% over x64, the slow
+    species otherwise lose order over a few thousand steps).  0 = never."""
+    if not sort_every:
+        return [0] * len(config.species)
+    b_field = getattr(config, "b_field_t", None)
+    drift = []
+    for isp, spd in enumerate(config.species):
+        v = thermal_std(config.temperatures_ev[isp], spd.mass_kg, config.consts.dt_s,
+                        config.grid.dx_m) * float(spd.nstep)
+        drift.append(v if species_kind(spd, b_field) != _lib.PB_KIND_INACTIVE else 0.0)
+    vmax = max(drift) or 1.0
+    return [0 if v <= 0.0 else sort_every * int(min(ratio_cap, max(1, round(vmax / v)))) for v in drift]
+
+
 class Engine:
     """One GPU's share of a run: its particle shard plus a grid replica."""
 
+    # Tuning attributes (class-level defaults = the measured-best settings;
+    # tests and A/B scripts override them on an instance or subclass).
     supports_collisions = False  # CanonicalEngine (canonical.py) runs them
-    use_cell8 = os.environ.get("PB_CELL8", "1") != "0"
-    force_cell8 = os.environ.get("PB_CELL8", "1") == "2"  # also in charged-only runs (A/B)
-    sort_ratio_cap = int(os.environ.get("PB_SORT_RATIO_CAP", "16"))
+    use_cell8 = True     # 1-byte cell index for dense charged species
+    force_cell8 = False  # ... also in charged-only runs (measured slower there)
+    sort_ratio_cap = 16  # slow species are sorted at most 16x less often
     # Field-solve steps: push neutral movers while the field pipeline runs.
     # Measured 2.4% slower on one GPU (a second launch's ramp/tail costs more
     # than the ~30 us field pipeline it hides); with N > 1 it also hides the
-    # density allreduce.  PB_FIELD_SPLIT=1/0 forces it either way.
+    # density allreduce.  None = on iff N > 1; True/False force it.
     field_split = None
-    # pb_field_pipeline (one cooperative launch for smoothing + Poisson + E)
-    # measured 0.8-6% slower than the per-phase kernels inside graphs
-    # (configs 4 and 3), so it is opt-in: PB_FUSED_FIELD=1
-    fused_field = os.environ.get("PB_FUSED_FIELD", "0") == "1"
     supports_peer = True  # the fused peer-memory density exchange (N > 1)
     # serial field-solve cycle: density in one pb_rho_epilogue launch, bins
-    # cleared by the E kernel (PB_DENSITY_ONE=0: pb_density_step's two launches)
-    density_one = os.environ.get("PB_DENSITY_ONE", "1") != "0"
+    # cleared by the E kernel (False: pb_density_step's two launches)
+    density_one = True
 
     def __init__(self, config, device=None, *, rank: int = 0, world: int = 1,
                  group=None, init: str = "host", check_every: int = 1, peer: bool = None):
@@ -222,30 +238,15 @@ class Engine:
         self._tile_counter = self.status[off:off + 8]
         self.absorbed = np.zeros((len(self.sp), 2), dtype=np.int64)
         self.moved = np.zeros(len(self.sp), dtype=np.int64)
+        # in-kernel mover clock (pb_status.mover_ns / mover_launches), summed
+        # over syncs: the persistent movers' own duration, graph replays included
+        self.mover_ns = 0
+        self.mover_launches = 0
         self._load(init)
 
     # -- setup ------------------------------------------------------------------
     def _sort_periods(self, config) -> list:
-        """Per-species cell-sort period.  `sort_every` applies to the fastest
-        species (largest thermal drift per step, nstep included); slower ones
-        lose cell order proportionally more slowly and are sorted
-        proportionally less often (x16 at most: measured +0.4% over x64, the
-        slow species otherwise lose order over a few thousand steps).  0 = never."""
-        if not self.sort_every:
-            return [0] * len(self.sp)
-        drift = []
-        for isp, s in enumerate(self.sp):
-            t = config.temperatures_ev[isp]
-            v = thermal_std(t, s.sp.mass_kg, config.consts.dt_s, self.grid.dx_m) * s.fnstep
-            drift.append(v if s.kind != _lib.PB_KIND_INACTIVE else 0.0)
-        vmax = max(drift) or 1.0
-        out = []
-        for v in drift:
-            if v <= 0.0:
-                out.append(0)
-                continue
-            out.append(self.sort_every * int(min(self.sort_ratio_cap, max(1, round(vmax / v)))))
-        return out
+        return sort_periods_for(config, self.sort_every, self.sort_ratio_cap)
 
     def _species_cap(self, isp: int, nloc: int) -> int:
         return nloc
@@ -389,13 +390,6 @@ class Engine:
         sh = ctypes.c_void_p(st.cuda_stream)
         scr = self.field_scratch.data_ptr()
         with torch.cuda.stream(st):
-            if self.poisson == "scan" and self.fused_field:
-                # one cooperative launch: smoothing + scan Poisson + E
-                _lib.check(self.lib.pb_field_pipeline(
-                    rho.data_ptr(), self.rho_s.data_ptr(), self.phi.data_ptr(), self.e.data_ptr(),
-                    self.nc, int(cfg.smoothing_passes), self.grid.dx_m, cfg.consts.epsilon0,
-                    self.field_bc, cfg.phi_left, cfg.phi_right, scr, sh), "pb_field_pipeline")
-                return self.e
             src = rho
             if cfg.smoothing_passes > 0:
                 _lib.check(self.lib.pb_smooth_density(rho.data_ptr(), self.rho_s.data_ptr(), self.nc,
@@ -439,8 +433,7 @@ class Engine:
         rest = [k for k in range(len(self.sp)) if k not in neutral]
         split = self.field_split
         if split is None:
-            env = os.environ.get("PB_FIELD_SPLIT")
-            split = (env != "0") if env is not None else self.world > 1
+            split = self.world > 1
         if not neutral or not rest or not split:
             return [], list(range(len(self.sp)))
         return neutral, rest
@@ -466,7 +459,7 @@ class Engine:
         movers this is the plain serial cycle."""
         neutral, rest = self._field_split()
         if not neutral:
-            if self.density_one and not self.fused_field and self.peer is None:
+            if self.density_one and self.peer is None:
                 # one-kernel epilogue (no self-clear: neighbouring nodes read
                 # the same cells); E clears the bins (bitwise density())
                 rho = self._density_one()
@@ -951,6 +944,8 @@ class Engine:
         self._side.synchronize()
         raw = self.status.cpu().numpy()
         st = decode_status(raw)
+        self.mover_ns += int(st.mover_ns)
+        self.mover_launches += int(st.mover_launches)
         for k in range(len(self.sp)):
             self.moved[k] += st.moved[k]
             self.absorbed[k, 0] += st.absorbed[k][0]

@@ -152,9 +152,10 @@ def species_array(species: list, n_host=None):
 
 
 def status_template(device) -> torch.Tensor:
-    """Zeroed pb_status with cfl_index = UINT64_MAX, as raw bytes on device."""
+    """Zeroed pb_status with cfl_index = mover_t0 = UINT64_MAX, as raw bytes on device."""
     st = _lib.PbStatus()
     st.cfl_index = (1 << 64) - 1
+    st.mover_t0 = (1 << 64) - 1
     raw = bytes(ctypes.string_at(ctypes.addressof(st), _lib.STATUS_BYTES))
     return torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(device)
 

@@ -21,6 +21,20 @@ from golden_cfg import COLLISION_KATS, RUNS_ALL, cfg_from, host_species
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture
+def scatter_min(cuda):
+    """Set the canonical scatter-resort threshold; restores the default."""
+    from paper_2404_10270_b200 import _lib
+
+    lib = _lib.load()
+
+    def set_(n):
+        _lib.check(lib.pb_set_canonical_scatter_min(int(n)), "pb_set_canonical_scatter_min")
+
+    yield set_
+    set_(1 << 20)
+
+
 def _flat_from(d):
     from paper_2404_10270_b200.core import FlatSpecies
 
@@ -84,10 +98,10 @@ def _run(cfg):
 
 @pytest.mark.parametrize("resort", ["sort", "scatter"])
 @pytest.mark.parametrize("name", RUNS_ALL)
-def test_canonical_run_matches_reference_bitwise(cuda, name, resort, monkeypatch):
-    """resort: the full key sort (stores under PB_CANON_SCATTER_MIN, here all)
+def test_canonical_run_matches_reference_bitwise(cuda, name, resort, scatter_min):
+    """resort: the full key sort (stores under the scatter threshold, here all)
     or the scatter path (stayers by prefix count, movers sorted) forced on."""
-    monkeypatch.setenv("PB_CANON_SCATTER_MIN", "0" if resort == "scatter" else str(1 << 40))
+    scatter_min(0 if resort == "scatter" else 1 << 40)
     g = load_golden(f"{name}.npz")
     cfg = cfg_from(g, slot_order="canonical")
     m, h = _run(cfg)
@@ -155,7 +169,7 @@ def test_canonical_extensions_match_oracle(cuda, boundary):
         assert h["totals"][-1][0] < h["totals"][0][0] + m.tally.ionization
 
 
-def test_desk_criterion01_bitwise_and_ode(cuda, monkeypatch):
+def test_desk_criterion01_bitwise_and_ode(cuda, scatter_min):
     """pkg/configs/desk.toml to the ODE half-depletion step (the reference's
     acceptance criterion 01, pkg/tests/test_acceptance.py:73-117): every
     per-step diagnostic row, the last rho and the final stores equal the
@@ -165,7 +179,7 @@ def test_desk_criterion01_bitwise_and_ode(cuda, monkeypatch):
 
     from paper_2404_10270_b200 import load_config, run_simulation
 
-    monkeypatch.setenv("PB_CANON_SCATTER_MIN", "0")
+    scatter_min(0)
     g = load_golden("run_desk_criterion01.npz")
     cfg = load_config(os.path.join(os.path.dirname(__file__), "..", "configs", "desk.toml"))
     steps = int(g["steps"])

@@ -181,44 +181,6 @@ def test_poisson_scan_matches_reference_and_exact(cuda):
         assert np.max(np.abs(ea - eb)) <= 1e-8 * np.max(np.abs(eb)), code
 
 
-@pytest.mark.parametrize("nc", [3, 100, 2049, 65536, 300001])
-@pytest.mark.parametrize("passes", [0, 1, 3])
-def test_fused_field_pipeline_bitwise(cuda, nc, passes):
-    """pb_field_pipeline (one cooperative launch) == pb_smooth_density +
-    pb_solve_poisson_scan + pb_compute_efield, bit for bit."""
-    import ctypes
-
-    import torch
-
-    from conftest import bits_equal
-    from paper_2404_10270_b200 import _lib
-
-    lib = _lib.load()
-    sh = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    rng = np.random.default_rng(nc + passes)
-    for code in (0, 1):
-        rho = torch.from_numpy(40.0 * rng.standard_normal(nc + 1)).to(cuda)
-        if code == 0:
-            rho[nc] = rho[0]
-        scr = torch.zeros(lib.pb_field_scratch_bytes(nc) // 8 + 1, dtype=torch.float64, device=cuda)
-        a_s, a_phi, a_e = (torch.zeros(nc + 1, dtype=torch.float64, device=cuda) for _ in range(3))
-        _lib.check(lib.pb_field_pipeline(rho.data_ptr(), a_s.data_ptr(), a_phi.data_ptr(), a_e.data_ptr(),
-                                         nc, passes, 1e-5, 8.8541878128e-12, code, 1.5, -2.0,
-                                         scr.data_ptr(), sh))
-        b_s, b_phi, b_e = (torch.zeros(nc + 1, dtype=torch.float64, device=cuda) for _ in range(3))
-        src = rho
-        if passes:
-            _lib.check(lib.pb_smooth_density(rho.data_ptr(), b_s.data_ptr(), nc, passes, scr.data_ptr(), sh))
-            src = b_s
-        _lib.check(lib.pb_solve_poisson_scan(src.data_ptr(), b_phi.data_ptr(), nc, 1e-5, 8.8541878128e-12,
-                                             code, 1.5, -2.0, scr.data_ptr(), sh))
-        _lib.check(lib.pb_compute_efield(b_phi.data_ptr(), b_e.data_ptr(), nc, 1e-5, code, sh))
-        if passes:
-            assert bits_equal(a_s.cpu().numpy(), b_s.cpu().numpy()), code
-        assert bits_equal(a_phi.cpu().numpy(), b_phi.cpu().numpy()), code
-        assert bits_equal(a_e.cpu().numpy(), b_e.cpu().numpy()), code
-
-
 def _small_sheath(n_steps=60, nc=256, sort_every=10):
     from paper_2404_10270_b200.config import load_config
 
