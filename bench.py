@@ -82,6 +82,9 @@ WORKLOADS = {
            "strong", "configs/c4_sol_boris.toml"),
     "c5": ("config 5: 1M cells, 1B particles total (e-/D+/D), field solve off", "strong",
            "configs/c5_weak_1m.toml"),
+    "c4b": ("config 4 with a spatially varying B: Bz 2.5 -> 1.5 T along x, gathered per particle "
+            "(pb_species.b_nodes), Boris push, 100M particles, field solve", "strong",
+            "configs/c4b_sol_gradb.toml"),
 }
 
 
@@ -301,6 +304,9 @@ def run_ours(args, rank, world, local_rank):
     pushes_rank = sum(s.n for s in eng.sp if s.kind != 0)
     boris = cfg.b_field_t is not None
     alg_bytes = sum(s.n * species_alg_bytes(s.sp, boris) for s in eng.sp)
+    # gathered B: two 32-byte node reads per Boris push, served from L2 (the
+    # (nc+1) x 32 B profile is 3.2 MB); reported beside, not in, alg_bytes
+    b_node_bytes = (sum(s.n for s in eng.sp if s.kind == 3) * 64.0 if eng.b_nodes is not None else 0.0)
 
     def max_over_ranks(*vals):
         if world == 1:
@@ -504,6 +510,9 @@ def run_ours(args, rank, world, local_rank):
                                "of the timed steps"),
             "traffic": traffic, "traffic_source": traffic_src,
         },
+        **({"b_node_reads": {"bytes_per_launch": b_node_bytes, "bytes_per_boris_push": 64.0,
+                             "level": "L2 (node profile 32 B x (nc+1), not HBM state)"}}
+           if b_node_bytes else {}),
         "e2e": {"value": e2e_value, "unit": "particle-pushes/s",
                 "h2d_bytes_per_step": 0 if cfg.field_solve else nodes * 8,
                 "d2h_bytes_per_step": nodes * 8,

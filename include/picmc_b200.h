@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define PB_ABI_VERSION 2
+#define PB_ABI_VERSION 3
 
 #define PB_OK 0
 #define PB_ERR_INVALID 1
@@ -48,7 +48,7 @@ extern "C" {
 #define PB_KIND_INACTIVE 0 /* active_mover == False: not pushed            */
 #define PB_KIND_DRIFT 1    /* uncharged: x += nstep*vx, no kick (keeps -0.0) */
 #define PB_KIND_KICK 2     /* charged: one-sided gather, vx += a, drift      */
-#define PB_KIND_BORIS 3    /* charged + uniform B: Boris rotation (config 4) */
+#define PB_KIND_BORIS 3    /* charged + B: Boris rotation (config 4)         */
 
 /* Particle boundary: the reference always wraps (mover.py:156); absorbing
  * walls are the config-3 extension restated in oracle/ and DESIGN.md. */
@@ -87,6 +87,20 @@ typedef struct pb_species {
    * after anything reorders a species. */
   int8_t *cell8;
   int32_t *chunk_base;
+  /* Spatially varying B (SURVEY.md 8(b) `b_nodes_or_null`, carried per
+   * species so every mover entry point -- pb_push_deposit, the canonical
+   * resort / keys and the shims -- sees it without another argument):
+   * b_nodes[4*j + k] = B_k at node j in tesla (k = x, y, z; slot 3 is
+   * padding so one node is one 32-byte load), nc+1 nodes.  NULL = the
+   * uniform boris_t / boris_s above.  Otherwise, per Boris particle in cell
+   * j at cell-relative x (pre-push), with f = boris_f = q dt / (2 m):
+   *   t_k = f*B_k[j] + x*(f*B_k[j+1] - f*B_k[j])   (the one-sided gather
+   *                                                  of accel_nodes, mover.py:221)
+   *   s_k = (2*t_k) / (1 + ((t_x*t_x + t_y*t_y) + t_z*t_z))
+   * each operation rounded separately (no FMA), restated in
+   * oracle/picmc_oracle.c:boris_t_gather. */
+  const double *b_nodes;
+  double boris_f;
 } pb_species;
 
 #define PB_CELL8_CHUNK 2048

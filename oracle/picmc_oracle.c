@@ -125,6 +125,24 @@ static void boris(double *vx, double *vy, double *vz, double atemp,
   *vz = qz;
 }
 
+/* Spatially varying B (pb_species.b_nodes, include/picmc_b200.h): nodes
+ * hold (Bx, By, Bz, pad) in tesla; t = the one-sided linear gather of f*B
+ * (f = q dt / (2 m)) in the accel_nodes form (pkg/src/picmc/mover.py:221,
+ * _kernels.pyx:83-86), s = 2 t / (1 + |t|^2) in the host's
+ * boris_coefficients op order.  Each operation rounds separately. */
+static void boris_t_gather(const double *bnodes, double f, int32_t c, double x, double *t,
+                           double *s) {
+  const double *b0 = bnodes + 4 * (int64_t)c, *b1 = b0 + 4;
+  for (int k = 0; k < 3; ++k) {
+    const double t0 = f * b0[k];
+    const double t1 = f * b1[k];
+    t[k] = t0 + x * (t1 - t0);
+  }
+  const double t2 = t[0] * t[0] + t[1] * t[1] + t[2] * t[2];
+  const double den = 1.0 + t2;
+  for (int k = 0; k < 3; ++k) s[k] = (2.0 * t[k]) / den;
+}
+
 static int64_t pymod(int64_t a, int64_t m) {
   int64_t r = a % m;
   return r < 0 ? r + m : r;
@@ -146,7 +164,7 @@ int64_t or_step_flat(int kind, int bc, double fnstep, double kick_coef,
                      const double *bt, const double *bs, const double *e,
                      int64_t nc, int64_t n, double *x, double *vx, double *vy,
                      double *vz, double *yp, int32_t *cell, uint8_t *removed,
-                     int64_t *cfl_index) {
+                     int64_t *cfl_index, const double *bnodes, double bf) {
   for (int64_t i = 0; i < n; ++i) {
     const int32_t c = cell[i];
     if (kind == OR_KICK || kind == OR_BORIS) {
@@ -157,7 +175,9 @@ int64_t or_step_flat(int kind, int bc, double fnstep, double kick_coef,
         const double v = vx[i] + atemp;
         vx[i] = v;
       } else {
-        boris(&vx[i], &vy[i], &vz[i], atemp, bt, bs);
+        double tg[3], sg[3];
+        if (bnodes) boris_t_gather(bnodes, bf, c, x[i], tg, sg);
+        boris(&vx[i], &vy[i], &vz[i], atemp, bnodes ? tg : bt, bnodes ? sg : bs);
       }
     }
     if (kind != 0) x[i] = x[i] + fnstep * vx[i];
@@ -397,7 +417,7 @@ int64_t or_collide(uint64_t step_key, int64_t global_offset, int64_t nc, const d
 int64_t or_step_moved(int kind, int bc, double fnstep, double kick_coef, const double *bt,
                       const double *bs, const double *e, int64_t nc, int64_t n, double *x,
                       double *vx, double *vy, double *vz, double *yp, int32_t *cell,
-                      uint8_t *removed, uint8_t *moved) {
+                      uint8_t *removed, uint8_t *moved, const double *bnodes, double bf) {
   for (int64_t i = 0; i < n; ++i) moved[i] = 0;
   if (kind == 0) {
     for (int64_t i = 0; i < n; ++i) removed[i] = 0;
@@ -412,7 +432,9 @@ int64_t or_step_moved(int kind, int bc, double fnstep, double kick_coef, const d
       if (kind == OR_KICK) {
         vx[i] = vx[i] + atemp;
       } else {
-        boris(&vx[i], &vy[i], &vz[i], atemp, bt, bs);
+        double tg[3], sg[3];
+        if (bnodes) boris_t_gather(bnodes, bf, c, x[i], tg, sg);
+        boris(&vx[i], &vy[i], &vz[i], atemp, bnodes ? tg : bt, bnodes ? sg : bs);
       }
     }
     x[i] = x[i] + fnstep * vx[i];

@@ -38,7 +38,7 @@ PB_CELL8_CHUNK = 2048
 PB_DEPOSIT_FRAC_BITS = 48
 # largest per-cell, per-species particle count the fixed-point bins represent
 PB_MAX_CELL_COUNT = (1 << (64 - PB_DEPOSIT_FRAC_BITS)) - 1
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _p = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -53,6 +53,7 @@ class PbSpecies(ctypes.Structure):
         ("kind", _i32), ("deposit", _i32), ("fnstep", _f64),
         ("kick_coef", _f64), ("boris_t", _f64 * 3), ("boris_s", _f64 * 3),
         ("cell8", _p), ("chunk_base", _p),
+        ("b_nodes", _p), ("boris_f", _f64),
     ]
 
 

@@ -323,7 +323,7 @@ __device__ __forceinline__ uint64_t canon_push_one(const CanonPushArgs &a, int64
       const MoveOut o = transfer<BC>(x, c, a.nc);
       s.x[i] = x;
       if (KIND != PB_KIND_DRIFT) s.vx[i] = vx;
-      if (KIND == PB_KIND_BORIS) {
+      if (is_boris(KIND)) {
         s.vy[i] = vy;
         s.vz[i] = vz;
       }
@@ -486,7 +486,10 @@ static int launch_canon_push(const pb_species *src, const pb_canon *cv, const do
     case PB_KIND_INACTIVE: PB_CANON(PB_KIND_INACTIVE); break;
     case PB_KIND_DRIFT: PB_CANON(PB_KIND_DRIFT); break;
     case PB_KIND_KICK: PB_CANON(PB_KIND_KICK); break;
-    case PB_KIND_BORIS: PB_CANON(PB_KIND_BORIS); break;
+    case PB_KIND_BORIS:
+      if (src->b_nodes) PB_CANON(kKindBorisB);
+      else PB_CANON(PB_KIND_BORIS);
+      break;
     default:
       set_error("canonical push: unknown kind %d", src->kind);
       return PB_ERR_INVALID;

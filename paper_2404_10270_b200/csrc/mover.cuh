@@ -19,6 +19,44 @@ struct MoveOut {
   bool cfl;        // |floor(x)| >= nc
 };
 
+// Device-internal kind: PB_KIND_BORIS with a B node profile (b_nodes set).
+// A separate instantiation, so the uniform-B Boris path keeps its registers.
+constexpr int kKindBorisB = 4;
+__host__ __device__ constexpr bool is_boris(int k) { return k == PB_KIND_BORIS || k == kKindBorisB; }
+
+// Spatially varying B (pb_species.b_nodes): one 32-byte read-only load per
+// node (bx, by, bz, pad; L2-resident), the one-sided linear gather of
+// f*B in the same form as accel_nodes (pkg/src/picmc/mover.py:221), then
+// s = 2t / (1 + |t|^2) -- the host's boris_coefficients op order
+// (engine.py), so a constant profile reproduces the uniform path.
+__device__ __forceinline__ void ldg_node4(const double *p, double &a, double &b, double &c) {
+  double d;
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
+__device__ __forceinline__ double node_gather(double f, double b0, double b1, double x) {
+  const double t0 = __dmul_rn(f, b0);
+  const double t1 = __dmul_rn(f, b1);
+  return __dadd_rn(t0, __dmul_rn(x, __dsub_rn(t1, t0)));
+}
+
+__device__ __forceinline__ void boris_t_gather(const pb_species &s, int32_t cell, double x,
+                                               double &tx, double &ty, double &tz, double &sx,
+                                               double &sy, double &sz) {
+  double b0x, b0y, b0z, b1x, b1y, b1z;
+  ldg_node4(s.b_nodes + 4 * (int64_t)cell, b0x, b0y, b0z);
+  ldg_node4(s.b_nodes + 4 * (int64_t)cell + 4, b1x, b1y, b1z);
+  const double f = s.boris_f;
+  tx = node_gather(f, b0x, b1x, x);
+  ty = node_gather(f, b0y, b1y, x);
+  tz = node_gather(f, b0z, b1z, x);
+  const double t2 = __dadd_rn(__dadd_rn(__dmul_rn(tx, tx), __dmul_rn(ty, ty)), __dmul_rn(tz, tz));
+  const double den = __dadd_rn(1.0, t2);
+  sx = __ddiv_rn(__dmul_rn(2.0, tx), den);
+  sy = __ddiv_rn(__dmul_rn(2.0, ty), den);
+  sz = __ddiv_rn(__dmul_rn(2.0, tz), den);
+}
+
 template <int KIND>
 __device__ __forceinline__ void kick_drift(double &x, double &vx, double &vy,
                                            double &vz, int32_t cell,
@@ -32,7 +70,7 @@ __device__ __forceinline__ void kick_drift(double &x, double &vx, double &vy,
     const double v = __dadd_rn(vx, atemp);
     vx = v;
     x = __dadd_rn(x, __dmul_rn(s.fnstep, v));
-  } else if (KIND == PB_KIND_BORIS) {
+  } else if (is_boris(KIND)) {
     // Boris (config 4, restated in oracle/picmc_oracle.c:boris_push):
     // half kick, rotation v' = v- + v- x t, v+ = v- + v' x s, half kick.
     const double aj = __dmul_rn(s.kick_coef, __ldg(e + cell));
@@ -40,8 +78,9 @@ __device__ __forceinline__ void kick_drift(double &x, double &vx, double &vy,
     const double daj = __dsub_rn(aj1, aj);
     const double atemp = __dadd_rn(aj, __dmul_rn(x, daj));
     const double h = __dmul_rn(0.5, atemp);
-    const double tx = s.boris_t[0], ty = s.boris_t[1], tz = s.boris_t[2];
-    const double sx = s.boris_s[0], sy = s.boris_s[1], sz = s.boris_s[2];
+    double tx = s.boris_t[0], ty = s.boris_t[1], tz = s.boris_t[2];
+    double sx = s.boris_s[0], sy = s.boris_s[1], sz = s.boris_s[2];
+    if (KIND == kKindBorisB) boris_t_gather(s, cell, x, tx, ty, tz, sx, sy, sz);
     const double mx = __dadd_rn(vx, h), my = vy, mz = vz;
     const double px = __dadd_rn(mx, __dsub_rn(__dmul_rn(my, tz), __dmul_rn(mz, ty)));
     const double py = __dadd_rn(my, __dsub_rn(__dmul_rn(mz, tx), __dmul_rn(mx, tz)));

@@ -141,10 +141,10 @@ struct Pair {
 
 template <int KIND, bool YP>
 struct Fields {
-  static constexpr bool kNeedV = (KIND == PB_KIND_KICK || KIND == PB_KIND_BORIS ||
+  static constexpr bool kNeedV = (KIND == PB_KIND_KICK || is_boris(KIND) ||
                                   KIND == PB_KIND_DRIFT);
-  static constexpr bool kVy = YP || KIND == PB_KIND_BORIS;
-  static constexpr bool kVz = KIND == PB_KIND_BORIS;
+  static constexpr bool kVy = YP || is_boris(KIND);
+  static constexpr bool kVz = is_boris(KIND);
 };
 
 // Push, cell transfer, stores, tallies and deposit for particles i, i+1
@@ -188,7 +188,7 @@ __device__ __forceinline__ void handle_pair(const LaunchArgs &a,
       __stcs(reinterpret_cast<double2 *>(X + i), make_double2(q.x0, q.x1));
       if (KIND != PB_KIND_DRIFT)
         __stcs(reinterpret_cast<double2 *>(VX + i), make_double2(q.vx0, q.vx1));
-      if (KIND == PB_KIND_BORIS) {
+      if (is_boris(KIND)) {
         __stcs(reinterpret_cast<double2 *>(VY + i), make_double2(q.vy0, q.vy1));
         __stcs(reinterpret_cast<double2 *>(VZ + i), make_double2(q.vz0, q.vz1));
       }
@@ -196,7 +196,7 @@ __device__ __forceinline__ void handle_pair(const LaunchArgs &a,
     } else if (v0) {
       X[i] = q.x0;
       if (KIND != PB_KIND_DRIFT) VX[i] = q.vx0;
-      if (KIND == PB_KIND_BORIS) {
+      if (is_boris(KIND)) {
         VY[i] = q.vy0;
         VZ[i] = q.vz0;
       }
@@ -326,8 +326,13 @@ __device__ __forceinline__ void run_any(const LaunchArgs &a, int isp, int64_t be
       else ldg_dispatch<PB_KIND_KICK, false, BC, PUSH>(a, isp, beg, end, win, t, dep);
       break;
     case PB_KIND_BORIS:
-      if (yp) ldg_dispatch<PB_KIND_BORIS, true, BC, PUSH>(a, isp, beg, end, win, t, dep);
-      else ldg_dispatch<PB_KIND_BORIS, false, BC, PUSH>(a, isp, beg, end, win, t, dep);
+      if (s.b_nodes) {
+        if (yp) ldg_dispatch<kKindBorisB, true, BC, PUSH>(a, isp, beg, end, win, t, dep);
+        else ldg_dispatch<kKindBorisB, false, BC, PUSH>(a, isp, beg, end, win, t, dep);
+      } else {
+        if (yp) ldg_dispatch<PB_KIND_BORIS, true, BC, PUSH>(a, isp, beg, end, win, t, dep);
+        else ldg_dispatch<PB_KIND_BORIS, false, BC, PUSH>(a, isp, beg, end, win, t, dep);
+      }
       break;
     case PB_KIND_DRIFT:
       if (yp) ldg_dispatch<PB_KIND_DRIFT, true, BC, PUSH>(a, isp, beg, end, win, t, dep);
@@ -629,7 +634,7 @@ __device__ __forceinline__ void quad_process(const LaunchArgs &a, int isp, int64
   if (nv == 4) {
     st4(s.x + i, q.x[0], q.x[1], q.x[2], q.x[3]);
     if (KIND != PB_KIND_DRIFT) st4(s.vx + i, q.vx[0], q.vx[1], q.vx[2], q.vx[3]);
-    if (KIND == PB_KIND_BORIS) {
+    if (is_boris(KIND)) {
       st4(s.vy + i, q.vy[0], q.vy[1], q.vy[2], q.vy[3]);
       st4(s.vz + i, q.vz[0], q.vz[1], q.vz[2], q.vz[3]);
     }
@@ -640,7 +645,7 @@ __device__ __forceinline__ void quad_process(const LaunchArgs &a, int isp, int64
       if (k < nv) {
         s.x[i + k] = q.x[k];
         if (KIND != PB_KIND_DRIFT) s.vx[i + k] = q.vx[k];
-        if (KIND == PB_KIND_BORIS) {
+        if (is_boris(KIND)) {
           s.vy[i + k] = q.vy[k];
           s.vz[i + k] = q.vz[k];
         }
@@ -743,7 +748,10 @@ __device__ __forceinline__ int64_t claim_chunk(const LaunchArgs &a) {
   return (int64_t)__shfl_sync(0xffffffffu, c, 0);
 }
 
-template <int BC, bool BORIS>
+// BMODE: 0 no Boris species, 1 uniform-B Boris, 2 Boris with B nodes
+// (pb_species.b_nodes) -- separate kernels, so the gathered-B path's extra
+// registers do not cost the uniform one.
+template <int BC, int BMODE>
 __device__ __forceinline__ void quad_dispatch(const LaunchArgs &a, int isp, int64_t beg,
                                               int64_t end, const Window &win, Tally &t) {
   const pb_species &s = a.sp[isp];
@@ -756,7 +764,9 @@ __device__ __forceinline__ void quad_dispatch(const LaunchArgs &a, int isp, int6
   } while (0)
   if (s.kind == PB_KIND_KICK) {
     if (yp) PB_Q(PB_KIND_KICK, true); else PB_Q(PB_KIND_KICK, false);
-  } else if (BORIS && s.kind == PB_KIND_BORIS) {
+  } else if (BMODE == 2 && s.kind == PB_KIND_BORIS && s.b_nodes) {
+    if (yp) PB_Q(kKindBorisB, true); else PB_Q(kKindBorisB, false);
+  } else if (BMODE != 0 && s.kind == PB_KIND_BORIS) {
     if (yp) PB_Q(PB_KIND_BORIS, true); else PB_Q(PB_KIND_BORIS, false);
   } else {
     if (yp) PB_Q(PB_KIND_DRIFT, true); else PB_Q(PB_KIND_DRIFT, false);
@@ -770,8 +780,10 @@ __device__ __forceinline__ void quad_dispatch(const LaunchArgs &a, int isp, int6
 
 constexpr int kWarpsPerBlock = kThreads / 32;
 
-template <int BC, bool BORIS>
-__global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
+// The gathered-B kernel (BMODE 2) runs at 2 blocks/SM: its per-particle B
+// gather + divisions would spill at the 3-block register budget.
+template <int BC, int BMODE>
+__global__ void __launch_bounds__(kThreads, BMODE == 2 ? 2 : PB_QUAD_MINBLOCKS)
     k_push_quad(const __grid_constant__ LaunchArgs a) {
   pdl_enter();
   mover_clock_start(a.st);
@@ -792,7 +804,7 @@ __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
         win.gC = win.gR + a.nc;
       }
     }
-    quad_dispatch<BC, BORIS>(a, isp, beg, end, win, t);
+    quad_dispatch<BC, BMODE>(a, isp, beg, end, win, t);
   }
   if (cur >= 0) flush_tally(a, a.id[cur], t, nullptr);
   if (lane_id() == 0) release_work_counter(a.st, (unsigned long long)gridDim.x * kWarpsPerBlock);
@@ -1296,10 +1308,11 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
   if (push && all_move) {
     // Chunk list: species by descending bytes/particle.
     int order[PB_MAX_SPECIES];
-    bool boris = false;
+    bool boris = false, bgather = false;
     for (int k = 0; k < a.nsp; ++k) {
       order[k] = k;
       boris |= a.sp[k].kind == PB_KIND_BORIS;
+      bgather |= a.sp[k].kind == PB_KIND_BORIS && a.sp[k].b_nodes != nullptr;
     }
     for (int i = 1; i < a.nsp; ++i)
       for (int j = i; j > 0 && bytes_per_particle(a.sp[order[j]], true) >
@@ -1364,8 +1377,10 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
                                                     : k_push_ring<PB_BC_ABSORBING>,
                                "k_push_ring", ring_smem_bytes(), a, stream);
     KernFn fn = bc == PB_BC_PERIODIC
-                    ? (boris ? k_push_quad<PB_BC_PERIODIC, true> : k_push_quad<PB_BC_PERIODIC, false>)
-                    : (boris ? k_push_quad<PB_BC_ABSORBING, true> : k_push_quad<PB_BC_ABSORBING, false>);
+                    ? (bgather ? k_push_quad<PB_BC_PERIODIC, 2>
+                               : boris ? k_push_quad<PB_BC_PERIODIC, 1> : k_push_quad<PB_BC_PERIODIC, 0>)
+                    : (bgather ? k_push_quad<PB_BC_ABSORBING, 2>
+                               : boris ? k_push_quad<PB_BC_ABSORBING, 1> : k_push_quad<PB_BC_ABSORBING, 0>);
     return launch_persistent(fn, "k_push_quad", 0, a, stream);
   }
   // Deposit-only launches and launches with inactive depositing species:

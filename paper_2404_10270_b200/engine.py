@@ -81,6 +81,22 @@ def boris_coefficients(sp, consts, b_field) -> tuple:
     return t, s
 
 
+def b_field_nodes(config):
+    """Node B profile of a config with `b_grad_t_per_m`, as the (nc+1, 4)
+    f64 array pb_species.b_nodes reads (x, y, z, 0 per node, tesla):
+    B(X_j) = b_field_t + g * (X_j - L/2), X_j = j * dx.  None for a uniform
+    (or absent) field, which keeps the constant boris_t / boris_s."""
+    g = getattr(config, "b_grad_t_per_m", None)
+    if g is None or config.b_field_t is None:
+        return None
+    nc, dx = int(config.grid.nc), float(config.grid.dx_m)
+    xj = np.arange(nc + 1, dtype=np.float64) * dx - 0.5 * float(config.grid.length_m)
+    nodes = np.zeros((nc + 1, 4), dtype=np.float64)
+    for k in range(3):
+        nodes[:, k] = float(config.b_field_t[k]) + float(g[k]) * xj
+    return nodes
+
+
 def species_kind(sp, b_field) -> int:
     if not sp.active_mover:
         return _lib.PB_KIND_INACTIVE
@@ -166,6 +182,11 @@ class Engine:
         self.stream = torch.cuda.Stream(self.device)
         self._side = torch.cuda.Stream(self.device)  # overlapped density epilogue
         self._epi_prev = None  # event: last side-stream epilogue (eager overlap)
+        nodes = b_field_nodes(config)
+        self.b_nodes = None  # (nc+1, 4) device B profile, or None (uniform B)
+        if nodes is not None:
+            with torch.cuda.stream(self.stream):
+                self.b_nodes = torch.from_numpy(nodes).to(self.device)
         self.sp = []
         self.coef_dep = []
         ndep = 0
@@ -179,6 +200,7 @@ class Engine:
                 self.coef_dep.append(spd.charge_c * macro_weight(config, isp) / self.grid.dx_m)
             kick = velocity_kick_coef(spd, config.consts, self.grid.dx_m) if spd.charged else 0.0
             boris = boris_coefficients(spd, config.consts, self.b_field) if kind == _lib.PB_KIND_BORIS else None
+            boris_f = spd.charge_c * config.consts.dt_s / (2.0 * spd.mass_kg)
             # The mover reads a 1-byte cell offset instead of the 4-byte index
             # for charged species dense enough that a 2048-particle chunk spans
             # well under 127 cells (pb_species.cell8).
@@ -191,6 +213,7 @@ class Engine:
             with torch.cuda.stream(self.stream):
                 self.sp.append(DeviceSpecies(spd, nloc, self.device, kind=kind, deposit=dep,
                                              kick_coef=kick, boris=boris, absorbing=self.absorbing,
+                                             b_nodes=self.b_nodes, boris_f=boris_f,
                                              cap=self._species_cap(isp, nloc), cell8=cell8))
         self.ndep = ndep
         self._coef_c = (ctypes.c_double * max(ndep, 1))(*self.coef_dep)
@@ -309,6 +332,27 @@ class Engine:
             self.bins.zero_()
             _lib.check(self.lib.pb_deposit_only(arr, n, self.nc, self.bins.data_ptr(),
                                                 self.status.data_ptr(), self._sh()), "pb_deposit_only")
+
+    def set_b_field(self, nodes):
+        """Replace the magnetic field by an arbitrary node profile: `nodes`
+        is (nc+1, 3) tesla (host array or tensor), gathered per Boris
+        particle with the one-sided linear form (pb_species.b_nodes).  The
+        run must have been configured with a B field (b_field_t), which is
+        what makes the charged species Boris species."""
+        if self.b_field is None:
+            raise ConfigError("set_b_field needs a config with b_field_t (Boris species)")
+        b = torch.as_tensor(nodes, dtype=torch.float64)
+        if tuple(b.shape) != (self.nc + 1, 3):
+            raise ValueError(f"B nodes must have shape ({self.nc + 1}, 3), got {tuple(b.shape)}")
+        with torch.cuda.stream(self.stream):
+            dev = torch.zeros((self.nc + 1, 4), dtype=torch.float64, device=self.device)
+            dev[:, :3].copy_(b.to(self.device, non_blocking=False))
+        self.b_nodes = dev
+        for s in self.sp:
+            s.b_nodes = dev
+        self._arr = None  # species structs carry the pointer: rebuild them
+        self.graphs = {}
+        self._publish()
 
     def upload(self, flats: list):
         """Replace the particle state with host arrays (engine flat layout)."""

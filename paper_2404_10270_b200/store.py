@@ -28,7 +28,7 @@ class DeviceSpecies:
 
     def __init__(self, sp, n: int, device, *, kind: int, deposit: int,
                  kick_coef: float = 0.0, boris=None, absorbing: bool = False, cap: int = None,
-                 cell8: bool = False):
+                 cell8: bool = False, b_nodes=None, boris_f: float = 0.0):
         self.sp = sp
         self.name = sp.name
         self.device = device
@@ -38,6 +38,10 @@ class DeviceSpecies:
         self.fnstep = float(sp.nstep)
         self.kick_coef = float(kick_coef)
         self.boris = boris  # (t[3], s[3]) or None
+        # spatially varying B: (nc+1, 4) f64 device nodes shared by the
+        # engine's Boris species, and f = q dt / (2 m) (pb_species.b_nodes)
+        self.b_nodes = b_nodes
+        self.boris_f = float(boris_f)
         self.absorbing = absorbing
         self.has_yp = bool(sp.track_transverse)
         # cap > n leaves room for collision newborns (canonical mode).
@@ -97,6 +101,9 @@ class DeviceSpecies:
             for k in range(3):
                 s.boris_t[k] = t[k]
                 s.boris_s[k] = sv[k]
+        if self.b_nodes is not None and self.kind == _lib.PB_KIND_BORIS:
+            s.b_nodes = self.b_nodes.data_ptr()
+            s.boris_f = self.boris_f
         if self.cell8 is not None:
             s.cell8 = self.cell8.data_ptr()
             s.chunk_base = self.chunk_base.data_ptr()

@@ -408,6 +408,46 @@ def gen_desk_criterion01(picmc):
     print("desk criterion 01:", steps, "steps", m.diagnostics[-1])
 
 
+def gen_c1(picmc):
+    """BASELINE config 1 (configs/c1_desk_ppc100.toml: the desk ionisation
+    test at nc = 1000, ppc0 = 100, 100 steps, collisions on) run by the
+    reference's own run_simulation.  Records every step's diagnostics row,
+    the SHA-256 of every step's rho, the last rho and SHA-256 digests of the
+    final stores in slot order (300K particles: digests keep the file small
+    while the comparison stays bit-exact)."""
+    import hashlib
+    from dataclasses import replace
+
+    from picmc.config import load_config
+    from picmc.decomposition import merge_stores
+    from picmc.harness import run_simulation
+
+    root = os.path.dirname(os.path.dirname(HERE))
+    cfg = load_config(os.path.join(root, "configs", "c1_desk_ppc100.toml"))
+    cfg = replace(cfg, out_dir=None)
+    box = {"rho_sha": []}
+
+    def probe(step, st):
+        box["rho_sha"].append(hashlib.sha256(np.ascontiguousarray(st["rho"]).tobytes()).hexdigest())
+        if step == cfg.n_steps:
+            box["rho"] = st["rho"].copy()
+            box["final"] = merge_stores(st["stores"], st["partition"], cfg.grid)
+
+    m = run_simulation(cfg, on_step=probe)
+    flat = flatten_store(box["final"])
+    digests = {k: hashlib.sha256(np.ascontiguousarray(v).tobytes()).hexdigest() for k, v in flat.items()}
+    names = [s.name for s in cfg.species]
+    np.savez_compressed(
+        os.path.join(HERE, "run_c1_desk_ppc100.npz"),
+        steps=np.array(cfg.n_steps),
+        totals=np.array([[row[f"total_{n}"] for n in names] for row in m.diagnostics]),
+        tallies=np.array([[row["elastic"], row["excitation"], row["ionization"], row["suppressed"]]
+                          for row in m.diagnostics]),
+        rho_sha=np.array(json.dumps(box["rho_sha"])),
+        rho_last=box["rho"], digests=np.array(json.dumps(digests, sort_keys=True)))
+    print("config 1:", cfg.n_steps, "steps", m.diagnostics[-1])
+
+
 def raw_store(store, prefix):
     """Every array of a store, free space included (slot layout pinned)."""
     out = {}
@@ -537,6 +577,9 @@ def gen_fields_api(picmc):
 
 if __name__ == "__main__":
     ref = import_reference()
+    if sys.argv[1:] == ["c1"]:
+        gen_c1(ref)
+        sys.exit(0)
     gen_backend(ref)
     gen_resort(ref)
     gen_rng(ref)
@@ -549,6 +592,7 @@ if __name__ == "__main__":
     gen_collision_runs(ref)
     gen_collision_kats(ref)
     gen_desk_criterion01(ref)
+    gen_c1(ref)
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -146,14 +146,20 @@ def _ext_config(**kw):
     return RunConfig(**base)
 
 
-@pytest.mark.parametrize("boundary", ["periodic", "absorbing"])
+@pytest.mark.parametrize("boundary", ["periodic", "absorbing", "boris_gradb"])
 def test_canonical_extensions_match_oracle(cuda, boundary):
-    """Absorbing walls + collisions + nstep>1 + Dirichlet field solve: no
-    reference behaviour, so the oracle restatement is the bar (bit-exact)."""
+    """Absorbing walls + collisions + nstep>1 + Dirichlet field solve, and
+    the Boris push in a spatially varying B: no reference behaviour, so the
+    oracle restatement is the bar (bit-exact)."""
     from oracle import oracle
 
-    cfg = _ext_config(particle_boundary=boundary,
-                      boundary="dirichlet" if boundary == "absorbing" else "periodic")
+    if boundary == "boris_gradb":
+        # B gathered per particle from nodes (pb_species.b_nodes), strong
+        # enough (|t| ~ 0.01-0.05 for electrons) that the rotation matters
+        cfg = _ext_config(b_field_t=(0.4, -0.3, 2.0), b_grad_t_per_m=(150.0, 40.0, -900.0))
+    else:
+        cfg = _ext_config(particle_boundary=boundary,
+                          boundary="dirichlet" if boundary == "absorbing" else "periodic")
     h = oracle.run_canonical(cfg, host_species(cfg))
     m, d = _run(cfg)
     names = [s.name for s in cfg.species]

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for name in names:
         assert hasattr(lib, name), name
     assert set(names) == set(_lib.exported_names())
-    assert lib.pb_abi_version() == _lib.ABI_VERSION == 2
+    assert lib.pb_abi_version() == _lib.ABI_VERSION == 3
 
 
 def test_library_argument_errors_without_gpu():
@@ -80,7 +80,7 @@ def test_configs_load_and_validate():
     from paper_2404_10270_b200 import load_config
 
     names = sorted(f for f in os.listdir(os.path.join(ROOT, "configs")) if f.endswith(".toml"))
-    assert len(names) == 7
+    assert len(names) == 8
     cfgs = {n: load_config(os.path.join(ROOT, "configs", n)) for n in names}
     for n in ("desk.toml", "c1_desk_ppc100.toml"):
         assert cfgs[n].canonical() and cfgs[n].collisions.rates.rate_ionization_m3s == 2.5e-11
@@ -89,7 +89,9 @@ def test_configs_load_and_validate():
     c3 = cfgs["c3_sheath_absorbing.toml"]
     assert c3.particle_boundary == "absorbing" and c3.boundary == "dirichlet" and c3.sort_every == 50
     c4 = cfgs["c4_sol_boris.toml"]
-    assert c4.b_field_t == (0.2, 0.0, 2.0)
+    assert c4.b_field_t == (0.2, 0.0, 2.0) and c4.b_grad_t_per_m is None
+    c4b = cfgs["c4b_sol_gradb.toml"]
+    assert c4b.b_field_t == (0.2, 0.0, 2.0) and c4b.b_grad_t_per_m == (0.0, 0.0, -1.0)
     c2 = cfgs["c2_ionization_100k.toml"]
     assert c2.grid.nc * c2.ppc0 * len(c2.species) == 30_000_000
 
@@ -242,3 +244,44 @@ def test_peer_status_maps_to_engine_error():
         pytest.skip("library not built")
     with pytest.raises(EngineError):
         _lib.check(_lib.PB_ERR_PEER, "peer")
+
+
+def test_b_profile_config_and_nodes():
+    """b_grad_t_per_m: validation, and the engine's node profile equals the
+    oracle's restatement bit for bit (B(X_j) = B0 + g (X_j - L/2))."""
+    from dataclasses import replace
+
+    from oracle import oracle
+    from paper_2404_10270_b200 import ConfigError, load_config
+    from paper_2404_10270_b200.engine import b_field_nodes
+
+    cfg = load_config(os.path.join(ROOT, "configs", "c4b_sol_gradb.toml"))
+    nodes = b_field_nodes(cfg)
+    assert nodes.shape == (cfg.grid.nc + 1, 4) and not nodes[:, 3].any()
+    assert np.array_equal(nodes.view(np.uint64), oracle.b_nodes(cfg).view(np.uint64))
+    assert abs(nodes[0, 2] - 2.5) < 1e-12 and abs(nodes[-1, 2] - 1.5) < 1e-12
+    assert b_field_nodes(replace(cfg, b_grad_t_per_m=None)) is None
+    with pytest.raises(ConfigError, match="b_grad_t_per_m needs b_field_t"):
+        replace(cfg, b_field_t=None).validate()
+    with pytest.raises(ConfigError, match="three components"):
+        replace(cfg, b_grad_t_per_m=(1.0, 2.0)).validate()
+
+
+def test_errors_are_the_reference_classes_when_importable(tmp_path):
+    """With the reference package on the path, the engine raises the
+    reference's own exception classes (callers' `except picmc.errors.X`
+    keep working); without it, the same hierarchy is declared locally."""
+    import subprocess
+    import sys
+
+    from paper_2404_10270_b200 import errors
+
+    assert issubclass(errors.CflViolation, errors.EngineError)
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "picmc")):
+        pytest.skip("reference not installed (scripts/install_reference.sh)")
+    code = ("import picmc.errors as r, paper_2404_10270_b200.errors as e; "
+            "assert e.SHARED_WITH_REFERENCE and e.CflViolation is r.CflViolation "
+            "and e.EngineError is r.EngineError and e.ConfigError is r.ConfigError")
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([ref, ROOT]), PICMC_BACKEND="pure")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=str(tmp_path))
