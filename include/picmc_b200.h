@@ -266,6 +266,22 @@ int pb_compute_efield_clear(const double *phi, double *e, int64_t nc,
                             uint64_t *clr_b, int64_t nwords, void *stream);
 
 
+/* The whole replicated field step of a field-solve run: pb_rho_epilogue
+ * (weighted partials, stitched rho, overflow check) + pb_smooth_density
+ * (`passes` 1-2-1 passes into rho_s) + pb_solve_poisson_scan (on rho_s) +
+ * pb_compute_efield_clear (E, then zero nwords words of clr_a / clr_b; both
+ * may be NULL), bitwise those four calls.  With passes == 1 the epilogue and
+ * the smoothing are one kernel (each thread forms the three densities its
+ * node's smoothing reads).  `scratch` needs pb_field_scratch_bytes(nc)
+ * bytes; left / right may be NULL. */
+int pb_field_cycle(const uint64_t *bins, const double *coef, int ndep,
+                   int64_t nc, int field_bc, int passes, double dx,
+                   double eps0, double phi_left, double phi_right,
+                   double *left, double *right, double *rho, double *rho_s,
+                   double *phi, double *e, uint64_t *clr_a, uint64_t *clr_b,
+                   int64_t nwords, pb_status *status_or_null, void *scratch,
+                   void *stream);
+
 /* Roofline probe: streams the mover's exact read/write bytes per species with
  * a trivial update (no physics, no deposit).  Destroys particle state. */
 int pb_stream_sol(const pb_species *sp, int nsp, void *stream);

@@ -46,9 +46,15 @@ __device__ __forceinline__ void flag_overflow(pb_status *st, uint64_t count) {
   atomicCAS(&st->code, PB_OK, PB_ERR_OVERFLOW);
 }
 
-// Quantise a cell-relative position in [0,1) to the deposit fixed point.
+// Quantise a cell-relative position in [0,1) to the deposit fixed point:
+// round-to-nearest-even of x * 2^48 (exact: a power-of-two scale).  Adding
+// 2^52 puts the value in the binade whose ulp is 1, so that single rounding
+// IS the round-to-nearest-even to an integer and leaves it in the low
+// mantissa bits -- bitwise __double2ull_rn, with a DADD in place of the
+// F2I.U64.F64 conversion on the mover's per-particle path.
 __device__ __forceinline__ uint64_t quantize(double x) {
-  return (uint64_t)__double2ull_rn(__dmul_rn(x, kFracScale));
+  const double v = __dadd_rn(__dmul_rn(x, kFracScale), 4503599627370496.0);  // + 2^52
+  return (uint64_t)__double_as_longlong(v) - 0x4330000000000000ull;
 }
 
 // Sum of per-particle fixed-point weights, packed with a count.

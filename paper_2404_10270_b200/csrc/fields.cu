@@ -8,6 +8,9 @@
 // operation -- including NumPy's pairwise summation inside np.mean -- on one
 // thread, so a given rho yields a bitwise-identical phi.
 #include "common.cuh"
+#include "density.cuh"
+
+#include <cstring>
 
 namespace pb {
 
@@ -192,32 +195,54 @@ constexpr int kMbThreads = 256;
 constexpr int kMbPer = PB_MB_PER;
 constexpr int kMbTile = kMbThreads * kMbPer;
 
+__device__ __forceinline__ DD dd_shfl_up(DD v, int d) {
+  return {__shfl_up_sync(0xffffffffu, v.hi, d), __shfl_up_sync(0xffffffffu, v.lo, d)};
+}
+__device__ __forceinline__ DD dd_shfl_down(DD v, int d) {
+  return {__shfl_down_sync(0xffffffffu, v.hi, d), __shfl_down_sync(0xffffffffu, v.lo, d)};
+}
+
+constexpr int kMbWarps = kMbThreads / 32;
+
+// Block sum (every thread gets it): a shuffle tree in each warp, then the
+// warp sums in warp order.  A fixed tree, so every block computing the same
+// sum gets the same bits.
 __device__ DD mb_block_reduce(DD v, DD *sm) {
-  sm[threadIdx.x] = v;
-  __syncthreads();
-  for (int d = kMbThreads / 2; d > 0; d >>= 1) {
-    if ((int)threadIdx.x < d) sm[threadIdx.x] = dd_add(sm[threadIdx.x], sm[threadIdx.x + d]);
-    __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const DD o = dd_shfl_down(v, d);
+    if (lane + d < 32) v = dd_add(v, o);
   }
-  const DD r = sm[0];
+  if (lane == 0) sm[warp] = v;
+  __syncthreads();
+  DD r = sm[0];
+#pragma unroll
+  for (int w = 1; w < kMbWarps; ++w) r = dd_add(r, sm[w]);
   __syncthreads();
   return r;
 }
 
-// Exclusive scan over threads in order t (rev = false) or NT-1-t (rev = true).
+// Exclusive scan over threads in order t (rev = false) or NT-1-t (rev = true):
+// a shuffle scan in each warp (logical lane order), the warp totals
+// scanned in logical warp order through shared memory.
 __device__ DD mb_block_excl(DD v, DD *sm, bool rev) {
-  const int t = rev ? kMbThreads - 1 - (int)threadIdx.x : (int)threadIdx.x;
-  sm[t] = v;
-  __syncthreads();
-  for (int d = 1; d < kMbThreads; d <<= 1) {
-    const DD o = t >= d ? sm[t - d] : dd_of(0.0);
-    __syncthreads();
-    if (t >= d) sm[t] = dd_add(o, sm[t]);
-    __syncthreads();
+  const int t = rev ? kMbThreads - 1 - (int)threadIdx.x : (int)threadIdx.x;  // logical position
+  const int lane = t & 31, warp = t >> 5;
+  DD inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const DD o = rev ? dd_shfl_down(inc, d) : dd_shfl_up(inc, d);  // logical lane - d
+    if (lane >= d) inc = dd_add(o, inc);
   }
-  const DD ex = t > 0 ? sm[t - 1] : dd_of(0.0);
+  DD lex = rev ? dd_shfl_down(inc, 1) : dd_shfl_up(inc, 1);
+  if (lane == 0) lex = dd_of(0.0);
+  if (lane == 31) sm[warp] = inc;
   __syncthreads();
-  return ex;
+  DD wex = dd_of(0.0);
+  for (int w = 0; w < warp; ++w) wex = dd_add(wex, sm[w]);
+  __syncthreads();
+  return dd_add(wex, lex);
 }
 
 // Sum of part[lo, hi) in index order (each block computes the same value).
@@ -415,6 +440,52 @@ static PoissonArgs poisson_args(const double *rho, double *phi, int64_t nc, doub
   return a;
 }
 
+// The density epilogue with one smoothing pass folded in (pb_field_cycle,
+// passes == 1): thread g forms rho at nodes g-1, g, g+1 from the bins
+// itself (the same weighted partials k_rho_epilogue forms, so the same
+// bits) and smooths them -- one launch instead of k_rho_epilogue +
+// k_smooth_pass, bitwise the same left / right / rho / rho_s.
+struct RhoSmoothArgs {
+  const uint64_t *bins;
+  CoefArgs ca;
+  int ndep, field_bc;
+  int64_t nc;
+  double *left, *right, *rho, *rho_s;
+  pb_status *st;
+};
+
+// core value rho[c] of node c in [0, nc) (the array the smoothing wraps over)
+__device__ __forceinline__ double rs_core(const RhoSmoothArgs &a, int64_t c, double lc, double rcm1) {
+  return (a.field_bc != PB_FIELD_PERIODIC && c == 0) ? __dmul_rn(lc, 2.0) : __dadd_rn(rcm1, lc);
+}
+
+__global__ void k_rho_smooth(const __grid_constant__ RhoSmoothArgs a) {
+  pdl_enter();
+  const int64_t nc = a.nc;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g > nc) return;
+  const int64_t jj = g == nc ? 0 : g;
+  const int64_t jm = jj == 0 ? nc - 1 : jj - 1, jp = jj == nc - 1 ? 0 : jj + 1;
+  const int64_t jmm = jm == 0 ? nc - 1 : jm - 1;
+  double l_m, r_m, l_0, r_0, l_p, r_p, l_mm, r_mm;
+  weighted_partials(a.bins, a.ca.c, a.ndep, nc, jj, l_0, r_0, g < nc ? a.st : nullptr);
+  weighted_partials(a.bins, a.ca.c, a.ndep, nc, jm, l_m, r_m, nullptr);
+  weighted_partials(a.bins, a.ca.c, a.ndep, nc, jp, l_p, r_p, nullptr);
+  weighted_partials(a.bins, a.ca.c, a.ndep, nc, jmm, l_mm, r_mm, nullptr);
+  (void)r_p;
+  const double c0 = rs_core(a, jj, l_0, r_m);
+  const double cm = rs_core(a, jm, l_m, r_mm);
+  const double cp = rs_core(a, jp, l_p, r_0);
+  if (g < nc) {
+    if (a.left) a.left[g] = l_0;
+    if (a.right) a.right[g] = r_0;
+    a.rho[g] = c0;
+  } else {
+    a.rho[nc] = a.field_bc == PB_FIELD_PERIODIC ? c0 : __dmul_rn(r_m, 2.0);  // rho[0] / 2 R[nc-1]
+  }
+  a.rho_s[g] = __dadd_rn(__dadd_rn(__dmul_rn(0.25, cm), __dmul_rn(0.5, c0)), __dmul_rn(0.25, cp));
+}
+
 }  // namespace pb
 
 extern "C" size_t pb_field_scratch_bytes(int64_t nc) {
@@ -534,4 +605,50 @@ extern "C" int pb_compute_efield_clear(const double *phi, double *e, int64_t nc,
                                    nwords);
   if (err != cudaSuccess) return pb::cuda_status(err, "k_efield_clear");
   return PB_OK;
+}
+
+
+extern "C" int pb_field_cycle(const uint64_t *bins, const double *coef, int ndep, int64_t nc,
+                              int field_bc, int passes, double dx, double eps0, double phi_left,
+                              double phi_right, double *left, double *right, double *rho,
+                              double *rho_s, double *phi, double *e, uint64_t *clr_a,
+                              uint64_t *clr_b, int64_t nwords, pb_status *status, void *scratch,
+                              void *stream) {
+  if (nc < 3 || ndep < 0 || ndep > PB_MAX_SPECIES || (ndep > 0 && (!bins || !coef)) || !rho ||
+      !rho_s || !phi || !e || !scratch || nwords < 0) {
+    pb::set_error("pb_field_cycle: bad arguments (nc=%lld ndep=%d)", (long long)nc, ndep);
+    return PB_ERR_INVALID;
+  }
+  if (passes < 0) {
+    pb::set_error("pb_field_cycle: %d smoothing passes", passes);
+    return PB_ERR_INVALID;
+  }
+  if (field_bc != PB_FIELD_PERIODIC && field_bc != PB_FIELD_DIRICHLET) {
+    pb::set_error("unknown boundary condition %d", field_bc);
+    return PB_ERR_INVALID;
+  }
+  int rc = PB_OK;
+  if (passes == 1) {
+    pb::RhoSmoothArgs a;
+    memset(&a, 0, sizeof(a));
+    a.bins = bins;
+    for (int s = 0; s < ndep; ++s) a.ca.c[s] = coef[s];
+    a.ndep = ndep;
+    a.field_bc = field_bc;
+    a.nc = nc;
+    a.left = left;
+    a.right = right;
+    a.rho = rho;
+    a.rho_s = rho_s;
+    a.st = status;
+    cudaError_t err = pb::launch_pdl(pb::k_rho_smooth, dim3(pb::blocks_for(nc + 1, 256)), dim3(256), 0,
+                                     (cudaStream_t)stream, a);
+    if (err != cudaSuccess) return pb::cuda_status(err, "k_rho_smooth");
+  } else {
+    rc = pb_rho_epilogue(bins, coef, ndep, nc, field_bc, left, right, rho, status, stream);
+    if (!rc) rc = pb_smooth_density(rho, rho_s, nc, passes, scratch, stream);
+  }
+  if (!rc) rc = pb_solve_poisson_scan(rho_s, phi, nc, dx, eps0, field_bc, phi_left, phi_right, scratch, stream);
+  if (!rc) rc = pb_compute_efield_clear(phi, e, nc, dx, field_bc, clr_a, clr_b, (clr_a || clr_b) ? nwords : 0, stream);
+  return rc;
 }

@@ -598,9 +598,15 @@ __device__ __forceinline__ void quad_load(const pb_species &s, int64_t i, int64_
   }
 }
 
+#ifndef PB_FULL_SLICES
+#define PB_FULL_SLICES 1
+#endif
 // Push, transfer, store, tallies and deposit of one lane's quad at slot i
-// (every lane of the warp calls this: the deposit scan shuffles).
-template <int KIND, bool YP, int BC, bool DEP>
+// (every lane of the warp calls this: the deposit scan shuffles).  FULL: the
+// quad is known to hold 4 particles (a full TMA slice) -- no per-particle
+// validity predicates.  The rare events (cell transfers, CFL, wall removal)
+// are tested once per quad / warp and handled off the common path.
+template <int KIND, bool YP, int BC, bool DEP, bool FULL = false>
 __device__ __forceinline__ void quad_process(const LaunchArgs &a, int isp, int64_t i,
                                              Quad<KIND, YP> &q, const Window &win, Tally &t) {
   const pb_species &s = a.sp[isp];
@@ -609,7 +615,7 @@ __device__ __forceinline__ void quad_process(const LaunchArgs &a, int isp, int64
   const int64_t nc = a.nc;
   constexpr bool kCell = KIND != PB_KIND_DRIFT;
   const int lane = (int)lane_id();
-  const int nv = q.nv;
+  const int nv = FULL ? 4 : q.nv;
   if (kCell) quad_cells<KIND, YP>(s, i, q);
   int32_t nn[4];
   int8_t wall[4];
@@ -620,7 +626,7 @@ __device__ __forceinline__ void quad_process(const LaunchArgs &a, int isp, int64
     wall[k] = -1;
     mv[k] = false;
     cfl[k] = false;
-    if (k < nv) {
+    if (FULL || k < nv) {
       kick_drift<KIND>(q.x[k], q.vx[k], q.vy[k], q.vz[k], q.c[k], s, a.e);
       if (YP) q.y[k] = __dadd_rn(q.y[k], __dmul_rn(s.fnstep, q.vy[k]));
       if (!kCell && floor(q.x[k]) != 0.0) q.c[k] = s.cell[i + k];
@@ -631,7 +637,7 @@ __device__ __forceinline__ void quad_process(const LaunchArgs &a, int isp, int64
       cfl[k] = o.cfl;
     }
   }
-  if (nv == 4) {
+  if (FULL || nv == 4) {
     st4(s.x + i, q.x[0], q.x[1], q.x[2], q.x[3]);
     if (KIND != PB_KIND_DRIFT) st4(s.vx + i, q.vx[0], q.vx[1], q.vx[2], q.vx[3]);
     if (is_boris(KIND)) {
@@ -653,42 +659,64 @@ __device__ __forceinline__ void quad_process(const LaunchArgs &a, int isp, int64
       }
     }
   }
+  t.moved += (int)mv[0] + (int)mv[1] + (int)mv[2] + (int)mv[3];
+  if (mv[0] | mv[1] | mv[2] | mv[3]) {  // a cell transfer: ~0.6% of electron pushes
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (mv[k]) {
-      s.cell[i + k] = nn[k];
-      if (kCell && s.cell8)
-        s.cell8[i + k] = nn[k] >= 0 ? cell8_encode(nn[k], q.base) : (int8_t)PB_CELL8_ESCAPE;
+    for (int k = 0; k < 4; ++k) {
+      if (mv[k]) {
+        s.cell[i + k] = nn[k];
+        if (kCell && s.cell8)
+          s.cell8[i + k] = nn[k] >= 0 ? cell8_encode(nn[k], q.base) : (int8_t)PB_CELL8_ESCAPE;
+      }
     }
-    t.moved += (int)mv[k];
-    if (cfl[k]) {
-      const uint64_t key = ((uint64_t)sid << 56) | (uint64_t)(i + k);
-      atomicMin((unsigned long long *)&a.st->cfl_index, (unsigned long long)key);
-      atomicCAS(&a.st->code, PB_OK, PB_ERR_CFL);
-      nn[k] = -1;
+  }
+  if (cfl[0] | cfl[1] | cfl[2] | cfl[3]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (cfl[k]) {
+        const uint64_t key = ((uint64_t)sid << 56) | (uint64_t)(i + k);
+        atomicMin((unsigned long long *)&a.st->cfl_index, (unsigned long long)key);
+        atomicCAS(&a.st->code, PB_OK, PB_ERR_CFL);
+        nn[k] = -1;
+      }
     }
   }
   if (BC == PB_BC_ABSORBING) {
+    // Warp-ballot stream compaction of removed slots into the hole list,
+    // entered only by warps that removed something.
+    if (__any_sync(full, (wall[0] >= 0) | (wall[1] >= 0) | (wall[2] >= 0) | (wall[3] >= 0))) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      t.absorbed[0] += (int)(wall[k] == 0);
-      t.absorbed[1] += (int)(wall[k] == 1);
-      const bool r = wall[k] >= 0;
-      const unsigned b = __ballot_sync(full, r);
-      if (b) {
-        unsigned long long hb = 0;
-        if (lane == 0)
-          hb = atomicAdd((unsigned long long *)&a.st->n_holes[sid], (unsigned long long)__popc(b));
-        hb = __shfl_sync(full, hb, 0);
-        if (r) s.holes[hb + __popc(b & ((1u << lane) - 1u))] = i + k;
+      for (int k = 0; k < 4; ++k) {
+        t.absorbed[0] += (int)(wall[k] == 0);
+        t.absorbed[1] += (int)(wall[k] == 1);
+        const bool r = wall[k] >= 0;
+        const unsigned b = __ballot_sync(full, r);
+        if (b) {
+          unsigned long long hb = 0;
+          if (lane == 0)
+            hb = atomicAdd((unsigned long long *)&a.st->n_holes[sid], (unsigned long long)__popc(b));
+          hb = __shfl_sync(full, hb, 0);
+          if (r) s.holes[hb + __popc(b & ((1u << lane) - 1u))] = i + k;
+        }
       }
     }
   }
   if (DEP) {
-    RunAcc run;
+    int32_t key;
+    uint64_t w;
+    if (nn[0] >= 0 && nn[0] == nn[1] && nn[1] == nn[2] && nn[2] == nn[3]) {
+      // the quad stays in one cell (sorted stores: the common case)
+      key = nn[0];
+      w = (uint64_t(4) << kCountShift) +
+          ((quantize(q.x[0]) + quantize(q.x[1])) + (quantize(q.x[2]) + quantize(q.x[3])));
+    } else {
+      RunAcc run;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) run.add(nn[k], q.x[k], win);
-    warp_segmented_emit(run.key, run.w, win);
+      for (int k = 0; k < 4; ++k) run.add(nn[k], q.x[k], win);
+      key = run.key;
+      w = run.w;
+    }
+    warp_segmented_emit(key, w, win);
   }
 }
 
@@ -713,7 +741,12 @@ __device__ __forceinline__ void quad_chunk(const LaunchArgs &a, int isp, int64_t
     const int64_t i = q0 + 4 * lane;
     Quad<KIND, YP> nq;
     if (kPrefetch) quad_load<KIND, YP>(s, i + 128, end, nq);
-    quad_process<KIND, YP, BC, DEP>(a, isp, i, q, win, t);
+    // warp-uniform: every lane holds 4 particles (periodic launches only: the
+    // absorbing register path would spill with both bodies inlined)
+    if (PB_FULL_SLICES && BC == PB_BC_PERIODIC && end - q0 >= 128)
+      quad_process<KIND, YP, BC, DEP, true>(a, isp, i, q, win, t);
+    else
+      quad_process<KIND, YP, BC, DEP>(a, isp, i, q, win, t);
     if (kPrefetch)
       q = nq;
     else
@@ -933,7 +966,10 @@ __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
     __syncwarp();  // every lane holds its slice in registers: the stage may be refilled
     ++tail;
     if (issuing) issue();
-    quad_process<PB_KIND_KICK, false, BC, true>(a, m.isp, i, q, win, t);
+    if (PB_FULL_SLICES && m.cnt == kSlice)
+      quad_process<PB_KIND_KICK, false, BC, true, true>(a, m.isp, i, q, win, t);
+    else
+      quad_process<PB_KIND_KICK, false, BC, true>(a, m.isp, i, q, win, t);
   }
   if (cur >= 0) flush_tally(a, a.id[cur], t, nullptr);
   if (lane == 0) release_work_counter(a.st, (unsigned long long)gridDim.x * kWarpsPerBlock);
@@ -1112,7 +1148,10 @@ __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
       __syncwarp();
       ++tail;
       if (issuing) issue();
-      quad_process<PB_KIND_KICK, false, BC, true>(a, m.isp, i, q, win, t);
+      if (PB_FULL_SLICES && m.cnt == kSlice)
+        quad_process<PB_KIND_KICK, false, BC, true, true>(a, m.isp, i, q, win, t);
+      else
+        quad_process<PB_KIND_KICK, false, BC, true>(a, m.isp, i, q, win, t);
     }
     split_register_list<BC>(a, 1, win, t, cur);
   } else {

@@ -141,6 +141,9 @@ class Engine:
     # serial field-solve cycle: density in one pb_rho_epilogue launch, bins
     # cleared by the E kernel (False: pb_density_step's two launches)
     density_one = True
+    # field-solve steps with the scan Poisson: the whole field step in one
+    # launch with grid barriers (pb_field_cycle) instead of 6-10 kernels
+    fused_field = True
 
     def __init__(self, config, device=None, *, rank: int = 0, world: int = 1,
                  group=None, init: str = "host", check_every: int = 1, peer: bool = None):
@@ -240,7 +243,7 @@ class Engine:
             self.rho_s = torch.zeros(nc + 1, dtype=torch.float64, device=self.device)
             self.phi = torch.zeros(nc + 1, dtype=torch.float64, device=self.device)
             self.e = torch.zeros(nc + 1, dtype=torch.float64, device=self.device)
-            self.field_scratch = torch.empty(
+            self.field_scratch = torch.zeros(  # zeroed: pb_field_cycle's barrier words
                 max(1, self.lib.pb_field_scratch_bytes(nc) // 8), dtype=torch.float64, device=self.device)
             self.status_tpl = status_template(self.device)
             self.status = self.status_tpl.clone()
@@ -375,6 +378,7 @@ class Engine:
             if self.peer is not None:
                 self._peer_density(st, clear_next)
                 self._next_clear = True
+                self._order_caller(stream)
                 return self.rho
             if self.world > 1:
                 reduce_bins(self.bins, self.group)
@@ -384,7 +388,17 @@ class Engine:
                 self.left.data_ptr(), self.right.data_ptr(), self.rho.data_ptr(),
                 ctypes.c_void_p(st.cuda_stream)), "pb_density_step")
         self._next_clear = True
+        self._order_caller(stream)
         return self.rho
+
+    def _order_caller(self, stream):
+        """A public call on the engine stream (stream=None) returns device
+        tensors: order the caller's current stream after it, so reading the
+        result right away (e.g. .cpu()) sees the kernel's writes."""
+        if stream is None:
+            caller = torch.cuda.current_stream(self.device)
+            if caller.cuda_stream != self.stream.cuda_stream:
+                caller.wait_stream(self.stream)
 
     def _setup_peer(self, nbins: int, nc: int):
         from .peer import PeerBuffers
@@ -453,6 +467,7 @@ class Engine:
             else:
                 _lib.check(self.lib.pb_compute_efield(self.phi.data_ptr(), self.e.data_ptr(), self.nc,
                                                       self.grid.dx_m, self.field_bc, sh), "pb_compute_efield")
+        self._order_caller(stream)
         return self.e
 
     def _subset(self, which):
@@ -495,6 +510,35 @@ class Engine:
         self._next_clear = True
         return self.rho
 
+    def _fused_ok(self) -> bool:
+        return (self.cfg.field_solve and self.fused_field and self.peer is None and self.poisson == "scan"
+                and not self._field_split()[0])
+
+    def _fused_cycle(self):
+        """pb_field_cycle on the engine stream (after the bin allreduce when
+        N > 1): the density epilogue with the smoothing pass folded in, the
+        scan Poisson solve and E, which also zeroes the bin set just read
+        (the push deposits into the other one, zeroed one step earlier)."""
+        cfg = self.cfg
+        read = self.bins_pp[self.cur]
+        with torch.cuda.stream(self.stream):
+            if self.world > 1:
+                reduce_bins(self.bins, self.group)
+            _lib.check(self.lib.pb_field_cycle(
+                self.bins.data_ptr(), self._coef_c, self.ndep, self.nc, self.field_bc,
+                int(cfg.smoothing_passes), self.grid.dx_m, cfg.consts.epsilon0, cfg.phi_left, cfg.phi_right,
+                self.left.data_ptr(), self.right.data_ptr(), self.rho.data_ptr(), self.rho_s.data_ptr(),
+                self.phi.data_ptr(), self.e.data_ptr(), read.data_ptr(), None, read.numel(),
+                self.status.data_ptr(), self.field_scratch.data_ptr(), self._sh()), "pb_field_cycle")
+        self._next_clear = True
+        return (self.rho_s if cfg.smoothing_passes > 0 else self.rho), self.e
+
+    def _compact(self):
+        """Absorbing walls: fill the removed particles' slots from the tail (pb_compact)."""
+        arr, n = self._species()
+        _lib.check(self.lib.pb_compact(arr, n, self.status.data_ptr(), self.compact_scratch.data_ptr(),
+                                       self.compact_scratch.numel(), self._sh()), "pb_compact")
+
     def _field_cycle(self):
         """Field-solve step body.  The species that need no field (neutral
         movers) are pushed on the engine stream while the density epilogue
@@ -503,7 +547,11 @@ class Engine:
         movers this is the plain serial cycle."""
         neutral, rest = self._field_split()
         if not neutral:
-            if self.density_one and self.peer is None:
+            if self._fused_ok():
+                # density + smoothing + scan Poisson + E + bin clears: one
+                # launch (pb_field_cycle), bitwise the per-phase kernels below
+                rho, e = self._fused_cycle()
+            elif self.density_one and self.peer is None:
                 # one-kernel epilogue (no self-clear: neighbouring nodes read
                 # the same cells); E clears the bins (bitwise density())
                 rho = self._density_one()
@@ -555,9 +603,7 @@ class Engine:
     def resort(self):
         with torch.cuda.stream(self.stream):
             if self.absorbing:
-                arr, n = self._species()
-                _lib.check(self.lib.pb_compact(arr, n, self.status.data_ptr(), self.compact_scratch.data_ptr(),
-                                               self.compact_scratch.numel(), self._sh()), "pb_compact")
+                self._compact()
             due = self._sorts_due(1)
             if due:
                 self.sort_by_cell(due)
@@ -801,10 +847,7 @@ class Engine:
                 else:
                     rho, e = self._field_cycle()
                 if self.absorbing:
-                    arr, m = self._species()
-                    _lib.check(self.lib.pb_compact(arr, m, self.status.data_ptr(),
-                                                   self.compact_scratch.data_ptr(),
-                                                   self.compact_scratch.numel(), self._sh()), "pb_compact")
+                    self._compact()
                 self._snap_counts(gp, j)
                 if overlap:
                     snap_stream = self._side  # rho_j is final once epilogue j is done
@@ -853,10 +896,7 @@ class Engine:
                 else:
                     self._field_cycle()
                 if self.absorbing:
-                    arr, n = self._species()
-                    _lib.check(self.lib.pb_compact(arr, n, self.status.data_ptr(),
-                                                   self.compact_scratch.data_ptr(),
-                                                   self.compact_scratch.numel(), self._sh()), "pb_compact")
+                    self._compact()
             if prev is not None:
                 self.stream.wait_event(prev)
             if not overlap and self._field_split()[0]:

@@ -2,8 +2,9 @@
 their cell range of the population, step with the density allreduce on the
 side stream (field-free) or the split field cycle (field solve), and must
 reproduce the single-rank density bit for bit (fixed-point bins are summed
-exactly, so the reduction order cannot matter).  The NCCL transport is the
-only part not exercised here."""
+exactly, so the reduction order cannot matter).  With two or more GPUs
+visible the same runs go through NCCL / NVLink peer memory, one GPU per
+rank (test_two_gpus_nccl_match_one_rank_and_oracle; skipped on one GPU)."""
 
 import os
 import socket
@@ -27,16 +28,19 @@ def _cfg(field):
                      sort_every=4)
 
 
-def _worker(rank, world, port, field, out, peer=False):
+def _worker(rank, world, port, field, out, peer=False, nccl=False):
     import torch
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # nccl: one GPU per rank (the production transport); else gloo, all on cuda:0
+    dev = torch.device("cuda", rank if nccl else 0)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl" if nccl else "gloo", rank=rank, world_size=world)
     from paper_2404_10270_b200 import Engine
 
-    eng = Engine(_cfg(field), device=torch.device("cuda", 0), rank=rank, world=world, check_every=0,
+    eng = Engine(_cfg(field), device=dev, rank=rank, world=world, check_every=0,
                  peer=peer)
     assert (eng.peer is not None) == peer  # the peer-memory exchange mapped every rank's buffers
     assert eng._field_split()[0] if field else True  # the N>1 default overlaps the neutral push
@@ -51,6 +55,9 @@ def _worker(rank, world, port, field, out, peer=False):
     eng.sync()
     if rank == 0:
         np.save(out, np.array(rhos))
+    fl = eng.download()
+    np.savez(out + f".rank{rank}.npz", **{f"sp{k}_{n}": a for k, f in enumerate(fl)
+                                         for n, a in list(f.fields().items()) + [("cell", f.cell)]})
     dist.barrier()
     eng.close()
     dist.barrier()
@@ -86,6 +93,64 @@ def test_two_ranks_match_one_rank_bitwise(cuda, tmp_path, field, peer):
     assert got.shape == np.array(want).shape
     for k, (a, b) in enumerate(zip(got, want)):
         assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), k
+    if not field:
+        _check_union_vs_oracle(out, 2, 16)  # 9 eager + 6 replayed + 1
+
+
+def _check_union_vs_oracle(out, world, steps):
+    """Field-free runs: the union of the ranks' particles after `steps`
+    steps equals the C oracle stepping the whole population on the host
+    (E = 0, same initial load), per-cell multisets bit for bit -- the
+    multi-rank path pinned to the oracle directly, not only to one rank."""
+    from oracle import oracle
+    from paper_2404_10270_b200.core import init_species_host, velocity_kick_coef
+    from paper_2404_10270_b200.engine import species_kind
+
+    cfg = _cfg(False)
+    nc = cfg.grid.nc
+    e = np.zeros(nc + 1)
+    parts = [np.load(out + f".rank{r}.npz") for r in range(world)]
+    for k, spd in enumerate(cfg.species):
+        f = init_species_host(cfg, k)
+        kind = species_kind(spd, None)
+        coef = velocity_kick_coef(spd, cfg.consts, cfg.grid.dx_m) if spd.charged else 0.0
+        for _ in range(steps):
+            _, _, cfl = oracle.step_flat(kind, 0, float(spd.nstep), coef, e, nc, f.x, f.vx, f.vy, f.vz, f.yp,
+                                         f.cell)
+            assert cfl == -1
+        names = list(f.fields())
+        got = {n: np.concatenate([p[f"sp{k}_{n}"] for p in parts]) for n in names}
+        cell = np.concatenate([p[f"sp{k}_cell"] for p in parts])
+        assert np.array_equal(oracle.canonical(cell, got), oracle.canonical(f.cell, f.fields())), spd.name
+
+
+@pytest.mark.skipif("__import__('torch').cuda.device_count() < 2")
+@pytest.mark.parametrize("peer", [False, True])
+def test_two_gpus_nccl_match_one_rank_and_oracle(cuda, tmp_path, peer):
+    """Runs whenever >= 2 GPUs are visible: one rank per GPU with the NCCL
+    process group -- peer False: reduce_bins as an NCCL allreduce of the
+    fixed-point bins; peer True: pb_peer_density_step over NVLink IPC
+    mappings (co-residency checked at launch).  rho per step equals the
+    single-GPU run bit for bit and the particles equal the oracle."""
+    import torch.multiprocessing as mp
+
+    from paper_2404_10270_b200 import Engine
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = str(tmp_path / "rho.npy")
+    mp.spawn(_worker, args=(2, port, False, out, peer, True), nprocs=2, join=True)
+    got = np.load(out)
+    eng = Engine(_cfg(False), device=cuda, check_every=0)
+    want = []
+    for _ in range(16):
+        rho, _ = eng.step()
+        want.append(rho.cpu().numpy().copy())
+    want = [want[k] for k in list(range(9)) + [15]]
+    for k, (a, b) in enumerate(zip(got, want)):
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), k
+    _check_union_vs_oracle(out, 2, 16)
 
 
 def _canon_worker(rank, world, port, out):
