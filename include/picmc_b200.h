@@ -249,9 +249,12 @@ int pb_smooth_density(const double *rho, double *out, int64_t nc, int passes,
 int pb_solve_poisson(const double *rho, double *phi, int64_t nc, double dx,
                      double eps0, int field_bc, double phi_left,
                      double phi_right, void *scratch, void *stream);
-/* Same solve in parallel: the closed-form pivots turn both Thomas sweeps
- * into prefix sums (double-double accumulation); ~1e-15 relative to the
- * serial elimination, O(nc/1024) depth.  Used for large field grids. */
+/* Same system in parallel: its Green's-function form (the closed-form
+ * Thomas pivots telescoped through both sweeps) needs ONE prefix scan of
+ * (sum r, sum (k+1) r) over 512-unknown tiles plus the totals (periodic: the
+ * mean enters in closed form); ~1e-14 max|phi| from a long-double
+ * elimination at 1e5 unknowns.  Three launches (tile aggregates, tile
+ * prefixes, tile solves).  Used for large field grids. */
 int pb_solve_poisson_scan(const double *rho, double *phi, int64_t nc,
                           double dx, double eps0, int field_bc,
                           double phi_left, double phi_right, void *scratch,
@@ -270,10 +273,13 @@ int pb_compute_efield_clear(const double *phi, double *e, int64_t nc,
  * (weighted partials, stitched rho, overflow check) + pb_smooth_density
  * (`passes` 1-2-1 passes into rho_s) + pb_solve_poisson_scan (on rho_s) +
  * pb_compute_efield_clear (E, then zero nwords words of clr_a / clr_b; both
- * may be NULL), bitwise those four calls.  With passes == 1 the epilogue and
- * the smoothing are one kernel (each thread forms the three densities its
- * node's smoothing reads).  `scratch` needs pb_field_scratch_bytes(nc)
- * bytes; left / right may be NULL. */
+ * may be NULL), bitwise those four calls, in ONE launch (k_field_fused:
+ * every tile forms its density window and local scan, one grid-wide
+ * arrival count, then the solve and E) when passes <= 4 and the
+ * ceil((nc-1)/512) tiles fit co-resident on the device, else as kernels.
+ * `scratch` needs pb_field_scratch_bytes(nc) bytes, ZEROED before its first
+ * use (its two counter words return to zero after every launch); left /
+ * right may be NULL. */
 int pb_field_cycle(const uint64_t *bins, const double *coef, int ndep,
                    int64_t nc, int field_bc, int passes, double dx,
                    double eps0, double phi_left, double phi_right,

@@ -89,6 +89,14 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// The two halves, for kernels that should hold their dependents back (a
+// dependent launched early is resident beside the kernel; see
+// k_field_fused).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 bool pdl_enabled();  // compile-time PB_PDL (default 1)
 
 // Launch `kern` with programmatic stream serialisation (when enabled); the

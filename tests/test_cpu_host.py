@@ -285,3 +285,55 @@ def test_errors_are_the_reference_classes_when_importable(tmp_path):
             "and e.EngineError is r.EngineError and e.ConfigError is r.ConfigError")
     env = dict(os.environ, PYTHONPATH=os.pathsep.join([ref, ROOT]), PICMC_BACKEND="pure")
     subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=str(tmp_path))
+
+
+def _thomas_exact(r):
+    """_thomas_unit (pkg/src/picmc/fields.py:138-153) in exact rationals."""
+    from fractions import Fraction
+
+    n = len(r)
+    diag, y = [Fraction(-2)], [r[0]]
+    for i in range(1, n):
+        m = 1 / diag[i - 1]
+        diag.append(Fraction(-2) - m)
+        y.append(r[i] - m * y[i - 1])
+    x = [None] * n
+    x[n - 1] = y[n - 1] / diag[n - 1]
+    for i in range(n - 2, -1, -1):
+        x[i] = (y[i] - x[i + 1]) / diag[i]
+    return x
+
+
+@pytest.mark.parametrize("nc", [3, 4, 9, 40])
+def test_closed_form_poisson_exact(nc):
+    """The closed form the scan solve implements (csrc/fields.cu, DESIGN
+    3.3) equals the reference's elimination (fields.py:156-202) exactly in
+    rational arithmetic: Dirichlet x_k, the periodic mean part, and the
+    periodic shift sum_k x_k from the tile sum M."""
+    from fractions import Fraction as F
+
+    rng = np.random.default_rng(nc)
+    rho = [F(int(v), 7) for v in rng.integers(-90, 90, nc + 1)]
+    scale, pl, pr = F(11, 3), F(5, 2), F(-3)
+    n = nc - 1
+    for periodic in (False, True):
+        if periodic:
+            mean = sum(rho[:nc]) / nc
+            a = [-rho[j + 1] * scale for j in range(n)]
+            r = [-(rho[j + 1] - mean) * scale for j in range(n)]
+        else:
+            mean = F(0)
+            a = [-rho[j + 1] * scale for j in range(n)]
+            a[0] -= pl
+            a[n - 1] -= pr
+            r = a
+        x = _thomas_exact(r)
+        S = [sum(a[: k + 1]) for k in range(n)]
+        Z = [sum((j + 1) * a[j] for j in range(k + 1)) for k in range(n)]
+        sm = scale * mean
+        xc = [-(Z[k] + (k + 1) * ((S[-1] - S[k]) - Z[-1] / (n + 1))) - sm * F((k + 1) * (n - k), 2)
+              for k in range(n)]
+        assert xc == x
+        if periodic:
+            M = sum(F((j + 1) * (2 * n - j), 2) * a[j] for j in range(n))
+            assert -(M - Z[-1] * F(n, 2)) - sm * F(n * (n + 1) * (n + 2), 12) == sum(x)

@@ -145,3 +145,76 @@ def test_engine_fused_cycle_matches_per_phase(cuda, case):
         assert x.n == y.n
         for k in x.fields():
             assert bits_equal(x.fields()[k], y.fields()[k]), k
+
+
+@pytest.mark.parametrize("bc", ["periodic", "dirichlet"])
+@pytest.mark.parametrize("nc,passes", [(65536, 4), (65536, 5), (3, 1), (4, 0), (512, 2), (513, 1), (514, 1),
+                                       (1025, 3), (1026, 2), (1027, 1)])
+def test_field_cycle_edges_bitwise(cuda, nc, bc, passes):
+    """The single-launch cycle at its limits: the largest pass count it takes
+    (4), the per-phase fallback past it (5), one tile (nc <= 513), and last
+    tiles that are full (nc = 512 m + 1), hold one unknown (its first is its
+    last: nc = 512 m + 2) or two."""
+    from paper_2404_10270_b200 import _lib
+
+    lib = _lib.load()
+    code = _lib.PB_FIELD_PERIODIC if bc == "periodic" else _lib.PB_FIELD_DIRICHLET
+    bins = _bins(nc, 3, seed=7 * nc + passes)
+    args = (lib, bins, [-1.1e-9, 2.9e-9, 0.7e-9], 3, nc, code, passes, 2e-5, 8.8541878128e-12, -0.5, 2.0, cuda)
+    a = _chain(*args, fused=False)
+    b = _chain(*args, fused=True)
+    for k in ("left", "right", "rho", "rho_s", "phi", "e"):
+        assert bits_equal(a[k], b[k]), k
+    assert a["bins_zero"] and b["bins_zero"]
+
+
+@pytest.mark.parametrize("bc", ["periodic", "dirichlet"])
+def test_field_cycle_epochs_and_graph_replay(cuda, bc):
+    """One scratch over many launches (the flags' launch epoch advances
+    every call) and inside a replayed CUDA graph: every call equals the
+    per-phase chain on its own bins."""
+    import torch
+
+    from paper_2404_10270_b200 import _lib
+    from paper_2404_10270_b200.store import status_template
+
+    lib = _lib.load()
+    code = _lib.PB_FIELD_PERIODIC if bc == "periodic" else _lib.PB_FIELD_DIRICHLET
+    nc, ndep, passes = 40000, 2, 1
+    coef = [-1.7e-9, 2.3e-9]
+    c = (ctypes.c_double * ndep)(*coef)
+    t = lambda n: torch.zeros(n, dtype=torch.float64, device=cuda)  # noqa: E731
+    out = {k: t(nc + 1) for k in ("rho", "rho_s", "phi", "e")}
+    left, right = t(nc), t(nc)
+    scr = torch.zeros(lib.pb_field_scratch_bytes(nc), dtype=torch.uint8, device=cuda)
+    st = status_template(cuda)
+    b0 = torch.zeros(2 * ndep * nc, dtype=torch.int64, device=cuda)
+    src = torch.zeros_like(b0)
+    P = lambda x: x.data_ptr()  # noqa: E731
+
+    def call(stream):
+        b0.copy_(src)
+        _lib.check(lib.pb_field_cycle(P(b0), c, ndep, nc, code, passes, 1e-5, 8.8541878128e-12, 1.0, 0.0,
+                                      P(left), P(right), P(out["rho"]), P(out["rho_s"]), P(out["phi"]),
+                                      P(out["e"]), P(b0), None, b0.numel(), P(st), P(scr),
+                                      ctypes.c_void_p(stream.cuda_stream)), "pb_field_cycle")
+
+    s = torch.cuda.Stream(cuda)
+    g = torch.cuda.CUDAGraph()
+    for it in range(12):
+        bins = _bins(nc, ndep, seed=100 + it)
+        src.copy_(torch.from_numpy(bins.view(np.int64)))
+        if it < 6:
+            with torch.cuda.stream(s):
+                call(s)
+        else:
+            if it == 6:
+                with torch.cuda.graph(g, stream=s):
+                    call(torch.cuda.current_stream())
+            g.replay()
+        torch.cuda.synchronize()
+        ref = _chain(lib, bins, coef, ndep, nc, code, passes, 1e-5, 8.8541878128e-12, 1.0, 0.0, cuda,
+                     fused=False)
+        for k in ("rho", "rho_s", "phi", "e"):
+            assert bits_equal(ref[k], out[k].cpu().numpy()), (it, k)
+        assert not b0.any().item()
