@@ -134,6 +134,7 @@ typedef struct pb_status {
 
 /* ---- library ------------------------------------------------------------ */
 int pb_abi_version(void);
+size_t pb_status_bytes(void); /* sizeof(pb_status) as compiled */
 const char *pb_last_error(void);
 int pb_device_sm_count(int *out);
 

@@ -116,6 +116,7 @@ STATUS_BYTES = ctypes.sizeof(PbStatus)
 # name -> (restype, argtypes); mirrors include/picmc_b200.h one to one.
 _SIGS = {
     "pb_abi_version": (ctypes.c_int, []),
+    "pb_status_bytes": (ctypes.c_size_t, []),
     "pb_set_canonical_scatter_min": (ctypes.c_int, [_i64]),
     "pb_last_error": (ctypes.c_char_p, []),
     "pb_device_sm_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),

@@ -100,15 +100,17 @@ class CanonicalEngine(Engine):
     def deposit_current(self):
         """(Re)build per-cell offs/counts of the loaded, cell-sorted store."""
         nc = self.nc
-        if not hasattr(self, "layout_scratch"):
-            self.layout_scratch = torch.empty(self.lib.pb_layout_scratch_bytes(nc), dtype=torch.uint8,
-                                              device=self.device)
-            self.offs = [torch.zeros(nc + 1, dtype=torch.int64, device=self.device) for _ in self.sp]
-            self.counts = [torch.zeros(nc, dtype=torch.int64, device=self.device) for _ in self.sp]
-        for k, s in enumerate(self.sp):
-            _lib.check(self.lib.pb_cell_layout(s.cell.data_ptr(), s.n, nc, self.offs[k].data_ptr(),
-                                               self.counts[k].data_ptr(), self.layout_scratch.data_ptr(),
-                                               self.layout_scratch.numel(), self._sh()), "pb_cell_layout")
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(self.stream):  # zero-fills ordered before the layout kernels
+            if not hasattr(self, "layout_scratch"):
+                self.layout_scratch = torch.empty(self.lib.pb_layout_scratch_bytes(nc), dtype=torch.uint8,
+                                                  device=self.device)
+                self.offs = [torch.zeros(nc + 1, dtype=torch.int64, device=self.device) for _ in self.sp]
+                self.counts = [torch.zeros(nc, dtype=torch.int64, device=self.device) for _ in self.sp]
+            for k, s in enumerate(self.sp):
+                _lib.check(self.lib.pb_cell_layout(s.cell.data_ptr(), s.n, nc, self.offs[k].data_ptr(),
+                                                   self.counts[k].data_ptr(), self.layout_scratch.data_ptr(),
+                                                   self.layout_scratch.numel(), self._sh()), "pb_cell_layout")
 
     # -- step phases ----------------------------------------------------------
     def density(self) -> torch.Tensor:
@@ -149,6 +151,7 @@ class CanonicalEngine(Engine):
                 self.nb_k = torch.zeros(sn.n, dtype=torch.int32, device=self.device)
             self._arr = None
         cap = min(se.cap - se.n, si.cap - si.n)
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))  # growth / nb_k fills above
         with torch.cuda.stream(self.stream):
             pe, pn, pi = se.pb(), sn.pb(), si.pb()
             _lib.check(self.lib.pb_collide(

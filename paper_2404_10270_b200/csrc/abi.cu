@@ -120,6 +120,8 @@ __global__ void k_stitch(const double *__restrict__ left, const double *__restri
 
 extern "C" int pb_abi_version(void) { return PB_ABI_VERSION; }
 
+extern "C" size_t pb_status_bytes(void) { return sizeof(pb_status); }
+
 extern "C" const char *pb_last_error(void) { return pb::g_err; }
 
 extern "C" int pb_device_sm_count(int *out) {

@@ -460,13 +460,31 @@ __device__ __forceinline__ unsigned long long global_ns() {
 
 // In-kernel launch clock (pb_status.mover_t0/mover_ns/mover_launches): one
 // RED.MIN per block at its start...
+// PB_MOVER_TRACE builds: every block's start and every warp's finish
+// (scripts/mover_tail_trace.py, pb_debug_warp_ends)
+#ifdef PB_MOVER_TRACE
+__device__ unsigned long long g_blk_start[2048];
+__device__ unsigned long long g_warp_end[8192];
+#endif
 __device__ __forceinline__ void mover_clock_start(pb_status *st) {
-  if (threadIdx.x == 0) atomicMin((unsigned long long *)&st->mover_t0, global_ns());
+  if (threadIdx.x == 0) {
+    const unsigned long long t = global_ns();
+    atomicMin((unsigned long long *)&st->mover_t0, t);
+#ifdef PB_MOVER_TRACE
+    if (blockIdx.x < 2048) g_blk_start[blockIdx.x] = t;
+#endif
+  }
 }
 
 __device__ __forceinline__ void release_work_counter(pb_status *st, unsigned long long claimers) {
 #ifdef PB_RELEASE_FENCE
   __threadfence();
+#endif
+#ifdef PB_MOVER_TRACE
+  {
+    const unsigned w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (w < 8192) g_warp_end[w] = global_ns();
+  }
 #endif
   const unsigned long long d = atomicAdd((unsigned long long *)&st->tile_done, 1ull);
   if (d == claimers - 1) {
@@ -1464,3 +1482,16 @@ extern "C" int pb_deposit_only(const pb_species *sp, int nsp, int64_t nc, uint64
 }
 
 extern "C" const char *pb_last_mover_kernel(void) { return pb::g_last_kernel; }
+
+#ifdef PB_MOVER_TRACE
+// debug: the last launch's block starts and per-warp finish times (globaltimer ns)
+extern "C" int pb_debug_warp_ends(unsigned long long *out, int n, unsigned long long *starts, int nb) {
+  if (n > 8192) n = 8192;
+  if (nb > 2048) nb = 2048;
+  if (cudaMemcpyFromSymbol(out, pb::g_warp_end, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
+    return PB_ERR_CUDA;
+  return cudaMemcpyFromSymbol(starts, pb::g_blk_start, (size_t)nb * sizeof(unsigned long long)) == cudaSuccess
+             ? PB_OK
+             : PB_ERR_CUDA;
+}
+#endif

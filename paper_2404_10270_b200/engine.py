@@ -279,6 +279,9 @@ class Engine:
 
     def _load(self, init: str):
         cfg = self.cfg
+        # the stores were allocated (and n_dev filled) on the caller's stream;
+        # the engine stream is a non-blocking stream, so order it explicitly
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(self.stream):
             for isp, s in enumerate(self.sp):
                 if init == "host":
@@ -359,6 +362,7 @@ class Engine:
 
     def upload(self, flats: list):
         """Replace the particle state with host arrays (engine flat layout)."""
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(self.stream):
             for s, f in zip(self.sp, flats):
                 if f.n != s.n:

@@ -4,7 +4,7 @@
 # Summaries -> gpurun_out/sanitize_<tool>.txt
 OUT=gpurun_out
 mkdir -p $OUT
-SEL="tests/test_engine_gpu.py tests/test_backend_gpu.py tests/test_safety_gpu.py tests/test_bfield_gpu.py tests/test_canonical_gpu.py tests/test_fields_api_gpu.py tests/test_mover_api_gpu.py"
+SEL="tests/test_field_cycle_gpu.py tests/test_engine_gpu.py tests/test_backend_gpu.py tests/test_safety_gpu.py tests/test_bfield_gpu.py tests/test_canonical_gpu.py tests/test_fields_api_gpu.py tests/test_mover_api_gpu.py"
 DESEL="not full and not large and not criterion01 and not statistics and not drift and not free_streaming and not pipelined and not pipe_graphs"
 # positive control: memcheck must flag a deliberate out-of-bounds store
 nvcc -gencode arch=compute_100a,code=sm_100a -o /tmp/oob_control scripts/sanitize/oob_control.cu

@@ -49,6 +49,7 @@ def test_status_struct_layout_matches_header():
     # int32 code, int32 species, u64 index, 8 moved, 8x2 absorbed, 8 holes, overflow,
     # tile_next, tile_done, tile_next2, mover_t0, mover_ns, mover_launches
     assert _lib.STATUS_BYTES == 4 + 4 + 8 + 8 * 8 + 16 * 8 + 8 * 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8
+    assert _lib.load().pb_status_bytes() == _lib.STATUS_BYTES  # the C struct, as compiled
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
