@@ -892,8 +892,104 @@ struct WarpRing {
   SliceMeta *meta;
 };
 
+// Intra-block slice sharing (k_push_ring): each warp's claimed chunk is
+// handed out slice by slice through a shared word, generation:16 |
+// next slice:24 | slices:24, with the chunk's [base, end) and species in a
+// two-generation buffer.  The owner takes its slices with the same atomic,
+// so once the global chunk counter runs dry the warps that finish first take
+// the remaining slices of their block's busy warps: a block ends when its
+// eight warps' leftovers are done, not when its slowest warp finishes its
+// whole last chunk (profiles/r02_mover_tail.txt: 24 us of warp finishing
+// spread in a 91 us config-3 launch).
+struct ShareChunk {
+  int64_t base, end;
+  int32_t isp, pad;
+};
+struct ShareState {
+  unsigned long long word[kWarpsPerBlock];
+  ShareChunk gen[kWarpsPerBlock][2];
+};
+constexpr int kShareSliceShift = 24;
+constexpr unsigned long long kShareMask = (1ull << 24) - 1;
+
 static constexpr int ring_smem_bytes() {
-  return kWarpsPerBlock * kRing * (kSliceBytes + (int)sizeof(uint64_t) + (int)sizeof(SliceMeta));
+  return kWarpsPerBlock * kRing * (kSliceBytes + (int)sizeof(uint64_t) + (int)sizeof(SliceMeta)) +
+         (int)sizeof(ShareState);
+}
+
+// Take the next slice of warp v's shared chunk in two halves: share_fetch
+// issues the atomic (lane 0 keeps the raw word, not yet waited on), and
+// share_decode broadcasts it -- true with [sb, sb + cnt) of species isp,
+// false when that chunk was exhausted.  The owner fetches its next take one
+// slice ahead, so the shared-memory atomic's latency stays off the issue
+// path (taken back to back it cost config 3 ~3% of the push).  Warp-collective.
+__device__ __forceinline__ unsigned long long share_fetch(ShareState *sh, int v) {
+  unsigned long long old = 0;
+  if (lane_id() == 0) old = atomicAdd(&sh->word[v], 1ull << kShareSliceShift);
+  return old;
+}
+__device__ __forceinline__ bool share_decode(const ShareState *sh, int v, unsigned long long raw, int64_t &sb,
+                                             int &cnt, int &isp, uint32_t &gen) {
+  const unsigned long long old = __shfl_sync(0xffffffffu, raw, 0);
+  gen = (uint32_t)(old >> 48);
+  const unsigned long long idx = (old >> kShareSliceShift) & kShareMask, n = old & kShareMask;
+  if (idx >= n) return false;
+  const ShareChunk c = sh->gen[v][gen & 1];
+  sb = c.base + (int64_t)idx * kSlice;
+  cnt = (int)(c.end - sb < kSlice ? c.end - sb : kSlice);
+  isp = c.isp;
+  return true;
+}
+__device__ __forceinline__ bool share_take(ShareState *sh, int v, int64_t &sb, int &cnt, int &isp,
+                                           uint32_t &gen) {
+  return share_decode(sh, v, share_fetch(sh, v), sb, cnt, isp, gen);
+}
+
+// Owner: publish [beg, end) of species isp as warp w's next chunk generation.
+__device__ __forceinline__ void share_install(ShareState *sh, int w, uint32_t gen, int64_t beg, int64_t end,
+                                              int isp) {
+  if (lane_id() == 0) {
+    ShareChunk &c = sh->gen[w][(gen + 1) & 1];
+    c.base = beg;
+    c.end = end;
+    c.isp = isp;
+    __threadfence_block();
+    const unsigned long long n = (unsigned long long)((end - beg + kSlice - 1) / kSlice);
+    atomicExch(&sh->word[w], ((unsigned long long)((gen + 1) & 0xffff) << 48) | n);
+  }
+  __syncwarp();
+}
+
+// Once the work lists are drained: the leftover ring slices of the block's
+// ring warps [0, nring), through the register path (any warp of the block).
+template <int BC>
+__device__ __forceinline__ void steal_ring_slices(const LaunchArgs &a, ShareState *share, int w, int nring,
+                                                  Window &win, Tally &t, int &cur) {
+  const int lane = (int)lane_id();
+  for (int v = 1; v <= nring; ++v) {
+    const int victim = (w + v) % kWarpsPerBlock;
+    if (victim >= nring || victim == w) continue;
+    int64_t sb;
+    int cnt, isp;
+    uint32_t gen;
+    while (share_take(share, victim, sb, cnt, isp, gen)) {
+      const pb_species &s = a.sp[isp];
+      if (isp != cur) {
+        if (cur >= 0) flush_tally(a, a.id[cur], t, nullptr);
+        t = Tally();
+        cur = isp;
+        win.gR = a.bins + (size_t)s.deposit * 2 * (size_t)a.nc;
+        win.gC = win.gR + a.nc;
+      }
+      Quad<PB_KIND_KICK, false> q;
+      const int64_t i = sb + 4 * lane;
+      quad_load<PB_KIND_KICK, false>(s, i, sb + cnt, q);
+      if (PB_FULL_SLICES && cnt == kSlice)
+        quad_process<PB_KIND_KICK, false, BC, true, true>(a, isp, i, q, win, t);
+      else
+        quad_process<PB_KIND_KICK, false, BC, true>(a, isp, i, q, win, t);
+    }
+  }
 }
 
 template <int BC>
@@ -906,30 +1002,37 @@ __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
   const int w = threadIdx.x >> 5;
   uint64_t *bars = reinterpret_cast<uint64_t *>(r_smem + (size_t)kWarpsPerBlock * kRing * kSliceBytes);
   SliceMeta *metas = reinterpret_cast<SliceMeta *>(bars + kWarpsPerBlock * kRing);
+  ShareState *share = reinterpret_cast<ShareState *>(metas + kWarpsPerBlock * kRing);
   const WarpRing r{r_smem + (size_t)w * kRing * kSliceBytes, bars + w * kRing, metas + w * kRing};
   if (lane == 0) {
     for (int k = 0; k < kRing; ++k) mbar_init(&r.bar[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    share->word[w] = 0;  // generation 0, no slices: the first take claims
   }
-  __syncwarp();
+  __syncthreads();  // every warp's share word is initialised before any thief reads it
   const int64_t total = a.tile_start[a.nsp];
   Window win{nullptr, nullptr, 0, 0, nullptr, nullptr};
   Tally t;
   int cur = -1;
-  int64_t ibeg = 0, iend = 0;
-  int iisp = 0;
   bool issuing = true;
   uint32_t head = 0, tail = 0;
+  unsigned long long pend = share_fetch(share, w);  // lane 0: the take of the next slice
   auto issue = [&]() {
-    while (ibeg >= iend) {  // current chunk exhausted (or empty): claim the next
+    int64_t ibeg;
+    int cnt, iisp;
+    uint32_t gen;
+    while (!share_decode(share, w, pend, ibeg, cnt, iisp, gen)) {  // own chunk exhausted: claim the next
       const int64_t c = claim_chunk(a);
       if (c >= total) {
         issuing = false;
         return;
       }
-      iisp = chunk_species(a, c, ibeg, iend);
+      int64_t beg, end;
+      const int isp = chunk_species(a, c, beg, end);
+      if (end > beg) share_install(share, w, gen, beg, end, isp);
+      pend = share_fetch(share, w);
     }
-    const int cnt = (int)(iend - ibeg < kSlice ? iend - ibeg : kSlice);
+    pend = share_fetch(share, w);  // one slice ahead: waited on at the next issue
     const uint32_t st = head % kRing;
     if (lane == 0) {
       r.meta[st].base = ibeg;
@@ -946,7 +1049,6 @@ __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
         mbar_arrive(&r.bar[st]);  // partial slice: loaded directly, phase still completes
       }
     }
-    ibeg += cnt;
     ++head;
   };
   while (issuing && head - tail < (uint32_t)kRing) issue();
@@ -989,6 +1091,9 @@ __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
     else
       quad_process<PB_KIND_KICK, false, BC, true>(a, m.isp, i, q, win, t);
   }
+  // the global counter is dry and this warp's ring is drained: take the
+  // leftover slices of the block's other warps
+  steal_ring_slices<BC>(a, share, w, kWarpsPerBlock, win, t, cur);
   if (cur >= 0) flush_tally(a, a.id[cur], t, nullptr);
   if (lane == 0) release_work_counter(a.st, (unsigned long long)gridDim.x * kWarpsPerBlock);
 }
@@ -1010,9 +1115,13 @@ __global__ void __launch_bounds__(kThreads, PB_QUAD_MINBLOCKS)
 constexpr int kSplitRingWarps = PB_SPLIT_RING_WARPS;
 constexpr int kSplitStages = PB_SPLIT_STAGES;
 
+// (No slice sharing here: the per-slice shared-memory atomic on the ring
+// warps' issue path cost config 2 3.5% of the push, more than its tail
+// gained -- profiles/r02_mover_tail.txt.)
 static constexpr int split_smem_bytes() {
   return kSplitRingWarps * kSplitStages * (kSliceBytes + (int)sizeof(uint64_t) + (int)sizeof(SliceMeta));
 }
+
 
 __device__ __forceinline__ int list_chunk(const LaunchArgs &a, const ChunkList &L, int64_t c,
                                           int64_t &beg, int64_t &end) {
