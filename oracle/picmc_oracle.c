@@ -128,7 +128,7 @@ static void boris(double *vx, double *vy, double *vz, double atemp,
 /* Spatially varying B (pb_species.b_nodes, include/picmc_b200.h): nodes
  * hold (Bx, By, Bz, pad) in tesla; t = the one-sided linear gather of f*B
  * (f = q dt / (2 m)) in the accel_nodes form (pkg/src/picmc/mover.py:221,
- * _kernels.pyx:83-86), s = 2 t / (1 + |t|^2) in the host's
+ * _kernels.pyx:83-86), s = t * (2 / (1 + |t|^2)) in the host's
  * boris_coefficients op order.  Each operation rounds separately. */
 static void boris_t_gather(const double *bnodes, double f, int32_t c, double x, double *t,
                            double *s) {
@@ -139,8 +139,8 @@ static void boris_t_gather(const double *bnodes, double f, int32_t c, double x, 
     t[k] = t0 + x * (t1 - t0);
   }
   const double t2 = t[0] * t[0] + t[1] * t[1] + t[2] * t[2];
-  const double den = 1.0 + t2;
-  for (int k = 0; k < 3; ++k) s[k] = (2.0 * t[k]) / den;
+  const double g = 2.0 / (1.0 + t2);
+  for (int k = 0; k < 3; ++k) s[k] = t[k] * g;
 }
 
 static int64_t pymod(int64_t a, int64_t m) {

@@ -27,8 +27,9 @@ __host__ __device__ constexpr bool is_boris(int k) { return k == PB_KIND_BORIS |
 // Spatially varying B (pb_species.b_nodes): one 32-byte read-only load per
 // node (bx, by, bz, pad; L2-resident), the one-sided linear gather of
 // f*B in the same form as accel_nodes (pkg/src/picmc/mover.py:221), then
-// s = 2t / (1 + |t|^2) -- the host's boris_coefficients op order
-// (engine.py), so a constant profile reproduces the uniform path.
+// s = t * (2 / (1 + |t|^2)) -- one division per particle; the host's
+// boris_coefficients op order (engine.py), so a constant profile reproduces
+// the uniform path.
 __device__ __forceinline__ void ldg_node4(const double *p, double &a, double &b, double &c) {
   double d;
   asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
@@ -51,10 +52,10 @@ __device__ __forceinline__ void boris_t_gather(const pb_species &s, int32_t cell
   ty = node_gather(f, b0y, b1y, x);
   tz = node_gather(f, b0z, b1z, x);
   const double t2 = __dadd_rn(__dadd_rn(__dmul_rn(tx, tx), __dmul_rn(ty, ty)), __dmul_rn(tz, tz));
-  const double den = __dadd_rn(1.0, t2);
-  sx = __ddiv_rn(__dmul_rn(2.0, tx), den);
-  sy = __ddiv_rn(__dmul_rn(2.0, ty), den);
-  sz = __ddiv_rn(__dmul_rn(2.0, tz), den);
+  const double g = __ddiv_rn(2.0, __dadd_rn(1.0, t2));
+  sx = __dmul_rn(tx, g);
+  sy = __dmul_rn(ty, g);
+  sz = __dmul_rn(tz, g);
 }
 
 template <int KIND>

@@ -799,9 +799,10 @@ __device__ __forceinline__ int64_t claim_chunk(const LaunchArgs &a) {
   return (int64_t)__shfl_sync(0xffffffffu, c, 0);
 }
 
-// BMODE: 0 no Boris species, 1 uniform-B Boris, 2 Boris with B nodes
-// (pb_species.b_nodes) -- separate kernels, so the gathered-B path's extra
-// registers do not cost the uniform one.
+// BMODE: 0 no Boris species, 1 uniform-B Boris, 2 every charged mover a
+// Boris species with B nodes (pb_species.b_nodes), 3 any mix with B nodes --
+// separate kernels, so the gathered-B path's extra registers do not cost the
+// uniform one.
 template <int BC, int BMODE>
 __device__ __forceinline__ void quad_dispatch(const LaunchArgs &a, int isp, int64_t beg,
                                               int64_t end, const Window &win, Tally &t) {
@@ -813,11 +814,15 @@ __device__ __forceinline__ void quad_dispatch(const LaunchArgs &a, int isp, int6
     if (dep) quad_chunk<K, Y, BC, true>(a, isp, beg, end, win, t);  \
     else quad_chunk<K, Y, BC, false>(a, isp, beg, end, win, t);     \
   } while (0)
-  if (s.kind == PB_KIND_KICK) {
+  // BMODE 2 launches hold only gathered-B Boris and neutral species (the
+  // host checks): the kick and uniform-Boris bodies are not compiled in, so
+  // the kernel's code -- which runs cold in the instruction cache, the two
+  // live paths interleaved across warps -- stays small
+  if (BMODE != 2 && s.kind == PB_KIND_KICK) {
     if (yp) PB_Q(PB_KIND_KICK, true); else PB_Q(PB_KIND_KICK, false);
-  } else if (BMODE == 2 && s.kind == PB_KIND_BORIS && s.b_nodes) {
+  } else if (BMODE >= 2 && s.kind == PB_KIND_BORIS && s.b_nodes) {
     if (yp) PB_Q(kKindBorisB, true); else PB_Q(kKindBorisB, false);
-  } else if (BMODE != 0 && s.kind == PB_KIND_BORIS) {
+  } else if (BMODE != 0 && BMODE != 2 && s.kind == PB_KIND_BORIS) {
     if (yp) PB_Q(PB_KIND_BORIS, true); else PB_Q(PB_KIND_BORIS, false);
   } else {
     if (yp) PB_Q(PB_KIND_DRIFT, true); else PB_Q(PB_KIND_DRIFT, false);
@@ -834,7 +839,7 @@ constexpr int kWarpsPerBlock = kThreads / 32;
 // The gathered-B kernel (BMODE 2) runs at 2 blocks/SM: its per-particle B
 // gather + divisions would spill at the 3-block register budget.
 template <int BC, int BMODE>
-__global__ void __launch_bounds__(kThreads, BMODE == 2 ? 2 : PB_QUAD_MINBLOCKS)
+__global__ void __launch_bounds__(kThreads, BMODE >= 2 ? 2 : PB_QUAD_MINBLOCKS)
     k_push_quad(const __grid_constant__ LaunchArgs a) {
   pdl_enter();
   mover_clock_start(a.st);
@@ -1474,11 +1479,13 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
   if (push && all_move) {
     // Chunk list: species by descending bytes/particle.
     int order[PB_MAX_SPECIES];
-    bool boris = false, bgather = false;
+    bool boris = false, bgather = false, bonly = true;
     for (int k = 0; k < a.nsp; ++k) {
       order[k] = k;
       boris |= a.sp[k].kind == PB_KIND_BORIS;
       bgather |= a.sp[k].kind == PB_KIND_BORIS && a.sp[k].b_nodes != nullptr;
+      // gathered-B only: every charged mover a gathered-B Boris species
+      if (a.sp[k].kind == PB_KIND_KICK || (a.sp[k].kind == PB_KIND_BORIS && !a.sp[k].b_nodes)) bonly = false;
     }
     for (int i = 1; i < a.nsp; ++i)
       for (int j = i; j > 0 && bytes_per_particle(a.sp[order[j]], true) >
@@ -1543,9 +1550,9 @@ static int launch(const pb_species *sp, int nsp, const double *e, int64_t nc, in
                                                     : k_push_ring<PB_BC_ABSORBING>,
                                "k_push_ring", ring_smem_bytes(), a, stream);
     KernFn fn = bc == PB_BC_PERIODIC
-                    ? (bgather ? k_push_quad<PB_BC_PERIODIC, 2>
+                    ? (bgather ? (bonly ? k_push_quad<PB_BC_PERIODIC, 2> : k_push_quad<PB_BC_PERIODIC, 3>)
                                : boris ? k_push_quad<PB_BC_PERIODIC, 1> : k_push_quad<PB_BC_PERIODIC, 0>)
-                    : (bgather ? k_push_quad<PB_BC_ABSORBING, 2>
+                    : (bgather ? (bonly ? k_push_quad<PB_BC_ABSORBING, 2> : k_push_quad<PB_BC_ABSORBING, 3>)
                                : boris ? k_push_quad<PB_BC_ABSORBING, 1> : k_push_quad<PB_BC_ABSORBING, 0>);
     return launch_persistent(fn, "k_push_quad", 0, a, stream);
   }

@@ -73,11 +73,13 @@ def reduce_bins(bins: torch.Tensor, group=None):
 
 
 def boris_coefficients(sp, consts, b_field) -> tuple:
-    """t = q B dt / (2 m), s = 2 t / (1 + |t|^2) (standard Boris rotation)."""
+    """t = q B dt / (2 m), s = t * (2 / (1 + |t|^2)) (standard Boris rotation;
+    one division, the form the gathered-B kernel evaluates per particle)."""
     f = sp.charge_c * consts.dt_s / (2.0 * sp.mass_kg)
     t = [f * float(b) for b in b_field]
     t2 = t[0] * t[0] + t[1] * t[1] + t[2] * t[2]
-    s = [2.0 * c / (1.0 + t2) for c in t]
+    g = 2.0 / (1.0 + t2)
+    s = [c * g for c in t]
     return t, s
 
 
