@@ -1173,7 +1173,10 @@ __device__ __forceinline__ void split_register_list(const LaunchArgs &a, int g, 
         win.gC = win.gR + a.nc;
       }
     }
-    quad_dispatch<BC, false>(a, isp, beg, end, win, t);
+    if (g == 0)  // list 0 is ring-eligible by construction: KICK, no yp, depositing
+      quad_chunk<PB_KIND_KICK, false, BC, true>(a, isp, beg, end, win, t);
+    else
+      quad_dispatch<BC, false>(a, isp, beg, end, win, t);
   }
 }
 
