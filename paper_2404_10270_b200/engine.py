@@ -520,24 +520,33 @@ class Engine:
         return (self.cfg.field_solve and self.fused_field and self.peer is None and self.poisson == "scan"
                 and not self._field_split()[0])
 
-    def _fused_cycle(self):
+    def _fused_cycle(self, rho_out=None):
         """pb_field_cycle on the engine stream (after the bin allreduce when
         N > 1): the density epilogue with the smoothing pass folded in, the
         scan Poisson solve and E, which also zeroes the bin set just read
-        (the push deposits into the other one, zeroed one step earlier)."""
+        (the push deposits into the other one, zeroed one step earlier).
+        rho_out: write the reported density (rho_s, or rho without
+        smoothing) there instead of the engine's own buffer (run_pipelined's
+        result slots: no snapshot copy)."""
         cfg = self.cfg
         read = self.bins_pp[self.cur]
+        rho_buf, rho_s_buf = self.rho, self.rho_s
+        if rho_out is not None:
+            if cfg.smoothing_passes > 0:
+                rho_s_buf = rho_out
+            else:
+                rho_buf = rho_out
         with torch.cuda.stream(self.stream):
             if self.world > 1:
                 reduce_bins(self.bins, self.group)
             _lib.check(self.lib.pb_field_cycle(
                 self.bins.data_ptr(), self._coef_c, self.ndep, self.nc, self.field_bc,
                 int(cfg.smoothing_passes), self.grid.dx_m, cfg.consts.epsilon0, cfg.phi_left, cfg.phi_right,
-                self.left.data_ptr(), self.right.data_ptr(), self.rho.data_ptr(), self.rho_s.data_ptr(),
+                self.left.data_ptr(), self.right.data_ptr(), rho_buf.data_ptr(), rho_s_buf.data_ptr(),
                 self.phi.data_ptr(), self.e.data_ptr(), read.data_ptr(), None, read.numel(),
                 self.status.data_ptr(), self.field_scratch.data_ptr(), self._sh()), "pb_field_cycle")
         self._next_clear = True
-        return (self.rho_s if cfg.smoothing_passes > 0 else self.rho), self.e
+        return (rho_s_buf if cfg.smoothing_passes > 0 else rho_buf), self.e
 
     def _compact(self):
         """Absorbing walls: fill the removed particles' slots from the tail (pb_compact)."""
@@ -545,8 +554,9 @@ class Engine:
         _lib.check(self.lib.pb_compact(arr, n, self.status.data_ptr(), self.compact_scratch.data_ptr(),
                                        self.compact_scratch.numel(), self._sh()), "pb_compact")
 
-    def _field_cycle(self):
-        """Field-solve step body.  The species that need no field (neutral
+    def _field_cycle(self, rho_out=None):
+        """Field-solve step body.  rho_out: see _fused_cycle (honoured on the
+        single-launch path only; check the returned tensor).  The species that need no field (neutral
         movers) are pushed on the engine stream while the density epilogue
         (and across GPUs its allreduce), smoothing, Poisson and E run on the
         side stream; the charged push then waits for E.  Without neutral
@@ -556,7 +566,7 @@ class Engine:
             if self._fused_ok():
                 # density + smoothing + scan Poisson + E + bin clears: one
                 # launch (pb_field_cycle), bitwise the per-phase kernels below
-                rho, e = self._fused_cycle()
+                rho, e = self._fused_cycle(rho_out)
             elif self.density_one and self.peer is None:
                 # one-kernel epilogue (no self-clear: neighbouring nodes read
                 # the same cells); E clears the bins (bitwise density())
@@ -723,11 +733,14 @@ class Engine:
 
     def _snap_counts(self, gp, j):
         """Absorbing runs: snapshot every species' device live count of step
-        slot (gp, j) (stream order: after the step's compaction)."""
+        slot (gp, j) (after the step's compaction), on the side stream so the
+        copies stay out of the engine stream's kernel chain (the graph joins
+        the side stream at its end; the next compaction comes a push later)."""
         if not self.absorbing:
             return
         P = self._pipe
-        with torch.cuda.stream(self.stream):
+        self._side.wait_stream(self.stream)
+        with torch.cuda.stream(self._side):
             for k, s in enumerate(self.sp):
                 P["nsnap"][gp, j, k:k + 1].copy_(s.n_dev, non_blocking=True)
 
@@ -808,6 +821,7 @@ class Engine:
                 with torch.cuda.stream(self.stream):
                     P["snap"][gp, 0].copy_(rho, non_blocking=True)
                 self._snap_counts(gp, 0)
+                self.stream.wait_stream(self._side)  # the count copies ran on the side stream
             with torch.cuda.stream(self.stream):
                 ev = torch.cuda.Event()
                 ev.record(self.stream)
@@ -851,19 +865,22 @@ class Engine:
                     prev = done
                     self.push(P["e"][gp, j] if with_input else self.e)
                 else:
-                    rho, e = self._field_cycle()
+                    # the single-launch field step writes the reported density
+                    # straight into the result slot
+                    rho, e = self._field_cycle(rho_out=P["snap"][gp, j])
                 if self.absorbing:
                     self._compact()
                 self._snap_counts(gp, j)
-                if overlap:
-                    snap_stream = self._side  # rho_j is final once epilogue j is done
-                else:
-                    if self._field_split()[0]:
-                        self.stream.wait_stream(self._side)
-                    snap_stream = self.stream
-                with torch.cuda.stream(snap_stream):
-                    P["snap"][gp, j].copy_(rho, non_blocking=True)
-            if overlap or self._field_split()[0]:
+                if rho.data_ptr() != P["snap"][gp, j].data_ptr():
+                    if overlap:
+                        snap_stream = self._side  # rho_j is final once epilogue j is done
+                    else:
+                        if self._field_split()[0]:
+                            self.stream.wait_stream(self._side)
+                        snap_stream = self.stream
+                    with torch.cuda.stream(snap_stream):
+                        P["snap"][gp, j].copy_(rho, non_blocking=True)
+            if overlap or self._field_split()[0] or self.absorbing:
                 self.stream.wait_stream(self._side)  # join the forked side stream
         # capture advanced the host-side parity; replay() of this graph does
         # the same, so restore it and let the caller account the steps
