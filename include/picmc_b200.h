@@ -78,7 +78,7 @@ typedef struct pb_species {
   double fnstep;            /* float(nstep) (mover.py:248)                */
   double kick_coef;         /* q dt^2/(m dx), velocity_kick_coef (mover.py:38-40) */
   double boris_t[3];        /* q B dt / (2 m)                             */
-  double boris_s[3];        /* 2 t / (1 + |t|^2)                          */
+  double boris_s[3];        /* t * (2 / (1 + |t|^2))                      */
   /* Optional compressed cell index read by the production mover instead of
    * `cell` (1 byte instead of 4 per charged particle): cell8[i] =
    * cell[i] - chunk_base[i / PB_CELL8_CHUNK], or PB_CELL8_ESCAPE when that
@@ -96,7 +96,7 @@ typedef struct pb_species {
    * j at cell-relative x (pre-push), with f = boris_f = q dt / (2 m):
    *   t_k = f*B_k[j] + x*(f*B_k[j+1] - f*B_k[j])   (the one-sided gather
    *                                                  of accel_nodes, mover.py:221)
-   *   s_k = (2*t_k) / (1 + ((t_x*t_x + t_y*t_y) + t_z*t_z))
+   *   s_k = t_k * (2 / (1 + ((t_x*t_x + t_y*t_y) + t_z*t_z)))
    * each operation rounded separately (no FMA), restated in
    * oracle/picmc_oracle.c:boris_t_gather. */
   const double *b_nodes;
