@@ -280,13 +280,18 @@ int pb_compute_efield_clear(const double *phi, double *e, int64_t nc,
  * ceil((nc-1)/512) tiles fit co-resident on the device, else as kernels.
  * `scratch` needs pb_field_scratch_bytes(nc) bytes, ZEROED before its first
  * use (its two counter words return to zero after every launch); left /
- * right may be NULL. */
+ * right may be NULL.  compact_sp / compact_nsp (NULL / 0: none): also
+ * pb_compact those species (the previous step's absorbing-wall holes;
+ * compact_scratch as pb_compact's) -- extra blocks of the same launch,
+ * independent of the field work. */
 int pb_field_cycle(const uint64_t *bins, const double *coef, int ndep,
                    int64_t nc, int field_bc, int passes, double dx,
                    double eps0, double phi_left, double phi_right,
                    double *left, double *right, double *rho, double *rho_s,
                    double *phi, double *e, uint64_t *clr_a, uint64_t *clr_b,
                    int64_t nwords, pb_status *status_or_null, void *scratch,
+                   const pb_species *compact_sp, int compact_nsp,
+                   void *compact_scratch, size_t compact_scratch_bytes,
                    void *stream);
 
 /* Roofline probe: streams the mover's exact read/write bytes per species with

@@ -150,7 +150,8 @@ _SIGS = {
     "pb_compute_efield": (ctypes.c_int, [_p, _p, _i64, _f64, ctypes.c_int, _p]),
     "pb_compute_efield_clear": (ctypes.c_int, [_p, _p, _i64, _f64, ctypes.c_int, _p, _p, _i64, _p]),
     "pb_field_cycle": (ctypes.c_int, [_p, _p, ctypes.c_int, _i64, ctypes.c_int, ctypes.c_int, _f64, _f64, _f64,
-                                      _f64, _p, _p, _p, _p, _p, _p, _p, _p, _i64, _p, _p, _p]),
+                                      _f64, _p, _p, _p, _p, _p, _p, _p, _p, _i64, _p, _p,
+                                      ctypes.POINTER(PbSpecies), ctypes.c_int, _p, ctypes.c_size_t, _p]),
     "pb_stream_sol": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_int, _p]),
     "pb_init_species": (ctypes.c_int, [ctypes.POINTER(PbSpecies), ctypes.c_uint64,
                                        _i64, _i64, _i64, _f64, _p]),

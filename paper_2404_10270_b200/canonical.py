@@ -46,6 +46,7 @@ class CanonicalEngine(Engine):
 
     supports_collisions = True
     supports_peer = False  # its density allreduces fp64 partials (exact, rank order)
+    fold_compaction = False  # its own resort
     use_cell8 = False  # the canonical kernels read the full cell index
 
     def __init__(self, config, device=None, *, rank: int = 0, world: int = 1, group=None,

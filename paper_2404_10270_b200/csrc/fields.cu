@@ -8,6 +8,7 @@
 // operation -- including NumPy's pairwise summation inside np.mean -- on one
 // thread, so a given rho yields a bitwise-identical phi.
 #include "common.cuh"
+#include "compact.cuh"
 #include "density.cuh"
 
 #include <cstring>
@@ -500,6 +501,9 @@ struct FieldArgs {
   int64_t nwords;
   double two_dx;
   pb_status *st;
+  // absorbing walls: the previous step's holes are filled by cpt.nsp extra
+  // blocks of the same launch (blockIdx >= G), independent of the field work
+  CompactArgs cpt;
 };
 
 struct Window {
@@ -643,13 +647,27 @@ __global__ void __launch_bounds__(kMbThreads) k_field_fused(const __grid_constan
 #else
   pdl_enter();
 #endif
-  FF_MARK(0);
-  __shared__ Window win;
+  __shared__ union {
+    Window win;
+    CompactSmem<kMbThreads> cpt;
+  } su;
+  Window &win = su.win;
   __shared__ Agg sm_agg[kMbWarps];
   __shared__ Agg s_pre[4];
   __shared__ double px[kMbTile + 2];
   const ScanArgs &sa = a.sa;
   const int t = blockIdx.x, G = sa.G;
+  if (t >= G) {  // a compaction block: the previous step's holes of one species
+    compact_species<kMbThreads>(a.cpt, t - G, su.cpt);
+    __syncthreads();
+    if (threadIdx.x == 0 &&
+        atomicAdd((unsigned long long *)&a.sync[1], 1ull) == (unsigned long long)(G + a.cpt.nsp - 1)) {
+      a.sync[0] = 0;
+      a.sync[1] = 0;
+    }
+    return;
+  }
+  FF_MARK(0);
   const int64_t nc = sa.nc, base = (int64_t)t * kMbTile;
   const int64_t kend = base + kMbTile < sa.n ? base + kMbTile : sa.n;
   const bool periodic = sa.field_bc == PB_FIELD_PERIODIC;
@@ -730,7 +748,7 @@ __global__ void __launch_bounds__(kMbThreads) k_field_fused(const __grid_constan
   __syncthreads();
   FF_MARK(7);
   if (threadIdx.x == 0 &&
-      atomicAdd((unsigned long long *)&a.sync[1], 1ull) == (unsigned long long)(G - 1)) {
+      atomicAdd((unsigned long long *)&a.sync[1], 1ull) == (unsigned long long)(G + a.cpt.nsp - 1)) {
     a.sync[0] = 0;
     a.sync[1] = 0;
   }
@@ -944,7 +962,8 @@ extern "C" int pb_field_cycle(const uint64_t *bins, const double *coef, int ndep
                               double phi_right, double *left, double *right, double *rho,
                               double *rho_s, double *phi, double *e, uint64_t *clr_a,
                               uint64_t *clr_b, int64_t nwords, pb_status *status, void *scratch,
-                              void *stream) {
+                              const pb_species *compact_sp, int compact_nsp, void *compact_scratch,
+                              size_t compact_scratch_bytes, void *stream) {
   if (nc < 3 || ndep < 0 || ndep > PB_MAX_SPECIES || (ndep > 0 && (!bins || !coef)) || !rho ||
       !rho_s || !phi || !e || !scratch || nwords < 0) {
     pb::set_error("pb_field_cycle: bad arguments (nc=%lld ndep=%d)", (long long)nc, ndep);
@@ -960,6 +979,16 @@ extern "C" int pb_field_cycle(const uint64_t *bins, const double *coef, int ndep
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nw = (clr_a || clr_b) ? nwords : 0;
+  pb::CompactArgs cpt;
+  memset(&cpt, 0, sizeof(cpt));
+  if (compact_nsp > 0) {
+    if (!status) {
+      pb::set_error("pb_field_cycle: compaction needs the status");
+      return PB_ERR_INVALID;
+    }
+    const int rc = pb::compact_args(compact_sp, compact_nsp, status, compact_scratch, compact_scratch_bytes, cpt);
+    if (rc) return rc;
+  }
   if (passes <= pb::kFfMaxPasses) {
     const pb::FieldScratch fl = pb::field_scratch_layout(nc);
     pb::FieldArgs a;
@@ -981,21 +1010,28 @@ extern "C" int pb_field_cycle(const uint64_t *bins, const double *coef, int ndep
     a.nwords = nw;
     a.two_dx = 2.0 * dx;
     a.st = status;
-    if (fl.G <= pb::field_fused_max_grid()) {  // one launch
-      cudaError_t err = pb::launch_pdl(pb::k_field_fused, dim3(fl.G), dim3(pb::kMbThreads), 0, st, a);
+    a.cpt = cpt;
+    if (fl.G + cpt.nsp <= pb::field_fused_max_grid()) {  // one launch
+      cudaError_t err =
+          pb::launch_pdl(pb::k_field_fused, dim3(fl.G + cpt.nsp), dim3(pb::kMbThreads), 0, st, a);
       if (err != cudaSuccess) return pb::cuda_status(err, "k_field_fused");
       return PB_OK;
     }
+    a.cpt.nsp = 0;  // the kernels below take no compaction blocks
     // too many tiles to be co-resident: the same phases as kernels
     cudaError_t err = pb::launch_pdl(pb::k_field_window, dim3(fl.G), dim3(pb::kMbThreads), 0, st, a);
     if (err != cudaSuccess) return pb::cuda_status(err, "k_field_window");
     int rc = scan_solve(rho_s, phi, a.sa, st, false);
     if (!rc) rc = pb_compute_efield_clear(phi, e, nc, dx, field_bc, clr_a, clr_b, nw, stream);
+    if (!rc && cpt.nsp > 0)
+      rc = pb_compact(compact_sp, compact_nsp, status, compact_scratch, compact_scratch_bytes, stream);
     return rc;
   }
   int rc = pb_rho_epilogue(bins, coef, ndep, nc, field_bc, left, right, rho, status, stream);
   if (!rc) rc = pb_smooth_density(rho, rho_s, nc, passes, scratch, stream);
   if (!rc) rc = pb_solve_poisson_scan(rho_s, phi, nc, dx, eps0, field_bc, phi_left, phi_right, scratch, stream);
   if (!rc) rc = pb_compute_efield_clear(phi, e, nc, dx, field_bc, clr_a, clr_b, nw, stream);
+  if (!rc && cpt.nsp > 0)
+    rc = pb_compact(compact_sp, compact_nsp, status, compact_scratch, compact_scratch_bytes, stream);
   return rc;
 }

@@ -17,6 +17,9 @@
 #include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
+#include "compact.cuh"
+
+#include <cstring>
 
 namespace pb {
 
@@ -82,10 +85,6 @@ __global__ void k_cell_scatter(const __grid_constant__ ScatterArgs a) {
   }
 }
 
-__device__ __forceinline__ int8_t cell8_of(int32_t cell, int32_t base) {
-  const int32_t d = cell - base;
-  return (cell >= 0 && d > PB_CELL8_ESCAPE && d <= 127) ? (int8_t)d : (int8_t)PB_CELL8_ESCAPE;
-}
 
 // chunk_base = first cell of each PB_CELL8_CHUNK-slot chunk minus a margin
 // (cell-sorted chunks then fit in int8 offsets with room for drift);
@@ -109,70 +108,44 @@ static size_t scan_temp_bytes(int64_t nc) {
   return t;
 }
 
-// ---- absorbing-wall compaction -------------------------------------------
+// ---- absorbing-wall compaction (compact.cuh) -------------------------------
 constexpr int kCompactThreads = 1024;
 
-struct CompactArgs {
-  pb_species sp[PB_MAX_SPECIES];
-  int id[PB_MAX_SPECIES];
-  int nsp;
-  int64_t *tail;  // scratch: per species, cap entries
-  int64_t tail_stride;
-  pb_status *st;
-};
-
-// One block per species: the survivors in the tail [n-k, n) fill the holes
-// below n-k.  Tail survivors are enumerated in slot order with a block scan
-// over warp ballots; holes are consumed through a cursor.
 __global__ void __launch_bounds__(kCompactThreads)
     k_compact(const __grid_constant__ CompactArgs a) {
   pdl_enter();
-  using Scan = cub::BlockScan<int, kCompactThreads>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ int64_t s_cnt;
-  __shared__ unsigned long long s_cursor;
-  const int isp = blockIdx.x;
-  if (isp >= a.nsp) return;
-  const pb_species &s = a.sp[isp];
-  const int sid = a.id[isp];
-  const int64_t n = *s.n_dev;
-  const int64_t k = a.st->n_holes[sid];
-  if (k <= 0) return;
-  const int64_t n2 = n - k;
-  int64_t *tail = a.tail + (size_t)isp * a.tail_stride;
-  if (threadIdx.x == 0) {
-    s_cnt = 0;
-    s_cursor = 0;
+  __shared__ CompactSmem<kCompactThreads> sm;
+  if ((int)blockIdx.x < a.nsp) compact_species<kCompactThreads>(a, blockIdx.x, sm);
+}
+
+int compact_args(const pb_species *sp, int nsp, pb_status *status, void *scratch, size_t scratch_bytes,
+                 CompactArgs &a) {
+  memset(&a, 0, sizeof(a));
+  if (nsp < 0 || nsp > PB_MAX_SPECIES || !status) {
+    set_error("pb_compact: bad arguments");
+    return PB_ERR_INVALID;
   }
-  __syncthreads();
-  for (int64_t b = n2; b < n; b += kCompactThreads) {
-    const int64_t i = b + threadIdx.x;
-    const int alive = (i < n && s.cell[i] >= 0) ? 1 : 0;
-    int pos, total;
-    Scan(tmp).ExclusiveSum(alive, pos, total);
-    if (alive) tail[s_cnt + pos] = i;
-    __syncthreads();
-    if (threadIdx.x == 0) s_cnt += total;
-    __syncthreads();
+  int64_t nmax = 1;
+  for (int k = 0; k < nsp; ++k) {
+    if (sp[k].kind == PB_KIND_INACTIVE || sp[k].n <= 0) continue;
+    if (!sp[k].n_dev || !sp[k].holes) {
+      set_error("pb_compact: species %d lacks n_dev/holes", k);
+      return PB_ERR_INVALID;
+    }
+    a.sp[a.nsp] = sp[k];
+    a.id[a.nsp] = k;
+    a.nsp++;
+    if (sp[k].n > nmax) nmax = sp[k].n;
   }
-  for (int64_t j = threadIdx.x; j < k; j += kCompactThreads) {
-    const int64_t h = s.holes[j];
-    if (h >= n2) continue;
-    const unsigned long long t = atomicAdd(&s_cursor, 1ull);
-    const int64_t src = tail[t];
-    s.x[h] = s.x[src];
-    s.vx[h] = s.vx[src];
-    s.vy[h] = s.vy[src];
-    s.vz[h] = s.vz[src];
-    if (s.yp) s.yp[h] = s.yp[src];
-    s.cell[h] = s.cell[src];
-    if (s.cell8) s.cell8[h] = cell8_of(s.cell[src], s.chunk_base[h / PB_CELL8_CHUNK]);
+  if (a.nsp == 0) return PB_OK;
+  if (!scratch || scratch_bytes < (size_t)a.nsp * (size_t)nmax * sizeof(int64_t)) {
+    set_error("pb_compact: scratch too small");
+    return PB_ERR_INVALID;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    *s.n_dev = n2;
-    a.st->n_holes[sid] = 0;
-  }
+  a.tail = (int64_t *)scratch;
+  a.tail_stride = nmax;
+  a.st = status;
+  return PB_OK;
 }
 
 }  // namespace pb
@@ -241,32 +214,9 @@ extern "C" size_t pb_compact_scratch_bytes(int64_t n) {
 
 extern "C" int pb_compact(const pb_species *sp, int nsp, pb_status *status,
                           void *scratch, size_t scratch_bytes, void *stream) {
-  if (nsp < 0 || nsp > PB_MAX_SPECIES || !status) {
-    pb::set_error("pb_compact: bad arguments");
-    return PB_ERR_INVALID;
-  }
   pb::CompactArgs a;
-  memset(&a, 0, sizeof(a));
-  int64_t nmax = 1;
-  for (int k = 0; k < nsp; ++k) {
-    if (sp[k].kind == PB_KIND_INACTIVE || sp[k].n <= 0) continue;
-    if (!sp[k].n_dev || !sp[k].holes) {
-      pb::set_error("pb_compact: species %d lacks n_dev/holes", k);
-      return PB_ERR_INVALID;
-    }
-    a.sp[a.nsp] = sp[k];
-    a.id[a.nsp] = k;
-    a.nsp++;
-    if (sp[k].n > nmax) nmax = sp[k].n;
-  }
-  if (a.nsp == 0) return PB_OK;
-  if (!scratch || scratch_bytes < (size_t)a.nsp * (size_t)nmax * sizeof(int64_t)) {
-    pb::set_error("pb_compact: scratch too small");
-    return PB_ERR_INVALID;
-  }
-  a.tail = (int64_t *)scratch;
-  a.tail_stride = nmax;
-  a.st = status;
+  const int rc = pb::compact_args(sp, nsp, status, scratch, scratch_bytes, a);
+  if (rc || a.nsp == 0) return rc;
   cudaError_t le = pb::launch_pdl(pb::k_compact, dim3(a.nsp), dim3(pb::kCompactThreads), 0,
                                   (cudaStream_t)stream, a);
   if (le != cudaSuccess) return pb::cuda_status(le, "k_compact");

@@ -146,6 +146,11 @@ class Engine:
     # field-solve steps with the scan Poisson: the whole field step in one
     # launch with grid barriers (pb_field_cycle) instead of 6-10 kernels
     fused_field = True
+    # absorbing walls on the single-launch field path: a step's holes are
+    # filled by compaction blocks of the NEXT step's field launch (no separate
+    # launch); anything that looks at the stores first compacts eagerly
+    # (_flush_holes), and a due sort compacts before it sorts
+    fold_compaction = True
 
     def __init__(self, config, device=None, *, rank: int = 0, world: int = 1,
                  group=None, init: str = "host", check_every: int = 1, peer: bool = None):
@@ -364,6 +369,7 @@ class Engine:
 
     def upload(self, flats: list):
         """Replace the particle state with host arrays (engine flat layout)."""
+        self._flush_holes()  # no pending holes may reach the new state
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(self.stream):
             for s, f in zip(self.sp, flats):
@@ -544,9 +550,29 @@ class Engine:
                 int(cfg.smoothing_passes), self.grid.dx_m, cfg.consts.epsilon0, cfg.phi_left, cfg.phi_right,
                 self.left.data_ptr(), self.right.data_ptr(), rho_buf.data_ptr(), rho_s_buf.data_ptr(),
                 self.phi.data_ptr(), self.e.data_ptr(), read.data_ptr(), None, read.numel(),
-                self.status.data_ptr(), self.field_scratch.data_ptr(), self._sh()), "pb_field_cycle")
+                self.status.data_ptr(), self.field_scratch.data_ptr(), *self._fold_args(), self._sh()),
+                "pb_field_cycle")
         self._next_clear = True
         return (rho_s_buf if cfg.smoothing_passes > 0 else rho_buf), self.e
+
+    def _folds_compaction(self) -> bool:
+        """The field launch compacts the previous step's holes (see
+        fold_compaction)."""
+        return self.absorbing and self.fold_compaction and self._fused_ok()
+
+    def _fold_args(self):
+        """pb_field_cycle's compaction arguments: the species (their holes
+        from the previous push) when the launch folds the compaction in."""
+        if not self._folds_compaction():
+            return (None, 0, None, 0)
+        arr, n = self._species()
+        return (arr, n, self.compact_scratch.data_ptr(), self.compact_scratch.numel())
+
+    def _flush_holes(self):
+        """Fill pending absorbing-wall holes now (idempotent: nothing to do
+        when the last push removed nothing or they were filled already)."""
+        if self._folds_compaction():
+            self._compact()
 
     def _compact(self):
         """Absorbing walls: fill the removed particles' slots from the tail (pb_compact)."""
@@ -618,15 +644,18 @@ class Engine:
 
     def resort(self):
         with torch.cuda.stream(self.stream):
-            if self.absorbing:
-                self._compact()
             due = self._sorts_due(1)
+            # folded compaction: the next field launch fills the holes, unless
+            # a sort comes first
+            if self.absorbing and (due or not self._folds_compaction()):
+                self._compact()
             if due:
                 self.sort_by_cell(due)
 
     def sort_by_cell(self, which=None):
         """Radix sort species (all, or the indices in `which`) by cell into
         their spare buffers and swap."""
+        self._flush_holes()
         with torch.cuda.stream(self.stream):
             for k, s in enumerate(self.sp):
                 if which is not None and k not in which:
@@ -817,6 +846,7 @@ class Engine:
                 self.step_index += n
             else:
                 rho, _ = self.step(e_ext=P["e"][gp, 0] if with_input else None)
+                self._flush_holes()  # the live-count snapshot is post-compaction
                 self.stream.wait_stream(self._side)  # rho may come from the side stream
                 with torch.cuda.stream(self.stream):
                     P["snap"][gp, 0].copy_(rho, non_blocking=True)
@@ -918,8 +948,8 @@ class Engine:
                     self.push(self.field(rho))
                 else:
                     self._field_cycle()
-                if self.absorbing:
-                    self._compact()
+                if self.absorbing and not self._folds_compaction():
+                    self._compact()  # else: the next field launch fills this step's holes
             if prev is not None:
                 self.stream.wait_event(prev)
             if not overlap and self._field_split()[0]:
@@ -1047,6 +1077,7 @@ class Engine:
         host tallies, raise the first recorded error, and reset the status.
         window=(first, last): the steps run since the previous sync, named
         in error messages when the status was not checked every step."""
+        self._flush_holes()
         self.stream.synchronize()
         self._side.synchronize()
         raw = self.status.cpu().numpy()
@@ -1084,9 +1115,11 @@ class Engine:
             raise EngineError(f"step {self.step_index}: device status {st.code}")
 
     def totals(self) -> list:
+        self._flush_holes()
         return [s.live_count() for s in self.sp]
 
     def download(self) -> list:
+        self._flush_holes()
         self.stream.synchronize()
         return [s.download() for s in self.sp]
 

@@ -52,7 +52,7 @@ def _chain(lib, bins, coef, ndep, nc, bc, passes, dx, eps0, pl, pr, dev, fused):
             b1.copy_(torch.from_numpy(bins.view(np.int64)))
             _lib.check(lib.pb_field_cycle(P(b0), c, ndep, nc, bc, passes, dx, eps0, pl, pr, P(out["left"]),
                                           P(out["right"]), P(out["rho"]), P(out["rho_s"]), P(out["phi"]),
-                                          P(out["e"]), P(b0), P(b1), b0.numel(), P(st), P(scr), sh),
+                                          P(out["e"]), P(b0), P(b1), b0.numel(), P(st), P(scr), None, 0, None, 0, sh),
                        "pb_field_cycle")
     else:
         _lib.check(lib.pb_rho_epilogue(P(b0), c, ndep, nc, bc, P(out["left"]), P(out["right"]), P(out["rho"]),
@@ -196,7 +196,7 @@ def test_field_cycle_epochs_and_graph_replay(cuda, bc):
         b0.copy_(src)
         _lib.check(lib.pb_field_cycle(P(b0), c, ndep, nc, code, passes, 1e-5, 8.8541878128e-12, 1.0, 0.0,
                                       P(left), P(right), P(out["rho"]), P(out["rho_s"]), P(out["phi"]),
-                                      P(out["e"]), P(b0), None, b0.numel(), P(st), P(scr),
+                                      P(out["e"]), P(b0), None, b0.numel(), P(st), P(scr), None, 0, None, 0,
                                       ctypes.c_void_p(stream.cuda_stream)), "pb_field_cycle")
 
     s = torch.cuda.Stream(cuda)
