@@ -454,6 +454,7 @@ def run_ours(args, rank, world, local_rank):
                 "peer memory: pb_peer_density_step (bins summed over NVLink/IPC + epilogue, one kernel)"
                 if eng.peer is not None else
                 f"{args.dist_backend} all_reduce of the fixed-point bins + pb_density_step")
+    folded = eng._folds_compaction()  # walls compacted inside the field launch
     eng.close()
     del eng
     torch.cuda.empty_cache()
@@ -478,7 +479,7 @@ def run_ours(args, rank, world, local_rank):
     # field solve: the mover + k_field_fused (density, smoothing, Poisson, E
     # in one launch); walls: + k_compact
     launches_per_step = 2 if cfg.field_solve else 3
-    if cfg.particle_boundary == "absorbing":
+    if cfg.particle_boundary == "absorbing" and not folded:
         launches_per_step += 1
     # our kernels per sort: k_cell_count + k_cell_scatter (+ k_cell8_build
     # where the compressed cell index is kept); the scan is CUB's
