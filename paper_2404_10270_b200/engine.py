@@ -266,6 +266,7 @@ class Engine:
         self._sub_cache = {}
         self.graphs = {}
         self._next_clear = False
+        self._holes_pending = False  # folded compaction: the last push's holes await a field launch
         # Mover work counter (pb_status.tile_next; self-resetting in the kernel).
         off = _lib.PbStatus.tile_next.offset
         self._tile_counter = self.status[off:off + 8]
@@ -552,6 +553,8 @@ class Engine:
                 self.phi.data_ptr(), self.e.data_ptr(), read.data_ptr(), None, read.numel(),
                 self.status.data_ptr(), self.field_scratch.data_ptr(), *self._fold_args(), self._sh()),
                 "pb_field_cycle")
+        if self._folds_compaction():
+            self._holes_pending = False
         self._next_clear = True
         return (rho_s_buf if cfg.smoothing_passes > 0 else rho_buf), self.e
 
@@ -569,9 +572,9 @@ class Engine:
         return (arr, n, self.compact_scratch.data_ptr(), self.compact_scratch.numel())
 
     def _flush_holes(self):
-        """Fill pending absorbing-wall holes now (idempotent: nothing to do
-        when the last push removed nothing or they were filled already)."""
-        if self._folds_compaction():
+        """Fill pending absorbing-wall holes now: the last push's holes when
+        no field launch has folded them in yet."""
+        if self._holes_pending:
             self._compact()
 
     def _compact(self):
@@ -579,6 +582,7 @@ class Engine:
         arr, n = self._species()
         _lib.check(self.lib.pb_compact(arr, n, self.status.data_ptr(), self.compact_scratch.data_ptr(),
                                        self.compact_scratch.numel(), self._sh()), "pb_compact")
+        self._holes_pending = False
 
     def _field_cycle(self, rho_out=None):
         """Field-solve step body.  rho_out: see _fused_cycle (honoured on the
@@ -627,6 +631,7 @@ class Engine:
         launch of the same step)."""
         if e is None:
             e = self.e
+        self._flush_holes()  # a direct push() after a step: no holes may be pushed
         arr, n = self._species() if subset is None else self._subset(subset)
         target = self.bins_pp[1 - self.cur]
         with torch.cuda.stream(self.stream):
@@ -638,6 +643,8 @@ class Engine:
                                                 self.status.data_ptr(), self._sh()), "pb_push_deposit")
             if self._timing is not None and subset is None:
                 self._timing[1].record(self.stream)
+        if self._folds_compaction():
+            self._holes_pending = True  # filled by the next field launch (or _flush_holes)
         if flip:
             self.cur = 1 - self.cur
             self._next_clear = False
@@ -841,6 +848,7 @@ class Engine:
                 with torch.cuda.stream(self.stream):
                     g.replay()
                 self._epi_prev = None
+                self._holes_pending = False  # pipe graphs compact every step (live-count snapshots)
                 self.cur ^= n & 1  # each replayed push deposited into the other set
                 self._next_clear = False
                 self.step_index += n
@@ -1046,6 +1054,7 @@ class Engine:
                     with torch.cuda.stream(self.stream):
                         g.replay()
                     self._epi_prev = None  # the graph joined its epilogues
+                    self._holes_pending = self._folds_compaction()  # its last push's holes
                     self.step_index += 2
                     left -= 2
                 else:

@@ -218,3 +218,42 @@ def test_field_cycle_epochs_and_graph_replay(cuda, bc):
         for k in ("rho", "rho_s", "phi", "e"):
             assert bits_equal(ref[k], out[k].cpu().numpy()), (it, k)
         assert not b0.any().item()
+
+
+def test_folded_compaction_flushes_before_direct_push_and_reads(cuda):
+    """Absorbing walls on the single-launch field path: a step leaves its
+    holes to the next field launch.  A direct push() / totals() / download()
+    / sort in between must see (and push) compacted stores only: same
+    particles, counts and tallies as the engine that compacts every step."""
+    from paper_2404_10270_b200 import Engine
+
+    kw = dict(field_solve=True, smoothing_passes=1, poisson="scan", boundary="dirichlet",
+              particle_boundary="absorbing", phi_left=0.0, phi_right=0.0)
+    cfg = _mk_config(nc=2000, ppc0=8, **kw)
+    flats = _random_flats(cfg, 5, vscale=0.9)  # fast particles: many wall removals
+    a = Engine(cfg, device=cuda, check_every=0)
+    b = Engine(cfg, device=cuda, check_every=0)
+    b.fold_compaction = False
+    assert a._folds_compaction() and not b._folds_compaction()
+    a.upload(flats)
+    b.upload(flats)
+    for _ in range(3):
+        a.step()
+        b.step()
+    assert a._holes_pending
+    assert a.totals() == b.totals()  # flushes a's holes
+    for _ in range(2):
+        a.step()
+        b.step()
+    a.push()  # direct push with the last step's holes pending
+    b.push()
+    a.sort_by_cell()
+    b.sort_by_cell()
+    a.sync()
+    b.sync()
+    assert np.array_equal(a.absorbed, b.absorbed) and a.absorbed.sum() > 0
+    from oracle import oracle
+
+    for x, y in zip(a.download(), b.download()):
+        assert x.n == y.n
+        assert np.array_equal(oracle.canonical(x.cell, x.fields()), oracle.canonical(y.cell, y.fields()))
