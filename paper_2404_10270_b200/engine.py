@@ -266,7 +266,7 @@ class Engine:
         self._sub_cache = {}
         self.graphs = {}
         self._next_clear = False
-        self._holes_pending = False  # folded compaction: the last push's holes await a field launch
+        self._holes_pending = False  # absorbing walls: the last push's holes are not filled yet
         # Mover work counter (pb_status.tile_next; self-resetting in the kernel).
         off = _lib.PbStatus.tile_next.offset
         self._tile_counter = self.status[off:off + 8]
@@ -643,8 +643,9 @@ class Engine:
                                                 self.status.data_ptr(), self._sh()), "pb_push_deposit")
             if self._timing is not None and subset is None:
                 self._timing[1].record(self.stream)
-        if self._folds_compaction():
-            self._holes_pending = True  # filled by the next field launch (or _flush_holes)
+        if self.absorbing:
+            # filled by resort(), the next folded field launch, or _flush_holes
+            self._holes_pending = True
         if flip:
             self.cur = 1 - self.cur
             self._next_clear = False
