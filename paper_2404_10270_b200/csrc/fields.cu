@@ -513,8 +513,7 @@ struct Window {
 
 // rho (+ smoothing) of tile t's window; writes the owned left / right / rho /
 // rho_s; returns sw with sw[i] = rho_s at node base + i, i in [0, 514).
-__device__ const double *window_rho(const FieldArgs &a, int t, Window &w) {
-  const ScanArgs &sa = a.sa;
+__device__ __forceinline__ const double *window_rho(const FieldArgs &a, const ScanArgs &sa, int t, Window &w) {
   const int64_t nc = sa.nc;
   const int P = a.passes;
   const bool periodic = sa.field_bc == PB_FIELD_PERIODIC;
@@ -641,6 +640,10 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
 #ifndef PB_FF_LATE_TRIGGER
 #define PB_FF_LATE_TRIGGER 1
 #endif
+// PER: the boundary condition as a compile-time constant (one instantiation
+// each): the kernel runs once per step, cold in the instruction cache after
+// the mover, so the code it does not need stays out of its path.
+template <bool PER>
 __global__ void __launch_bounds__(kMbThreads) k_field_fused(const __grid_constant__ FieldArgs a) {
 #if PB_FF_LATE_TRIGGER
   pdl_wait();  // the dependent (the mover) is released after the solve, below
@@ -655,7 +658,8 @@ __global__ void __launch_bounds__(kMbThreads) k_field_fused(const __grid_constan
   __shared__ Agg sm_agg[kMbWarps];
   __shared__ Agg s_pre[4];
   __shared__ double px[kMbTile + 2];
-  const ScanArgs &sa = a.sa;
+  ScanArgs sa = a.sa;
+  sa.field_bc = PER ? PB_FIELD_PERIODIC : PB_FIELD_DIRICHLET;  // folded at compile time
   const int t = blockIdx.x, G = sa.G;
   if (t >= G) {  // a compaction block: the previous step's holes of one species
     compact_species<kMbThreads>(a.cpt, t - G, su.cpt);
@@ -672,7 +676,7 @@ __global__ void __launch_bounds__(kMbThreads) k_field_fused(const __grid_constan
   const int64_t kend = base + kMbTile < sa.n ? base + kMbTile : sa.n;
   const bool periodic = sa.field_bc == PB_FIELD_PERIODIC;
 
-  const double *sw = window_rho(a, t, win);  // (synchronises the CTA)
+  const double *sw = window_rho(a, sa, t, win);  // (synchronises the CTA)
   FF_MARK(1);
   auto rs = [sw, base](int64_t j) { return sw[j - base]; };
   TileLocal L;
@@ -762,7 +766,7 @@ __global__ void __launch_bounds__(kMbThreads) k_field_window(const __grid_consta
   __shared__ Agg sm_agg[kMbWarps];
   const int t = blockIdx.x;
   const int64_t base = (int64_t)t * kMbTile;
-  const double *sw = window_rho(a, t, win);
+  const double *sw = window_rho(a, a.sa, t, win);
   TileLocal L;
   tile_local(a.sa, t, [sw, base](int64_t j) { return sw[j - base]; }, sm_agg, L);
   if (threadIdx.x == 0) a.sa.agg[t] = L.tot;
@@ -790,17 +794,39 @@ static FieldScratch field_scratch_layout(int64_t nc) {
   return f;
 }
 
-// largest grid of k_field_fused that is co-resident on this device
-static int field_fused_max_grid() {
-  static int cached = -1;
-  if (cached < 0) {
-    int dev = 0, sms = 0, per = 0;
+// Placement of k_field_fused: its blocks are latency chains, so they should
+// sit one (or as few as possible) per SM -- launched early behind the mover
+// (PDL), they would otherwise pile up on the first SMs the mover frees (up to
+// four per SM measured, the field step 9.4 -> 11.9 us).  Dynamic shared
+// memory pads each block so at most k = ceil(grid / SMs) fit on an SM.
+// Returns the padding (bytes) for `grid` blocks, or -1 when the grid cannot
+// be co-resident at all.
+static int field_fused_pad(int grid, bool periodic) {
+  static int sms = -1, static_smem[2] = {0, 0}, per_sm_smem = 0, max_optin = 0;
+  if (sms < 0) {
+    int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_field_fused, kMbThreads, 0);
-    cached = sms * per;
+    cudaDeviceGetAttribute(&per_sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    for (int p = 0; p < 2; ++p) {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, p ? (const void *)k_field_fused<true> : (const void *)k_field_fused<false>);
+      static_smem[p] = (int)fa.sharedSizeBytes;
+      cudaFuncSetAttribute(p ? (const void *)k_field_fused<true> : (const void *)k_field_fused<false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin - (int)fa.sharedSizeBytes);
+    }
   }
-  return cached;
+  const int k = (grid + sms - 1) / sms;  // blocks per SM wanted
+  const int reserve = 1024;              // per-block system shared memory
+  // the per-block footprint must exceed per_sm / (k + 1)
+  int pad = per_sm_smem / (k + 1) + 1 - reserve - static_smem[periodic ? 1 : 0];
+  if (pad < 0) pad = 0;
+  if (pad > max_optin - static_smem[periodic ? 1 : 0]) pad = max_optin - static_smem[periodic ? 1 : 0];
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per, periodic ? k_field_fused<true> : k_field_fused<false>, kMbThreads, pad);
+  return (int64_t)per * sms >= grid ? pad : -1;
 }
 
 // E from phi, then zero bin sets whose density has been taken (the serial
@@ -1011,9 +1037,11 @@ extern "C" int pb_field_cycle(const uint64_t *bins, const double *coef, int ndep
     a.two_dx = 2.0 * dx;
     a.st = status;
     a.cpt = cpt;
-    if (fl.G + cpt.nsp <= pb::field_fused_max_grid()) {  // one launch
+    const int pad = pb::field_fused_pad(fl.G + cpt.nsp, field_bc == PB_FIELD_PERIODIC);
+    if (pad >= 0) {  // one launch, every block co-resident, spread over the SMs
       cudaError_t err =
-          pb::launch_pdl(pb::k_field_fused, dim3(fl.G + cpt.nsp), dim3(pb::kMbThreads), 0, st, a);
+          pb::launch_pdl(field_bc == PB_FIELD_PERIODIC ? pb::k_field_fused<true> : pb::k_field_fused<false>,
+                         dim3(fl.G + cpt.nsp), dim3(pb::kMbThreads), (size_t)pad, st, a);
       if (err != cudaSuccess) return pb::cuda_status(err, "k_field_fused");
       return PB_OK;
     }
