@@ -61,7 +61,8 @@ def main():
     for it in range(30):
         b = bins.clone()
         _lib.check(lib.pb_field_cycle(P(b), c, ndep, nc, bc, 1, 1e-5, 8.85e-12, 0.0, 0.0, P(left), P(right),
-                                      P(rho), P(rho_s), P(phi), P(e), P(b), None, b.numel(), P(st), P(scr), sh),
+                                      P(rho), P(rho_s), P(phi), P(e), P(b), None, b.numel(), P(st), P(scr), None, 0,
+                                      None, 0, sh),
                    "pb_field_cycle")
         torch.cuda.synchronize()
         words = scr.view(torch.int64).cpu().numpy().view(np.uint64)
