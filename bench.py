@@ -194,20 +194,13 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def lib_digest() -> str:
-    """sha256 of the loaded libpicmc_b200.so (identifies the build)."""
-    import hashlib
-
+def build_traffic(workload, kernel):
+    """DRAM bytes per mover launch from an ncu --set full capture of THIS
+    kernel code (profiles/push_deposit_traffic.json records the sha256 of the
+    captured kernel's SASS next to the numbers); None when the capture is of
+    other code."""
     from paper_2404_10270_b200 import _lib
 
-    with open(_lib.LIB_PATH, "rb") as fh:
-        return hashlib.sha256(fh.read()).hexdigest()
-
-
-def build_traffic(workload):
-    """DRAM bytes per mover launch from an ncu --set full capture of THIS
-    build (profiles/push_deposit_traffic.json records the library's sha256
-    next to the numbers); None when the capture is of another build."""
     path = os.path.join(ROOT, "profiles", "push_deposit_traffic.json")
     try:
         with open(path) as fh:
@@ -217,9 +210,16 @@ def build_traffic(workload):
     ent = rec.get("workloads", {}).get(workload)
     if ent is None:
         return None, f"no capture for {workload}"
-    if rec.get("lib_sha256") != lib_digest():
-        return None, "capture is of another build"
-    return ent.get("dram_bytes_per_launch"), f"ncu --set full of this build ({rec.get('source', path)})"
+    short = ent.get("kernel", "").replace("void ", "").split("(")[0]
+    sym = _lib.MOVER_SYMBOLS.get(short)
+    if sym is None or not short.startswith(kernel):
+        return None, f"capture is of {short or 'another kernel'}, this launch ran {kernel}"
+    have = _lib.kernel_digest(sym)
+    if have is None:
+        return None, "cuobjdump unavailable: cannot tie the capture to this build"
+    if ent.get("kernel_sass_sha256") != have:
+        return None, "capture is of other kernel code"
+    return ent.get("dram_bytes_per_launch"), f"ncu --set full of this kernel code ({ent.get('source', path)})"
 
 
 # ---------------------------------------------------------------------------
@@ -474,7 +474,7 @@ def run_ours(args, rank, world, local_rank):
 
     peak, peak_kind = measured_peak()
     achieved = alg_bytes / (push_ms * 1e-3) / 1e9
-    traffic, traffic_src = build_traffic(args.workload)
+    traffic, traffic_src = build_traffic(args.workload, mover_kernel)
     # field-free: the mover + k_partials_clear + k_stitch (density epilogue);
     # field solve: the mover + k_field_fused (density, smoothing, Poisson, E
     # in one launch); walls: + k_compact

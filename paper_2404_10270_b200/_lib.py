@@ -233,3 +233,37 @@ def check(rc: int, what: str = ""):
     if rc in (PB_ERR_OVERFLOW, PB_ERR_PEER):
         raise EngineError(msg)
     raise RuntimeError(msg)
+
+
+
+# mangled names of the mover kernels whose DRAM traffic profiles/ records
+MOVER_SYMBOLS = {
+    "k_push_split<0>": "_ZN2pb12k_push_splitILi0EEEvNS_10LaunchArgsE",
+    "k_push_split<1>": "_ZN2pb12k_push_splitILi1EEEvNS_10LaunchArgsE",
+    "k_push_ring<0>": "_ZN2pb11k_push_ringILi0EEEvNS_10LaunchArgsE",
+    "k_push_ring<1>": "_ZN2pb11k_push_ringILi1EEEvNS_10LaunchArgsE",
+}
+
+
+def kernel_digest(symbol: str, path: str = None):
+    """sha256 of one kernel's sm_100a machine code in the library (its SASS
+    instruction lines from cuobjdump), or None when cuobjdump is missing or
+    the kernel is not found.  Unlike a digest of the whole file -- which
+    changes with the source mtimes that -lineinfo records -- it identifies the
+    code that ran, so an ncu capture stays attached to rebuilds of the same
+    sources and detaches when the kernel changes."""
+    import hashlib
+    import re
+    import shutil
+    import subprocess
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        return None
+    try:
+        out = subprocess.run([tool, "-sass", "-fun", symbol, path or LIB_PATH], capture_output=True,
+                             text=True, timeout=120).stdout
+    except (OSError, subprocess.SubprocessError):
+        return None
+    lines = [ln.strip() for ln in out.splitlines() if re.match(r"^\s+/\*[0-9a-f]{4}\*/", ln)]
+    return hashlib.sha256("\n".join(lines).encode()).hexdigest() if lines else None

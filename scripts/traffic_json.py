@@ -1,6 +1,8 @@
 """Write profiles/push_deposit_traffic.json from ncu --set full captures of
-the mover kernel, one per workload, tagged with the sha256 of the library
-that was captured (bench.py reports `roofline.traffic` only for that build).
+the mover kernel, one per workload, each tagged with the sha256 of that
+kernel's machine code in the library that was captured (_lib.kernel_digest;
+bench.py reports `roofline.traffic` only while the loaded library's kernel
+has the same code -- any rebuild of the same sources does).
 
   python scripts/traffic_json.py c2=gpurun_out/mover_c2.ncu-rep c3=gpurun_out/mover_c3.ncu-rep ...
 """
@@ -48,7 +50,10 @@ def main():
     wl = {}
     for arg in sys.argv[1:]:
         name, path = arg.split("=", 1)
-        wl[name] = read_rep(path)
+        rec = read_rep(path)
+        short = rec["kernel"].replace("void ", "").split("(")[0]
+        rec["kernel_sass_sha256"] = _lib.kernel_digest(_lib.MOVER_SYMBOLS[short])
+        wl[name] = rec
     out = {"lib_sha256": sha, "workloads": wl,
            "source": "ncu --set full --clock-control none (cold cache, one launch per workload)"}
     with open(os.path.join(ROOT, "profiles", "push_deposit_traffic.json"), "w") as fh:
