@@ -631,9 +631,27 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
           (k) == 0 ? (uint64_t)sm : ck;                              \
     }                                                                \
   } while (0)
+__device__ unsigned long long g_flog[512][2];  // per launch: CTA 0 start (past the wait), CTA 0 end
+__device__ unsigned long long g_flog_n;
+#define FF_LOG(k)                                                              \
+  do {                                                                         \
+    if (threadIdx.x == 0 && blockIdx.x == 0) {                                 \
+      uint64_t ns;                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));                   \
+      if ((k) == 0) {                                                          \
+        g_flog[g_flog_n % 512][0] = ns;                                        \
+      } else {                                                                 \
+        g_flog[g_flog_n % 512][1] = ns;                                        \
+        g_flog_n++;                                                            \
+      }                                                                        \
+    }                                                                          \
+  } while (0)
 #else
 #define FF_MARK(k) \
   do {             \
+  } while (0)
+#define FF_LOG(k) \
+  do {            \
   } while (0)
 #endif
 
@@ -672,6 +690,7 @@ __global__ void __launch_bounds__(kMbThreads) k_field_fused(const __grid_constan
     return;
   }
   FF_MARK(0);
+  FF_LOG(0);
   const int64_t nc = sa.nc, base = (int64_t)t * kMbTile;
   const int64_t kend = base + kMbTile < sa.n ? base + kMbTile : sa.n;
   const bool periodic = sa.field_bc == PB_FIELD_PERIODIC;
@@ -751,6 +770,7 @@ __global__ void __launch_bounds__(kMbThreads) k_field_fused(const __grid_constan
   // the last CTA out (every CTA is past its wait) re-arms the counters
   __syncthreads();
   FF_MARK(7);
+  FF_LOG(7);
   if (threadIdx.x == 0 &&
       atomicAdd((unsigned long long *)&a.sync[1], 1ull) == (unsigned long long)(G + a.cpt.nsp - 1)) {
     a.sync[0] = 0;
@@ -1063,3 +1083,12 @@ extern "C" int pb_field_cycle(const uint64_t *bins, const double *coef, int ndep
     rc = pb_compact(compact_sp, compact_nsp, status, compact_scratch, compact_scratch_bytes, stream);
   return rc;
 }
+
+#ifdef PB_FF_TRACE
+// debug: the field-step launch log (CTA 0 past its wait, CTA 0 end) and its count
+extern "C" int pb_debug_field_log(unsigned long long *out, unsigned long long *count) {
+  if (cudaMemcpyFromSymbol(out, pb::g_flog, sizeof(pb::g_flog)) != cudaSuccess) return PB_ERR_CUDA;
+  return cudaMemcpyFromSymbol(count, pb::g_flog_n, sizeof(unsigned long long)) == cudaSuccess ? PB_OK
+                                                                                            : PB_ERR_CUDA;
+}
+#endif

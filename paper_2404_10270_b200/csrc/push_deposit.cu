@@ -465,6 +465,8 @@ __device__ __forceinline__ unsigned long long global_ns() {
 #ifdef PB_MOVER_TRACE
 __device__ unsigned long long g_blk_start[2048];
 __device__ unsigned long long g_warp_end[8192];
+__device__ unsigned long long g_mlog[512][2];  // per launch: first block start, last warp end
+__device__ unsigned long long g_mlog_n;
 #endif
 __device__ __forceinline__ void mover_clock_start(pb_status *st) {
   if (threadIdx.x == 0) {
@@ -491,6 +493,13 @@ __device__ __forceinline__ void release_work_counter(pb_status *st, unsigned lon
     // ...and the last claimer to finish closes the launch's interval
     const unsigned long long t1 = global_ns();
     const unsigned long long t0 = atomicExch((unsigned long long *)&st->mover_t0, ~0ull);
+#ifdef PB_MOVER_TRACE
+    {
+      const unsigned long long k = atomicAdd(&g_mlog_n, 1ull) % 512;
+      g_mlog[k][0] = t0;
+      g_mlog[k][1] = t1;
+    }
+#endif
     if (t0 != ~0ull && t1 > t0) {
       atomicAdd((unsigned long long *)&st->mover_ns, t1 - t0);
       atomicAdd((unsigned long long *)&st->mover_launches, 1ull);
@@ -1612,5 +1621,11 @@ extern "C" int pb_debug_warp_ends(unsigned long long *out, int n, unsigned long 
   return cudaMemcpyFromSymbol(starts, pb::g_blk_start, (size_t)nb * sizeof(unsigned long long)) == cudaSuccess
              ? PB_OK
              : PB_ERR_CUDA;
+}
+// debug: the mover launch log (first block start, last warp end) and its count
+extern "C" int pb_debug_mover_log(unsigned long long *out, unsigned long long *count) {
+  if (cudaMemcpyFromSymbol(out, pb::g_mlog, sizeof(pb::g_mlog)) != cudaSuccess) return PB_ERR_CUDA;
+  return cudaMemcpyFromSymbol(count, pb::g_mlog_n, sizeof(unsigned long long)) == cudaSuccess ? PB_OK
+                                                                                            : PB_ERR_CUDA;
 }
 #endif
