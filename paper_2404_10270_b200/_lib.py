@@ -265,5 +265,5 @@ def kernel_digest(symbol: str, path: str = None):
                              text=True, timeout=120).stdout
     except (OSError, subprocess.SubprocessError):
         return None
-    lines = [ln.strip() for ln in out.splitlines() if re.match(r"^\s+/\*[0-9a-f]{4}\*/", ln)]
+    lines = [ln.strip() for ln in out.splitlines() if re.match(r"^\s+/\*[0-9a-f]{4,}\*/", ln)]
     return hashlib.sha256("\n".join(lines).encode()).hexdigest() if lines else None
