@@ -714,6 +714,15 @@ __global__ void __launch_bounds__(kMbThreads) k_field_fused(const __grid_constan
   }
   __syncthreads();
   FF_MARK(3);
+  // every CTA has read its bins (it arrived after reading them), so the bins
+  // are cleared here: the stores drain while the prefix, solve and E phases
+  // wait on L2 round trips, instead of after E on the way to the mover
+  if (a.nwords > 0) {
+    for (int64_t w = (int64_t)t * kMbThreads + threadIdx.x; w < a.nwords; w += (int64_t)G * kMbThreads) {
+      if (a.clr_a) a.clr_a[w] = 0;
+      if (a.clr_b) a.clr_b[w] = 0;
+    }
+  }
 
   Agg pre[4];
   {  // the tile prefixes this tile needs, formed by their owner threads
@@ -758,14 +767,6 @@ __global__ void __launch_bounds__(kMbThreads) k_field_fused(const __grid_constan
 #if PB_FF_LATE_TRIGGER
   pdl_trigger();
 #endif
-
-  // every CTA has read its bins (it published after reading them)
-  if (a.nwords > 0) {
-    for (int64_t w = (int64_t)t * kMbThreads + threadIdx.x; w < a.nwords; w += (int64_t)G * kMbThreads) {
-      if (a.clr_a) a.clr_a[w] = 0;
-      if (a.clr_b) a.clr_b[w] = 0;
-    }
-  }
 
   // the last CTA out (every CTA is past its wait) re-arms the counters
   __syncthreads();
