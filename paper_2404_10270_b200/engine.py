@@ -584,9 +584,12 @@ class Engine:
                                        self.compact_scratch.numel(), self._sh()), "pb_compact")
         self._holes_pending = False
 
-    def _field_cycle(self, rho_out=None):
+    def _field_cycle(self, rho_out=None, before_push=None):
         """Field-solve step body.  rho_out: see _fused_cycle (honoured on the
-        single-launch path only; check the returned tensor).  The species that need no field (neutral
+        single-launch path only; check the returned tensor).  before_push:
+        called between the field launch and the push (single-launch path;
+        run_pipelined snapshots the previous step's live counts there, once
+        the launch has folded that step's compaction in).  The species that need no field (neutral
         movers) are pushed on the engine stream while the density epilogue
         (and across GPUs its allreduce), smoothing, Poisson and E run on the
         side stream; the charged push then waits for E.  Without neutral
@@ -607,6 +610,8 @@ class Engine:
                 e = self.field(rho)
             if self.cfg.smoothing_passes > 0:
                 rho = self.rho_s
+            if before_push is not None:
+                before_push()
             self.push(e)
             return rho, e
         self._side.wait_stream(self.stream)
@@ -891,6 +896,12 @@ class Engine:
         start = self.cur
         overlap = not self.cfg.field_solve
         P = self._pipe
+        # absorbing walls with the compaction folded into the field launch:
+        # step j's holes are filled by step j+1's field launch, so step j's
+        # live counts are snapshotted right after it (before push j+1) and
+        # only the block's last step compacts on its own
+        fold = (self.absorbing and not overlap and self._folds_compaction() and self._fused_ok()
+                and not self._field_split()[0])
         with torch.cuda.graph(g, stream=self.stream):
             prev = None
             for j in range(n):
@@ -906,10 +917,12 @@ class Engine:
                 else:
                     # the single-launch field step writes the reported density
                     # straight into the result slot
-                    rho, e = self._field_cycle(rho_out=P["snap"][gp, j])
-                if self.absorbing:
-                    self._compact()
-                self._snap_counts(gp, j)
+                    hook = (lambda jj=j - 1: self._snap_counts(gp, jj)) if fold and j > 0 else None
+                    rho, e = self._field_cycle(rho_out=P["snap"][gp, j], before_push=hook)
+                if not fold or j == n - 1:
+                    if self.absorbing:
+                        self._compact()
+                    self._snap_counts(gp, j)
                 if rho.data_ptr() != P["snap"][gp, j].data_ptr():
                     if overlap:
                         snap_stream = self._side  # rho_j is final once epilogue j is done

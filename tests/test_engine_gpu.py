@@ -488,7 +488,7 @@ def test_prepare_pipe_graphs_covers_run(cuda, with_input):
         assert bits_equal(got[k], rho.cpu().numpy()), k
 
 
-@pytest.mark.parametrize("group", [1, 3])
+@pytest.mark.parametrize("group", [1, 3, 4])
 def test_run_pipelined_field_solve_absorbing(cuda, group):
     """Field-solve + absorbing walls + cell sorts through the pipelined loop
     (graphs of `group` steps, serial density -> Poisson -> E -> push ->
@@ -504,14 +504,17 @@ def test_run_pipelined_field_solve_absorbing(cuda, group):
     a.upload(flats)
     b.upload(flats)
     steps = 14
-    want = []
+    want, want_n = [], []
     for _ in range(steps):
         rho, _ = a.step()
         want.append(rho.cpu().numpy().copy())
-    got = {}
-    b.run_pipelined(steps, group=group, on_result=lambda k, r: got.__setitem__(k, r.numpy().copy()))
+        want_n.append([int(v) for v in a.totals()])  # live counts after the step's compaction
+    got, got_n = {}, {}
+    b.run_pipelined(steps, group=group, on_result=lambda k, r: got.__setitem__(k, r.numpy().copy()),
+                    on_counts=lambda k, c: got_n.__setitem__(k, [int(v) for v in c]))
     for k in range(steps):
         assert bits_equal(got[k], want[k]), k
+        assert got_n[k] == want_n[k], (k, got_n[k], want_n[k])
     a.sync()
     b.sync()
     assert np.array_equal(a.absorbed, b.absorbed) and a.absorbed.sum() > 0
