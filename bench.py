@@ -470,6 +470,7 @@ def run_ours(args, rank, world, local_rank):
     rs_pushes = sum(sum(r[f"total_{n}"] for n, sp in zip(names, cfg.species) if sp.active_mover)
                     for r in m.diagnostics[:-1])
     (rs_total,) = max_over_ranks(m.phase_seconds["total"])
+    (rs_device,) = max_over_ranks(m.phase_seconds["mover"])  # engine-stream events around the loop
     rs_value = rs_pushes / rs_total
 
     peak, peak_kind = measured_peak()
@@ -526,6 +527,7 @@ def run_ours(args, rank, world, local_rank):
         "e2e_run_simulation": {
             "value": rs_value, "unit": "particle-pushes/s", "steps": e2e_steps,
             "vs_run_pipelined": rs_value / e2e_value,
+            "wall_s": rs_total, "device_s": rs_device,
             "path": "paper_2404_10270_b200.run_simulation(config) (the picmc.run_simulation signature), "
                     "on_step=None: graph replay, status every CHECK_EVERY steps; pushes / phase_seconds"
                     "['total']"},
