@@ -113,6 +113,13 @@ def _run_graphed(engine, config, names):
     counts snapshotted on device; otherwise the totals are invariant).
     Returns (diagnostics rows 1..n, phase seconds)."""
     n = int(config.n_steps)
+    if any(engine.sort_periods):
+        # init, not the step loop, pays for the sort path's first use: CUDA
+        # loads kernels lazily (its first launch inside the loop stalled the
+        # engine stream by 3-150 ms, profiles/r02_run_simulation_spread.txt)
+        # and the scratch is allocated here; a cell sort is a no-op for the
+        # physics (the cycle's own sorts reorder slots the same way)
+        engine.sort_by_cell()
     engine.prepare_pipe_graphs(with_input=False, horizon=n)
     tot0 = _global_totals(engine)
     counts = np.zeros((n, len(names)), dtype=np.int64) if engine.absorbing else None
